@@ -1,0 +1,132 @@
+// Internal engine state shared by the engine, model and sampler translation units.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <chrono>
+#include <string>
+#include <vector>
+
+#include "common.cuh"
+
+namespace ab {
+
+// Device control block: one per engine, lives in device memory; copied to a
+// pinned mirror at the host's polling points.
+struct Ctl {
+  int32_t b;                  // active slots (the live batch)
+  int32_t stop;               // nonzero: every iteration kernel is a no-op
+  int32_t stop_reason;        // AB_RUN_* or -1
+  int32_t error;              // contract error code (see kErr*)
+  int32_t error_handle;
+  int32_t q_head, q_tail;     // FIFO ring indices (monotonic; slot = idx % Q)
+  int32_t n_events, n_admits; // logged in the current run
+  int32_t use_trigger, trigger_mode, stop_on_event, n_target, group_size;
+  int32_t iters_to_next;      // trace mode: iterations until the next finish (-1 unknown)
+  int32_t new_groups;         // scratch: groups completed in this iteration
+  int64_t version;
+  int64_t iteration_index, cumulative_tokens;
+  int64_t run_iters, max_iters;
+  int64_t completed_groups, completed_samples;
+  int64_t kv_free_top;        // transformer: free-page stack top
+  int64_t kv_fail;            // transformer: allocation failures
+  uint64_t clock_ns;          // scratch for clock reads
+};
+
+enum : int32_t { kErrNone = 0, kErrVersion = 1, kErrAtStop = 2, kErrNoTarget = 3, kErrOutOfKV = 4 };
+
+struct Model;  // transformer (model.cu)
+
+// POD view passed by value to kernels.
+struct EngineDev {
+  Ctl* ctl;
+  int S, Q, H, L, G_cap;
+  int stop_mode, model_kind, n_symbols, l_max, record;
+  int n_eos;
+  int eos[8];
+  int32_t* slot_handle;
+  int32_t* slot_tmp;
+  int32_t* slot_finish;  // reason+1, 0 = continues
+  int32_t* slot_token;   // token sampled this iteration
+  int32_t* q_buf;
+  int32_t* h_gen;
+  int32_t* h_stop;
+  int32_t* h_group;
+  ulonglong2* h_key;
+  int64_t* h_version;
+  int32_t* h_tokens;  // [H * L]
+  double* h_logp;     // [H * L]
+  int32_t* g_done;
+  ab_event* ev;
+  ab_admit* adm;
+  double* cf_logits;  // [n_symbols]
+  double* cf_cdf;
+  double* cf_logp;
+  int32_t* it_b;       // per run iteration: live batch (profiling / roofline)
+  int64_t* it_ctx;     // per run iteration: sum of context lengths
+  int it_cap;
+  uint64_t t0_ns;
+};
+
+struct KernelTimer {
+  std::string name;
+  int64_t launches = 0;
+  double ms = 0, bytes = 0, flops = 0;
+};
+
+struct Engine {
+  ab_engine_config cfg{};
+  ab_model_config mcfg{};
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  EngineDev d{};
+  Ctl* ctl_host = nullptr;  // pinned mirror
+  uint64_t* clock_host = nullptr;
+  Model* model = nullptr;
+  ab_sample_desc* stage_desc_host = nullptr;
+  ab_sample_desc* stage_desc_dev = nullptr;
+  int32_t* stage_i32_dev = nullptr;
+  int32_t* stage_i32_host = nullptr;
+  size_t stage_i32_cap = 0;
+  int64_t prefill_tokens = 0;
+  // profiling
+  bool profile = false;
+  int sample_every = 8;
+  std::vector<KernelTimer> timers;
+  struct PendingTime {
+    int timer;
+    cudaEvent_t a, b;
+    int64_t run_iter;  // -1: bytes known at launch
+    double bytes, flops;
+  };
+  std::vector<PendingTime> pending;
+  std::vector<cudaEvent_t> event_pool;
+
+  cudaEvent_t take_event();
+  int timer_index(const char* name);
+};
+
+// model.cu
+Model* model_create(Engine& e);
+void model_destroy(Model* m);
+int model_weight_count(Model* m);
+void model_weight_info(Model* m, int idx, std::string* name, int64_t* rows, int64_t* cols, void** dev_ptr);
+void model_open_group(Engine& e, int group_slot, const int32_t* prompt, int prompt_len);
+void model_release_group(Engine& e, int group_slot);
+void model_submit(Engine& e, const ab_sample_desc* descs_dev, int n);  // after per-handle state is set
+void model_release(Engine& e, const int32_t* handles_dev, int n);
+void model_iteration(Engine& e, int64_t run_iter, bool timed);         // pages + forward + sampler
+int64_t model_pages_total(Model* m);
+
+// profiling helper (engine.cu)
+struct ScopedTimer {
+  Engine& e;
+  int idx;
+  cudaEvent_t a = nullptr;
+  double bytes, flops;
+  int64_t run_iter;
+  ScopedTimer(Engine& eng, bool on, const char* name, int64_t run_iter_, double bytes_ = 0, double flops_ = 0);
+  ~ScopedTimer();
+};
+
+}  // namespace ab
