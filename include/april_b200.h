@@ -193,6 +193,9 @@ int ab_engine_synchronize(ab_engine* e);
 int ab_group_advantages(const double* rewards, int n_groups, int group_size, int mode, double eps, double* adv,
                         int32_t* zero_std_flags, int device);
 
+/* Test entry points (device pointers; used by tests/test_kernels_gpu.py). */
+int ab_debug_gemm(const void* W, const void* A, void* out, const void* bias, int N, int K, int M, int BN, int epi);
+
 #ifdef __cplusplus
 }
 #endif

@@ -113,6 +113,7 @@ _SIGS = {
     "ab_engine_kernel_stats": [P, C.POINTER(KernelStat), C.c_int, C.POINTER(C.c_int)],
     "ab_engine_synchronize": [P],
     "ab_group_advantages": [F64P, C.c_int, C.c_int, C.c_int, C.c_double, F64P, I32P, C.c_int],
+    "ab_debug_gemm": [P, P, P, P, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int],
 }
 EXPORTS = sorted(_SIGS) + ["ab_last_error", "ab_version"]
 

@@ -1,0 +1,53 @@
+"""Kernel numerics against plain PyTorch fp32 references of the same op."""
+
+import ctypes as C
+
+import pytest
+
+torch = pytest.importorskip("torch")
+
+from paper_2509_18521_b200 import _capi  # noqa: E402
+
+pytestmark = pytest.mark.gpu
+
+
+def _ptr(t):
+    return C.c_void_p(t.data_ptr()) if t is not None else None
+
+
+@pytest.mark.parametrize("bn", [32, 64, 128, 256])
+@pytest.mark.parametrize("shape", [(256, 128, 1), (512, 1536, 37), (2048, 1536, 300), (384, 256, 1000)])
+@pytest.mark.parametrize("epi", [0, 1, 2])
+def test_tcgen05_gemm_matches_torch(bn, shape, epi):
+    N, K, M = shape
+    g = torch.Generator(device="cuda").manual_seed(N * 7 + K + M)
+    W = (torch.randn(N, K, device="cuda", generator=g) * 0.05).to(torch.bfloat16)
+    A = (torch.randn(M, K, device="cuda", generator=g)).to(torch.bfloat16)
+    bias = (torch.randn(N, device="cuda", generator=g) * 0.1).to(torch.bfloat16) if epi == 0 else None
+    ref = A.float() @ W.float().t()
+    if epi == 0:
+        out = torch.empty(M, N, device="cuda", dtype=torch.bfloat16)
+        ref = ref + bias.float()
+    elif epi == 1:
+        out = torch.empty(M, N, device="cuda", dtype=torch.float32)
+    else:
+        base = torch.randn(M, N, device="cuda", generator=g)
+        out = base.clone()
+        ref = ref + base
+    _capi.call("ab_debug_gemm", _ptr(W), _ptr(A), _ptr(out), _ptr(bias), N, K, M, bn, epi)
+    torch.cuda.synchronize()
+    tol = 2e-2 if epi == 0 else 2e-3
+    torch.testing.assert_close(out.float(), ref, rtol=tol, atol=tol * max(1.0, ref.abs().max().item() * 0.01))
+
+
+def test_tcgen05_gemm_swiglu_epilogue():
+    N, K, M = 512, 256, 77  # N = 2 * features, rows interleaved in 64-row halves per 128-row tile
+    g = torch.Generator(device="cuda").manual_seed(5)
+    W = (torch.randn(N, K, device="cuda", generator=g) * 0.05).to(torch.bfloat16)
+    A = torch.randn(M, K, device="cuda", generator=g).to(torch.bfloat16)
+    out = torch.empty(M, N // 2, device="cuda", dtype=torch.bfloat16)
+    _capi.call("ab_debug_gemm", _ptr(W), _ptr(A), _ptr(out), None, N, K, M, 64, 3)
+    acc = A.float() @ W.float().t()
+    t = acc.view(M, N // 128, 2, 64)
+    ref = (torch.nn.functional.silu(t[:, :, 0]) * t[:, :, 1]).reshape(M, N // 2)
+    torch.testing.assert_close(out.float(), ref, rtol=2e-2, atol=2e-2)
