@@ -1,0 +1,346 @@
+#!/usr/bin/env python
+"""APRIL rollout benchmark on B200 (BASELINE.json metric).
+
+Workload (SURVEY.md §8d, config C2 = BASELINE.json configs[1]):
+  Qwen2.5-1.5B-shape random-init bf16 decoder, GRPO rollout, 64 prompts x n=8,
+  over-provisioned to 128 groups (2x), max_len 4096, log-normal(6.6, 1.0)
+  response lengths (rho 0.7) replayed as a length trace, 256-token synthetic
+  prompts, temperature 0.8, S = 1024 decode slots, one B200.
+
+A "step" is one RL rollout step of the scheduler: begin_step -> resume/open
+groups -> (prefill) -> fused decode until N whole groups are complete ->
+abort/park.  `value` is APRIL generated tokens/s with the step time measured
+on the device clock (payload kept on the GPU); `e2e` runs the same steps
+through the public API with the finished-response gather (token ids +
+behaviour log-probs copied to host lists), synthetic rewards and the GPU
+advantage kernel, timed by the host wall clock.  The synchronous baseline
+(no over-provisioning, no recycling) runs on the same engine code, same
+trace, afterwards.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl reference]
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "rollout tokens/s & RL-step rollout time, APRIL vs sync, long-tail lengths, 1–8 B200"
+
+WORKLOADS = {
+    "C2": dict(model="qwen2.5-1.5b", n=64, g=8, n_prime=128, slots=1024, l_max=4096, mu=6.6, sigma=1.0, rho=0.7,
+               prompt=256, temperature=0.8, adv="mean_std_baseline", page=64),
+    # small smoke workload (tiny decoder) for quick checks
+    "C1": dict(model="tiny", n=8, g=4, n_prime=16, slots=64, l_max=1024, mu=5.5, sigma=1.0, rho=0.7, prompt=32,
+               temperature=0.8, adv="mean_std_baseline", page=16),
+}
+
+
+def _peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), float(p["bf16_tflops"]), "measured"
+    except Exception:
+        return 6650.0, 1590.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons sampled during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device: int):
+        self.device = device
+        self.rows: list[list[str]] = []
+        self._stop = threading.Event()
+        self._t = threading.Thread(target=self._run, daemon=True)
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.Q}",
+                                      "--format=csv,noheader,nounits"], capture_output=True, text=True, timeout=5)
+                for line in out.stdout.strip().splitlines():
+                    self.rows.append([x.strip() for x in line.split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        self._t.join(timeout=10)
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        smax = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4) if len(r) > 3 + i and "Active" in r[3 + i]})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(smax) if smax else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+def build_engine(pb, w, device, seed, record=True):
+    spec = pb.PRESETS[w["model"]]
+    eng = pb.LengthDrivenEngine(
+        pb.EngineConfig(max_slots=w["slots"], l_max=w["l_max"]), global_seed=seed, model=spec,
+        sampling=pb.SamplingConfig(temperature=w["temperature"]), prompt_len=w["prompt"], page_size=w["page"],
+        device=device, record_payload=record, max_handles=max(4096, 4 * w["n_prime"] * w["g"]),
+        max_groups=4 * w["n_prime"] + 64)
+    return spec, eng
+
+
+def make_scheduler(pb, w, eng, mode, seed):
+    cfg = pb.SchedulerConfig(rollout_batch_size=w["n"], samples_per_prompt=w["g"],
+                             over_sampling_batch_size=w["n_prime"] if mode == "april" else w["n"], mode=mode)
+    dist = pb.LengthDistribution.lognormal(w["mu"], w["sigma"], w["l_max"])
+    return pb.Scheduler(cfg, eng, pb.InstanceSource(group_size=w["g"]), pb.LengthSampler(dist, w["rho"], seed))
+
+
+def learner_glue(pb, w, out, target_token=0):
+    """Synthetic GRPO glue (simulate.py:47-65): target-token-fraction rewards on the
+    delivered token ids, then the K6 advantage kernel over contiguous groups."""
+    samples = out.batch_samples()
+    rewards = []
+    for s in samples:
+        toks = s.token_ids()
+        rewards.append(sum(1 for t in toks if t % 4 == target_token) / len(toks) if toks else 0.0)
+    return pb.batch_advantages(rewards, w["g"], w["adv"])
+
+
+def run_steps(pb, w, sched, eng, k0, n, timed_e2e=False):
+    recs = []
+    for k in range(k0, k0 + n):
+        h2d0 = eng.io_bytes()
+        t0 = time.perf_counter()
+        out = sched.run_step(k)
+        if timed_e2e:
+            learner_glue(pb, w, out)
+        t1 = time.perf_counter()
+        h2d1 = eng.io_bytes()
+        recs.append(dict(step=k, tokens=out.tokens_generated, wall=out.rollout_wall_time, host=t1 - t0,
+                         iters=out.iterations, carried=out.carried_in_tokens,
+                         h2d=h2d1[0] - h2d0[0], d2h=h2d1[1] - h2d0[1], buffer=out.buffer_size_after))
+    return recs
+
+
+def cpu_baseline(w, budget_s=15.0):
+    import torch
+
+    import paper_2509_18521_b200 as pb
+    from oracle.cpu_model import CpuDecoder, random_weights
+
+    spec = pb.PRESETS[w["model"]]
+    dec = CpuDecoder(spec, random_weights(spec, 0))
+    batch, ctx = 64, 1024
+    probe = dec.decode_batch_rate(batch, ctx, 1)
+    iters = max(1, min(64, int(budget_s / max(probe["seconds"], 1e-3))))
+    r = dec.decode_batch_rate(batch, ctx, iters)
+    return {"value": r["tokens_per_s"], "unit": "tokens/s", "cores": torch.get_num_threads(), "kind": "port",
+            "sample": f"oracle/cpu_model.py fp32 {spec.name} full depth, {iters} decode iterations x batch {batch} "
+                      f"at context {ctx} ({r['seconds']:.1f} s)"}
+
+
+def reference_arm(args):
+    """--impl reference: the reference algorithm's CPU implementation (oracle port:
+    the scheduler/engine restatement oracle/sim_ref.py plus the fp32 decoder oracle/cpu_model.py)
+    on the host cores; each step is a bounded sample of the C2 rollout."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    import torch
+
+    import paper_2509_18521_b200 as pb
+    from oracle import sim_ref
+    from oracle.cpu_model import CpuDecoder, random_weights
+
+    w = WORKLOADS[args.workload]
+    spec = pb.PRESETS[w["model"]]
+    dec = CpuDecoder(spec, random_weights(spec, 0))
+    batch, ctx = 64, 1024
+    probe = dec.decode_batch_rate(batch, ctx, 1)
+    iters = max(1, min(32, int(args.ref_step_s / max(probe["seconds"], 1e-3))))
+    # the scheduling half of the reference path, same trace (APRIL step of the CPU simulator)
+    eng = sim_ref.OracleEngine(0.05, 0.002, w["slots"], w["l_max"])
+    sch = sim_ref.OracleScheduler(w["n"], w["g"], w["n_prime"], eng,
+                                  dist=sim_ref.TraceDist("lognormal", w["l_max"], w["mu"], w["sigma"]), rho=w["rho"])
+    rates, times = [], []
+    for k in range(args.warmup + args.steps):
+        t0 = time.perf_counter()
+        sch.run_step(k)
+        r = dec.decode_batch_rate(batch, ctx + 8 * k, iters, seed=k)
+        dt = time.perf_counter() - t0
+        if k >= args.warmup:
+            rates.append(r["tokens"] / dt)
+            times.append(dt)
+    v = statistics.mean(rates)
+    line = {"impl": "reference", "metric": METRIC, "value": v, "unit": "tokens/s", "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * statistics.mean(times),
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "config": {"workload": args.workload, "shape": spec.name, "prompts": w["n"],
+                       "samples_per_prompt": w["g"], "over_provision": w["n_prime"] / w["n"],
+                       "max_len": w["l_max"]},
+            "cpu_baseline": {"value": v, "unit": "tokens/s", "cores": torch.get_num_threads(), "kind": "port",
+                             "sample": f"per step: one APRIL scheduling step of oracle/sim_ref.py + {iters} fp32 "
+                                       f"decode iterations x batch {batch} of the full-depth {spec.name} decoder "
+                                       f"(oracle/cpu_model.py) at context ~{ctx}"},
+            "e2e": {"value": v, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line))
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=4)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--workload", default="C2", choices=sorted(WORKLOADS))
+    ap.add_argument("--sync-steps", type=int, default=2)
+    ap.add_argument("--no-sync", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--profile-every", type=int, default=8)
+    ap.add_argument("--ref-step-s", type=float, default=12.0)
+    ap.add_argument("--seed", type=int, default=0)
+    args = ap.parse_args()
+    if args.impl == "reference":
+        return reference_arm(args)
+
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    dist = None
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl")
+    import paper_2509_18521_b200 as pb
+
+    w = WORKLOADS[args.workload]
+    seed = args.seed + rank  # replicas: independent prompt streams per rank
+    hbm_peak, tf_peak, peak_kind = _peaks()
+
+    spec, eng = build_engine(pb, w, local, seed, record=True)
+    sched = make_scheduler(pb, w, eng, "april", seed)
+    run_steps(pb, w, sched, eng, 0, args.warmup)
+    if dist:
+        dist.barrier()
+    eng.profile(True, args.profile_every)
+    launches0 = eng.stats().kernel_launches
+    with ClockSampler(local) as clk:
+        t0 = time.perf_counter()
+        rec = run_steps(pb, w, sched, eng, args.warmup, args.steps)
+        t_dev = sum(r["wall"] for r in rec)
+        if dist:
+            import torch
+
+            tt = torch.tensor([t_dev], device="cuda")
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+            t_dev = float(tt)
+        t_host = time.perf_counter() - t0
+    launches = eng.stats().kernel_launches - launches0
+    kstats = {k["name"]: k for k in eng.kernel_stats()}
+    eng.profile(False)
+    tokens = sum(r["tokens"] for r in rec)
+    # e2e: same steps, payload gathered to host + rewards + advantages, host wall clock
+    rec_e2e = run_steps(pb, w, sched, eng, args.warmup + args.steps, args.steps, timed_e2e=True)
+    e2e_tps = sum(r["tokens"] for r in rec_e2e) / sum(r["host"] for r in rec_e2e)
+    stats = eng.stats()
+    eng.close()
+    del eng, sched
+
+    sync = None
+    if not args.no_sync:
+        _, eng_s = build_engine(pb, w, local, seed, record=True)
+        sch_s = make_scheduler(pb, w, eng_s, "baseline", seed)
+        rs = run_steps(pb, w, sch_s, eng_s, 0, args.sync_steps)
+        sync = {"tokens_per_s": sum(r["tokens"] for r in rs) / sum(r["wall"] for r in rs),
+                "ms_per_step": 1e3 * statistics.mean(r["wall"] for r in rs), "steps": len(rs),
+                "iterations_per_step": statistics.mean(r["iters"] for r in rs)}
+        eng_s.close()
+
+    total_tokens = tokens * world
+    value = total_tokens / t_dev if t_dev > 0 else 0.0
+    att = kstats.get("attention")
+    roof = None
+    if att and att["ms"] > 0:
+        ach = att["bytes"] / (att["ms"] * 1e-3) / 1e9
+        roof = {"kernel": "paged GQA decode attention (k_decode_attn + combine)", "bound": "hbm",
+                "achieved": ach, "peak": hbm_peak, "unit": "GB/s", "frac": ach / hbm_peak,
+                "peak_kind": peak_kind, "traffic": _ncu_traffic(), "launches_timed": att["launches"],
+                "avg_launch_us": 1e3 * att["ms"] / att["launches"]}
+    kern = {}
+    tot_ms = sum(k["ms"] for k in kstats.values()) or 1.0
+    for name, k in sorted(kstats.items(), key=lambda kv: -kv[1]["ms"]):
+        ms = k["ms"]
+        kern[name] = {"share": ms / tot_ms, "avg_us": 1e3 * ms / max(k["launches"], 1),
+                      "GB/s": k["bytes"] / (ms * 1e-3) / 1e9 if ms else None,
+                      "TFLOP/s": k["flops"] / (ms * 1e-3) / 1e12 if ms and k["flops"] else None}
+    ms_step = 1e3 * t_dev / max(len(rec), 1)
+    line = {
+        "metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "bf16", "data": "synthetic (random-init weights, Philox prompts, replayed "
+                                                     "log-normal length trace)",
+        "config": {"workload": f"{args.workload}: {spec.name}-shape GRPO APRIL rollout", "prompts": w["n"],
+                   "samples_per_prompt": w["g"], "over_provision_groups": w["n_prime"], "max_len": w["l_max"],
+                   "length_dist": f"lognormal({w['mu']}, {w['sigma']}), rho {w['rho']}",
+                   "prompt_len": w["prompt"], "slots": w["slots"], "temperature": w["temperature"],
+                   "parallelism": f"dp{world} replicas", "l2": "inputs larger than L2 (weights + KV >> 126 MB)"},
+        "april": {"tokens_per_s": value, "ms_per_step": ms_step, "steps": len(rec),
+                  "iterations_per_step": statistics.mean(r["iters"] for r in rec),
+                  "carried_in_tokens_per_step": statistics.mean(r["carried"] for r in rec)},
+        "sync": sync,
+        "april_over_sync": (value / world / sync["tokens_per_s"]) if sync else None,
+        "roofline": roof, "kernels": kern,
+        "e2e": {"value": e2e_tps * world, "unit": "tokens/s",
+                "h2d_bytes_per_step": int(statistics.mean(r["h2d"] for r in rec_e2e)),
+                "d2h_bytes_per_step": int(statistics.mean(r["d2h"] for r in rec_e2e))},
+        "clocks": clk.summary(), "gpu_launches": int(launches),
+        "kv_pages": {"total": stats.kv_pages_total, "free_after": stats.kv_pages_free},
+        "host_seconds_timed": t_host,
+    }
+    if rank == 0 and world == 1 and not args.no_cpu:
+        try:
+            line["cpu_baseline"] = cpu_baseline(w)
+        except Exception as exc:  # the baseline is reported, not required
+            line["cpu_baseline"] = {"value": None, "error": repr(exc)[:200]}
+    if rank == 0:
+        print(json.dumps(line))
+    if dist:
+        dist.barrier()
+        dist.destroy_process_group()
+    return 0
+
+
+def _ncu_traffic():
+    """dram read+write bytes per launch of the attention kernel from the committed ncu capture."""
+    p = os.path.join(ROOT, "profiles", "attention_dram_bytes.json")
+    try:
+        with open(p) as f:
+            return json.load(f).get("bytes_per_launch")
+    except Exception:
+        return None
+
+
+if __name__ == "__main__":
+    sys.exit(main())

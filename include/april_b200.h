@@ -144,6 +144,7 @@ typedef struct ab_stats {
   double clock;        /* device wall seconds since engine creation         */
   int64_t kv_pages_total, kv_pages_free;
   int64_t prefill_tokens; /* prompt tokens prefilled (excluded from "generated") */
+  int64_t kernel_launches; /* kernels this engine has launched */
 } ab_stats;
 
 typedef struct ab_kernel_stat {

@@ -77,7 +77,7 @@ class RunResult(C.Structure):
 class Stats(C.Structure):
     _fields_ = [("iteration_index", C.c_int64), ("cumulative_tokens", C.c_int64), ("active", C.c_int32),
                 ("queued", C.c_int32), ("clock", C.c_double), ("kv_pages_total", C.c_int64),
-                ("kv_pages_free", C.c_int64), ("prefill_tokens", C.c_int64)]
+                ("kv_pages_free", C.c_int64), ("prefill_tokens", C.c_int64), ("kernel_launches", C.c_int64)]
 
 
 class KernelStat(C.Structure):

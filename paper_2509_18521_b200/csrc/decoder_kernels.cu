@@ -1,0 +1,721 @@
+// Decoder kernels around the tcgen05 GEMMs: weight init, embedding,
+// RMSNorm, q/k-norm + RoPE + paged KV write, paged GQA decode attention
+// (split-KV, mma.sync bf16 tiles staged by cp.async into swizzled smem),
+// causal prefill attention for prompt groups, and KV page management.
+//
+// None of this has a reference counterpart (the reference decode engine is a
+// cost model, src/april_sim/engine.py:167-171); numerics are pinned by the
+// torch-CPU oracle in oracle/cpu_model.py.
+#include <cuda_bf16.h>
+
+#include <cfloat>
+
+#include "model.cuh"
+
+namespace ab {
+
+namespace {
+
+constexpr float kLog2e = 1.4426950408889634f;
+
+__device__ __forceinline__ bool stopped(const int* stop) { return stop != nullptr && *stop != 0; }
+
+// ---------------------------------------------------------------------------
+// weights
+// ---------------------------------------------------------------------------
+
+__global__ void k_init_weights(bf16* w, size_t n, uint64_t k0, uint64_t k1, float std, float constant, int mode) {
+  for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) {
+    if (mode == 1) {
+      w[i] = __float2bfloat16(constant);
+      continue;
+    }
+    const uint64_t a = philox_word(k0, k1, 2 * i), b = philox_word(k0, k1, 2 * i + 1);
+    const double u1 = ((double)(a >> 11) + 1.0) * 0x1.0p-53;  // (0, 1]
+    const double u2 = (double)(b >> 11) * 0x1.0p-53;
+    const double z = sqrt(-2.0 * log(u1)) * cospi(2.0 * u2);
+    w[i] = __float2bfloat16((float)(z * std));
+  }
+}
+
+__global__ void k_rope_table(float2* rope, int max_pos, int hd, float theta) {
+  const int half = hd / 2;
+  for (int idx = blockIdx.x * blockDim.x + threadIdx.x; idx < max_pos * half; idx += gridDim.x * blockDim.x) {
+    const int p = idx / half, i = idx % half;
+    const float inv = 1.0f / powf(theta, (float)(2 * i) / (float)hd);
+    const float ang = (float)p * inv;
+    float s, c;
+    sincosf(ang, &s, &c);
+    rope[idx] = make_float2(c, s);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// per-iteration row preparation + KV page allocation
+// ---------------------------------------------------------------------------
+
+__device__ __forceinline__ int pop_page(Ctl* c) {
+  const long long old = (long long)atomicAdd(reinterpret_cast<unsigned long long*>(&c->kv_free_top),
+                                             (unsigned long long)(-1ll));
+  return old - 1 >= 0 ? (int)(old - 1) : -1;
+}
+
+__global__ void k_prep_decode(EngineDev e, ModelDev m) {
+  Ctl* c = e.ctl;
+  if (c->stop) return;
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= c->b) return;
+  const int h = e.slot_handle[i];
+  const int pos = m.h_ctx[h];
+  m.row_tok[i] = m.h_last_tok[h];
+  m.row_pos[i] = pos;
+  m.row_btrow[i] = h;
+  if (c->run_iters < e.it_cap)
+    atomicAdd(reinterpret_cast<unsigned long long*>(&e.it_ctx[c->run_iters]), (unsigned long long)(pos + 1));
+  if (pos % m.P == 0) {
+    const int idx = pop_page(c);
+    if (idx < 0 || pos / m.P >= m.MP) {
+      atomicCAS(&c->error, kErrNone, kErrOutOfKV);
+      c->stop = 1;
+      c->stop_reason = -2;
+      return;
+    }
+    m.bt[(size_t)h * m.MP + pos / m.P] = m.free_pages[idx];
+  }
+}
+
+// ---------------------------------------------------------------------------
+// embedding / RMSNorm
+// ---------------------------------------------------------------------------
+
+__global__ void k_embed(ModelDev m, const bf16* __restrict__ emb, float* __restrict__ x, const int* rows_dev,
+                        int rows_cap, const int* stop) {
+  if (stopped(stop)) return;
+  const int rows = rows_dev ? min(*rows_dev, rows_cap) : rows_cap;
+  const int r = blockIdx.x;
+  if (r >= rows) return;
+  const bf16* src = emb + (size_t)m.row_tok[r] * m.d;
+  float* dst = x + (size_t)r * m.d;
+  for (int j = threadIdx.x * 8; j < m.d; j += blockDim.x * 8) {
+    const uint4 v = *reinterpret_cast<const uint4*>(src + j);
+    const bf16* b = reinterpret_cast<const bf16*>(&v);
+    float4 lo = make_float4(__bfloat162float(b[0]), __bfloat162float(b[1]), __bfloat162float(b[2]),
+                            __bfloat162float(b[3]));
+    float4 hi = make_float4(__bfloat162float(b[4]), __bfloat162float(b[5]), __bfloat162float(b[6]),
+                            __bfloat162float(b[7]));
+    *reinterpret_cast<float4*>(dst + j) = lo;
+    *reinterpret_cast<float4*>(dst + j + 4) = hi;
+  }
+}
+
+// one warp per row: y = bf16(x * rsqrt(mean(x^2) + eps) * w)
+__global__ void k_rmsnorm(const float* __restrict__ x, const bf16* __restrict__ w, bf16* __restrict__ out, int d,
+                          float eps, const int* rows_dev, int rows_cap, const int* stop) {
+  if (stopped(stop)) return;
+  const int rows = rows_dev ? min(*rows_dev, rows_cap) : rows_cap;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int r = blockIdx.x * (blockDim.x >> 5) + warp;
+  if (r >= rows) return;
+  const float* xr = x + (size_t)r * d;
+  float ss = 0.f;
+  for (int j = lane * 4; j < d; j += 128) {
+    const float4 v = *reinterpret_cast<const float4*>(xr + j);
+    ss += v.x * v.x + v.y * v.y + v.z * v.z + v.w * v.w;
+  }
+  ss = warp_sum(ss);
+  const float rs = rsqrtf(ss / (float)d + eps);
+  bf16* o = out + (size_t)r * d;
+  for (int j = lane * 4; j < d; j += 128) {
+    const float4 v = *reinterpret_cast<const float4*>(xr + j);
+    o[j + 0] = __float2bfloat16(v.x * rs * __bfloat162float(w[j + 0]));
+    o[j + 1] = __float2bfloat16(v.y * rs * __bfloat162float(w[j + 1]));
+    o[j + 2] = __float2bfloat16(v.z * rs * __bfloat162float(w[j + 2]));
+    o[j + 3] = __float2bfloat16(v.w * rs * __bfloat162float(w[j + 3]));
+  }
+}
+
+// ---------------------------------------------------------------------------
+// q/k-norm + RoPE (rotate-half) + KV write into the row's page
+// ---------------------------------------------------------------------------
+
+template <int HD>
+__global__ void k_rope_kv(ModelDev m, int layer, const bf16* __restrict__ qkv, const bf16* __restrict__ qn,
+                          const bf16* __restrict__ kn, bf16* __restrict__ qout, const int* rows_dev, int rows_cap,
+                          const int* stop) {
+  if (stopped(stop)) return;
+  const int rows = rows_dev ? min(*rows_dev, rows_cap) : rows_cap;
+  const int r = blockIdx.x;
+  if (r >= rows) return;
+  constexpr int NP = HD / 64;  // rotation pairs per lane
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+  const int pos = m.row_pos[r];
+  const int page = m.bt[(size_t)m.row_btrow[r] * m.MP + pos / m.P], slot = pos % m.P;
+  const float2* rp = m.rope + (size_t)pos * (HD / 2);
+  const bf16* src = qkv + (size_t)r * m.qkv_dim;
+  for (int head = warp; head < m.hq + 2 * m.hk; head += nw) {
+    const bf16* hv = src + head * HD;
+    float a[NP], b[NP];
+#pragma unroll
+    for (int j = 0; j < NP; ++j) {
+      a[j] = __bfloat162float(hv[lane * NP + j]);
+      b[j] = __bfloat162float(hv[lane * NP + j + HD / 2]);
+    }
+    if (head >= m.hq + m.hk) {  // V: straight into the page
+      const int kvh = head - m.hq - m.hk;
+      bf16* dst = m.kv + m.kv_off(layer, page, 1, kvh, slot);
+#pragma unroll
+      for (int j = 0; j < NP; ++j) {
+        dst[lane * NP + j] = __float2bfloat16(a[j]);
+        dst[lane * NP + j + HD / 2] = __float2bfloat16(b[j]);
+      }
+      continue;
+    }
+    const bool is_q = head < m.hq;
+    if (m.qk_norm) {
+      float ss = 0.f;
+#pragma unroll
+      for (int j = 0; j < NP; ++j) ss += a[j] * a[j] + b[j] * b[j];
+      ss = warp_sum(ss);
+      const float rs = rsqrtf(ss / (float)HD + m.eps);
+      const bf16* nw_ = is_q ? qn : kn;
+#pragma unroll
+      for (int j = 0; j < NP; ++j) {
+        a[j] = __bfloat162float(__float2bfloat16(a[j] * rs * __bfloat162float(nw_[lane * NP + j])));
+        b[j] = __bfloat162float(__float2bfloat16(b[j] * rs * __bfloat162float(nw_[lane * NP + j + HD / 2])));
+      }
+    }
+    float oa[NP], ob[NP];
+#pragma unroll
+    for (int j = 0; j < NP; ++j) {
+      const float2 cs = rp[lane * NP + j];
+      oa[j] = a[j] * cs.x - b[j] * cs.y;
+      ob[j] = b[j] * cs.x + a[j] * cs.y;
+    }
+    bf16* dst = is_q ? qout + (size_t)r * m.qd + head * HD : m.kv + m.kv_off(layer, page, 0, head - m.hq, slot);
+#pragma unroll
+    for (int j = 0; j < NP; ++j) {
+      dst[lane * NP + j] = __float2bfloat16(oa[j]);
+      dst[lane * NP + j + HD / 2] = __float2bfloat16(ob[j]);
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// paged GQA decode attention: one CTA per (slot, kv head, KV split)
+// ---------------------------------------------------------------------------
+
+__device__ __forceinline__ void cp_async16(void* dst, const void* src, bool valid) {
+  const uint32_t d = static_cast<uint32_t>(__cvta_generic_to_shared(dst));
+  const int n = valid ? 16 : 0;
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(d), "l"(src), "r"(n) : "memory");
+}
+__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_wait() {
+  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+
+__device__ __forceinline__ void ldsm_x4(uint32_t& r0, uint32_t& r1, uint32_t& r2, uint32_t& r3, const void* p) {
+  const uint32_t a = static_cast<uint32_t>(__cvta_generic_to_shared(p));
+  asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3)
+               : "r"(a));
+}
+__device__ __forceinline__ void ldsm_x4_t(uint32_t& r0, uint32_t& r1, uint32_t& r2, uint32_t& r3, const void* p) {
+  const uint32_t a = static_cast<uint32_t>(__cvta_generic_to_shared(p));
+  asm volatile("ldmatrix.sync.aligned.m8n8.x4.trans.shared.b16 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3)
+               : "r"(a));
+}
+
+__device__ __forceinline__ void mma16816(float (&c)[4], const uint32_t (&a)[4], uint32_t b0, uint32_t b1) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+      "{%0,%1,%2,%3};"
+      : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
+      : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
+}
+
+__device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
+  const __nv_bfloat162 v = __floats2bfloat162_rn(lo, hi);
+  return *reinterpret_cast<const uint32_t*>(&v);
+}
+
+constexpr int kAttTok = 64;     // tokens per smem tile
+constexpr int kAttThreads = 128;
+
+// swizzled offset (elements) of 16-byte chunk `ch` of row `row` in a [kAttTok][HD] bf16 tile
+template <int HD>
+__device__ __forceinline__ int swz(int row, int ch) {
+  return row * HD + ((ch ^ (row & 7)) << 3);
+}
+
+template <int HD>
+__device__ __forceinline__ void load_tile(const ModelDev& m, int layer, int kvh, const int32_t* bt, int tb, int te,
+                                          bf16* sK, bf16* sV) {
+  constexpr int CH = HD / 8;  // 16-byte chunks per row
+  for (int c = threadIdx.x; c < kAttTok * CH; c += kAttThreads) {
+    const int row = c / CH, ch = c % CH;
+    const int tok = tb + row;
+    const bool ok = tok < te;
+    const int t = ok ? tok : tb;
+    const int page = bt[t / m.P], slot = t % m.P;
+    const bf16* k = m.kv + m.kv_off(layer, page, 0, kvh, slot) + ch * 8;
+    const bf16* v = m.kv + m.kv_off(layer, page, 1, kvh, slot) + ch * 8;
+    cp_async16(sK + swz<HD>(row, ch), k, ok);
+    cp_async16(sV + swz<HD>(row, ch), v, ok);
+  }
+}
+
+template <int HD>
+__global__ void __launch_bounds__(kAttThreads) k_decode_attn(EngineDev e, ModelDev m, int layer,
+                                                           const bf16* __restrict__ q, float* __restrict__ part_o,
+                                                           float* __restrict__ part_ml, int max_splits, int chunk) {
+  const Ctl* c = e.ctl;
+  if (c->stop) return;
+  const int i = blockIdx.x;
+  if (i >= c->b) return;
+  const int kvh = blockIdx.y, sp = blockIdx.z;
+  const int n = m.row_pos[i] + 1;
+  const int c0 = sp * chunk;
+  if (c0 >= n) return;
+  const int c1 = min(n, c0 + chunk);
+  const int32_t* bt = m.bt + (size_t)m.row_btrow[i] * m.MP;
+
+  extern __shared__ __align__(128) uint8_t att_smem[];
+  bf16* sQ = reinterpret_cast<bf16*>(att_smem);  // [16][HD]
+  bf16* sK = sQ + 16 * HD;                        // [2][kAttTok][HD]
+  bf16* sV = sK + 2 * kAttTok * HD;
+  float* sRed = reinterpret_cast<float*>(sV + 2 * kAttTok * HD);  // [4 warps][16 rows][2] + [16][HD]
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int gq = m.gq;
+  // Q rows (gq valid, rest zero), unswizzled row-major [16][HD]
+  for (int idx = threadIdx.x; idx < 16 * HD / 8; idx += kAttThreads) {
+    const int row = idx / (HD / 8), ch = idx % (HD / 8);
+    uint4 v = make_uint4(0, 0, 0, 0);
+    if (row < gq) v = *reinterpret_cast<const uint4*>(q + (size_t)i * m.qd + (kvh * gq + row) * HD + ch * 8);
+    *reinterpret_cast<uint4*>(sQ + swz<HD>(row, ch)) = v;
+  }
+  const int ntiles = (c1 - c0 + kAttTok - 1) / kAttTok;
+  load_tile<HD>(m, layer, kvh, bt, c0, c1, sK, sV);
+  cp_commit();
+  __syncthreads();
+
+  // Q fragments (A operand, 16 x HD), held for the whole chunk
+  uint32_t qa[HD / 16][4];
+#pragma unroll
+  for (int kk = 0; kk < HD / 16; ++kk) {
+    const int row = (lane & 15), ch = kk * 2 + (lane >> 4);
+    ldsm_x4(qa[kk][0], qa[kk][1], qa[kk][2], qa[kk][3], sQ + swz<HD>(row, ch));
+  }
+  const float scale = rsqrtf((float)HD) * kLog2e;
+  float o[HD / 8][4];
+#pragma unroll
+  for (int t = 0; t < HD / 8; ++t) o[t][0] = o[t][1] = o[t][2] = o[t][3] = 0.f;
+  float mrow[2] = {-FLT_MAX, -FLT_MAX}, lrow[2] = {0.f, 0.f};
+  const int gr = lane >> 2, tq = lane & 3;
+
+  for (int t = 0; t < ntiles; ++t) {
+    const int tb = c0 + t * kAttTok;
+    if (t + 1 < ntiles) {
+      load_tile<HD>(m, layer, kvh, bt, tb + kAttTok, c1, sK + ((t + 1) & 1) * kAttTok * HD,
+                    sV + ((t + 1) & 1) * kAttTok * HD);
+      cp_commit();
+      cp_wait<1>();
+    } else {
+      cp_wait<0>();
+    }
+    __syncthreads();
+    const bf16* K = sK + (t & 1) * kAttTok * HD;
+    const bf16* Vt = sV + (t & 1) * kAttTok * HD;
+    // S = Q K^T for this warp's 16 tokens (two n-tiles of 8)
+    float s[2][4] = {{0.f, 0.f, 0.f, 0.f}, {0.f, 0.f, 0.f, 0.f}};
+    const int wt = warp * 16;
+#pragma unroll
+    for (int kk = 0; kk < HD / 16; ++kk) {
+      const int mi = lane >> 3, rr = lane & 7;
+      const int tok = wt + (mi >> 1) * 8 + rr, ch = kk * 2 + (mi & 1);
+      uint32_t b0, b1, b2, b3;
+      ldsm_x4(b0, b1, b2, b3, K + swz<HD>(tok, ch));
+      mma16816(s[0], qa[kk], b0, b1);
+      mma16816(s[1], qa[kk], b2, b3);
+    }
+    // scale + mask, online softmax over rows gr and gr+8
+    float mx[2] = {-FLT_MAX, -FLT_MAX};
+#pragma unroll
+    for (int j = 0; j < 2; ++j)
+#pragma unroll
+      for (int q4 = 0; q4 < 4; ++q4) {
+        const int tok = tb + wt + j * 8 + tq * 2 + (q4 & 1);
+        const float v = tok < c1 ? s[j][q4] * scale : -FLT_MAX;
+        s[j][q4] = v;
+        mx[q4 >> 1] = fmaxf(mx[q4 >> 1], v);
+      }
+    float alpha[2];
+#pragma unroll
+    for (int r = 0; r < 2; ++r) {
+      mx[r] = fmaxf(mx[r], __shfl_xor_sync(0xffffffffu, mx[r], 1));
+      mx[r] = fmaxf(mx[r], __shfl_xor_sync(0xffffffffu, mx[r], 2));
+      const float mn = fmaxf(mrow[r], mx[r]);
+      alpha[r] = (mrow[r] == -FLT_MAX) ? 0.f : exp2f(mrow[r] - mn);
+      mrow[r] = mn;
+    }
+    float rs[2] = {0.f, 0.f};
+#pragma unroll
+    for (int j = 0; j < 2; ++j)
+#pragma unroll
+      for (int q4 = 0; q4 < 4; ++q4) {
+        const int r = q4 >> 1;
+        const float p = (s[j][q4] == -FLT_MAX || mrow[r] == -FLT_MAX) ? 0.f : exp2f(s[j][q4] - mrow[r]);
+        s[j][q4] = p;
+        rs[r] += p;
+      }
+#pragma unroll
+    for (int r = 0; r < 2; ++r) lrow[r] = lrow[r] * alpha[r] + rs[r];
+#pragma unroll
+    for (int nt = 0; nt < HD / 8; ++nt) {
+      o[nt][0] *= alpha[0];
+      o[nt][1] *= alpha[0];
+      o[nt][2] *= alpha[1];
+      o[nt][3] *= alpha[1];
+    }
+    // O += P V  (A = P from the S accumulators, B = V via ldmatrix.trans)
+    uint32_t pa[4];
+    pa[0] = pack_bf16(s[0][0], s[0][1]);
+    pa[1] = pack_bf16(s[0][2], s[0][3]);
+    pa[2] = pack_bf16(s[1][0], s[1][1]);
+    pa[3] = pack_bf16(s[1][2], s[1][3]);
+#pragma unroll
+    for (int nt2 = 0; nt2 < HD / 16; ++nt2) {
+      const int mi = lane >> 3, rr = lane & 7;
+      const int tok = wt + (mi & 1) * 8 + rr, ch = nt2 * 2 + (mi >> 1);
+      uint32_t b0, b1, b2, b3;
+      ldsm_x4_t(b0, b1, b2, b3, Vt + swz<HD>(tok, ch));
+      mma16816(o[2 * nt2], pa, b0, b1);
+      mma16816(o[2 * nt2 + 1], pa, b2, b3);
+    }
+    __syncthreads();  // the buffer is refilled next round
+  }
+  // row sums across the quad
+#pragma unroll
+  for (int r = 0; r < 2; ++r) {
+    lrow[r] += __shfl_xor_sync(0xffffffffu, lrow[r], 1);
+    lrow[r] += __shfl_xor_sync(0xffffffffu, lrow[r], 2);
+  }
+  // combine the 4 warps (each saw a different 16-token slice of every tile)
+  float* sML = sRed;                 // [4][16][2]
+  float* sO = sRed + 4 * 16 * 2;     // [16][HD]
+  if (tq == 0) {
+    sML[(warp * 16 + gr) * 2 + 0] = mrow[0];
+    sML[(warp * 16 + gr) * 2 + 1] = lrow[0];
+    sML[(warp * 16 + gr + 8) * 2 + 0] = mrow[1];
+    sML[(warp * 16 + gr + 8) * 2 + 1] = lrow[1];
+  }
+  for (int idx = threadIdx.x; idx < 16 * HD; idx += kAttThreads) sO[idx] = 0.f;
+  __syncthreads();
+  float wsc[2];
+#pragma unroll
+  for (int r = 0; r < 2; ++r) {
+    const int row = gr + r * 8;
+    float M = -FLT_MAX;
+    for (int w = 0; w < 4; ++w) M = fmaxf(M, sML[(w * 16 + row) * 2]);
+    wsc[r] = mrow[r] == -FLT_MAX ? 0.f : exp2f(mrow[r] - M);
+  }
+#pragma unroll
+  for (int nt = 0; nt < HD / 8; ++nt) {
+    const int col = nt * 8 + tq * 2;
+    atomicAdd(&sO[gr * HD + col], o[nt][0] * wsc[0]);
+    atomicAdd(&sO[gr * HD + col + 1], o[nt][1] * wsc[0]);
+    atomicAdd(&sO[(gr + 8) * HD + col], o[nt][2] * wsc[1]);
+    atomicAdd(&sO[(gr + 8) * HD + col + 1], o[nt][3] * wsc[1]);
+  }
+  __syncthreads();
+  // partial (unnormalised O, m, l) for this split
+  for (int idx = threadIdx.x; idx < gq * HD; idx += kAttThreads) {
+    const int row = idx / HD, dcol = idx % HD;
+    const size_t base = ((size_t)i * m.hq + kvh * gq + row) * max_splits + sp;
+    part_o[base * HD + dcol] = sO[row * HD + dcol];
+  }
+  if (threadIdx.x < gq) {
+    const int row = threadIdx.x;
+    float M = -FLT_MAX, L = 0.f;
+    for (int w = 0; w < 4; ++w) M = fmaxf(M, sML[(w * 16 + row) * 2]);
+    for (int w = 0; w < 4; ++w) {
+      const float mw = sML[(w * 16 + row) * 2];
+      if (mw != -FLT_MAX) L += sML[(w * 16 + row) * 2 + 1] * exp2f(mw - M);
+    }
+    const size_t base = ((size_t)i * m.hq + kvh * gq + row) * max_splits + sp;
+    part_ml[base * 2 + 0] = M;
+    part_ml[base * 2 + 1] = L;
+  }
+}
+
+template <int HD>
+__global__ void k_attn_combine(EngineDev e, ModelDev m, const float* __restrict__ part_o,
+                               const float* __restrict__ part_ml, bf16* __restrict__ out, int max_splits, int chunk) {
+  const Ctl* c = e.ctl;
+  if (c->stop) return;
+  const int i = blockIdx.x;
+  if (i >= c->b) return;
+  const int head = blockIdx.y;
+  const int n = m.row_pos[i] + 1;
+  const int ns = (n + chunk - 1) / chunk;
+  const size_t base = ((size_t)i * m.hq + head) * max_splits;
+  float M = -FLT_MAX;
+  for (int s = 0; s < ns; ++s) M = fmaxf(M, part_ml[(base + s) * 2]);
+  float L = 0.f, acc = 0.f;
+  const int dcol = threadIdx.x;
+  for (int s = 0; s < ns; ++s) {
+    const float w = exp2f(part_ml[(base + s) * 2] - M);
+    L += part_ml[(base + s) * 2 + 1] * w;
+    acc += part_o[(base + s) * HD + dcol] * w;
+  }
+  out[(size_t)i * m.qd + head * HD + dcol] = __float2bfloat16(acc / L);
+}
+
+// ---------------------------------------------------------------------------
+// causal prefill attention over a prompt group's own tokens (paged K/V)
+// one warp per (row, q head)
+// ---------------------------------------------------------------------------
+
+template <int HD>
+__global__ void k_prefill_attn(ModelDev m, int layer, const bf16* __restrict__ q, bf16* __restrict__ out,
+                               const int* __restrict__ seg_start, const int* __restrict__ seg_group, int n_seg,
+                               int rows) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int r = blockIdx.x * (blockDim.x >> 5) + warp;
+  if (r >= rows) return;
+  const int head = blockIdx.y, kvh = head / m.gq;
+  int lo = 0, hi = n_seg - 1;
+  while (lo < hi) {  // last segment with start <= r
+    const int mid = (lo + hi + 1) >> 1;
+    if (seg_start[mid] <= r)
+      lo = mid;
+    else
+      hi = mid - 1;
+  }
+  const int p = r - seg_start[lo];
+  const int32_t* bt = m.bt + (size_t)(m.H + seg_group[lo]) * m.MP;
+  constexpr int E = HD / 32;
+  float qv[E], acc[E];
+  const bf16* qr = q + (size_t)r * m.qd + head * HD;
+#pragma unroll
+  for (int j = 0; j < E; ++j) {
+    qv[j] = __bfloat162float(qr[lane * E + j]) * rsqrtf((float)HD) * kLog2e;
+    acc[j] = 0.f;
+  }
+  float mx = -FLT_MAX, l = 0.f;
+  for (int t = 0; t <= p; ++t) {
+    const int page = bt[t / m.P], slot = t % m.P;
+    const bf16* k = m.kv + m.kv_off(layer, page, 0, kvh, slot);
+    float s = 0.f;
+#pragma unroll
+    for (int j = 0; j < E; ++j) s += qv[j] * __bfloat162float(k[lane * E + j]);
+    s = warp_sum(s);
+    const float mn = fmaxf(mx, s);
+    const float a = exp2f(mx - mn), pw = exp2f(s - mn);
+    l = l * a + pw;
+    const bf16* v = m.kv + m.kv_off(layer, page, 1, kvh, slot);
+#pragma unroll
+    for (int j = 0; j < E; ++j) acc[j] = acc[j] * a + pw * __bfloat162float(v[lane * E + j]);
+    mx = mn;
+  }
+  bf16* o = out + (size_t)r * m.qd + head * HD;
+#pragma unroll
+  for (int j = 0; j < E; ++j) o[lane * E + j] = __float2bfloat16(acc[j] / l);
+}
+
+// ---------------------------------------------------------------------------
+// page management
+// ---------------------------------------------------------------------------
+
+// fresh samples inherit their group's prompt pages; the partial tail page is copied
+__global__ void k_fork_meta(EngineDev e, ModelDev m, const ab_sample_desc* descs, int n, int32_t* tail_src,
+                            int32_t* tail_dst) {
+  Ctl* c = e.ctl;
+  const int k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= n) return;
+  tail_src[k] = -1;
+  const ab_sample_desc s = descs[k];
+  if (s.gen_len != 0) return;
+  const int h = s.handle, g = s.group_slot;
+  const int ctx = m.g_ctx[g];
+  const int nfull = ctx / m.P;
+  const int32_t* gb = m.bt + (size_t)(m.H + g) * m.MP;
+  int32_t* hb = m.bt + (size_t)h * m.MP;
+  for (int j = 0; j < nfull; ++j) hb[j] = gb[j];
+  m.h_ctx[h] = ctx;
+  m.h_last_tok[h] = m.g_last_tok[g];
+  m.h_shared[h] = nfull;
+  if (ctx % m.P) {
+    const int idx = pop_page(c);
+    if (idx < 0) {
+      atomicCAS(&c->error, kErrNone, kErrOutOfKV);
+      return;
+    }
+    hb[nfull] = m.free_pages[idx];
+    tail_src[k] = gb[nfull];
+    tail_dst[k] = hb[nfull];
+  }
+}
+
+__global__ void k_fork_copy(ModelDev m, const int32_t* tail_src, const int32_t* tail_dst) {
+  const int k = blockIdx.x, layer = blockIdx.y;
+  const int src = tail_src[k];
+  if (src < 0) return;
+  const int dst = tail_dst[k];
+  const size_t n = (size_t)2 * m.hk * m.P * m.hd / 8;  // uint4 chunks (K and V are adjacent)
+  const uint4* s = reinterpret_cast<const uint4*>(m.kv + m.kv_off(layer, src, 0, 0, 0));
+  uint4* d = reinterpret_cast<uint4*>(m.kv + m.kv_off(layer, dst, 0, 0, 0));
+  for (size_t j = threadIdx.x; j < n; j += blockDim.x) d[j] = s[j];
+}
+
+__global__ void k_release(EngineDev e, ModelDev m, const int32_t* handles, int n) {
+  Ctl* c = e.ctl;
+  const int k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= n) return;
+  const int h = handles[k];
+  const int have = (m.h_ctx[h] + m.P - 1) / m.P;
+  const int own0 = m.h_shared[h];
+  const int cnt = have - own0;
+  if (cnt > 0) {
+    const long long base =
+        (long long)atomicAdd(reinterpret_cast<unsigned long long*>(&c->kv_free_top), (unsigned long long)cnt);
+    for (int j = 0; j < cnt; ++j) m.free_pages[base + j] = m.bt[(size_t)h * m.MP + own0 + j];
+  }
+  m.h_ctx[h] = 0;
+  m.h_shared[h] = 0;
+}
+
+__global__ void k_group_alloc(EngineDev e, ModelDev m, const int* groups, const int* lens, const int* last_tok,
+                              int n) {
+  Ctl* c = e.ctl;
+  const int k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= n) return;
+  const int g = groups[k], len = lens[k];
+  const int np = (len + m.P - 1) / m.P;
+  int32_t* gb = m.bt + (size_t)(m.H + g) * m.MP;
+  for (int j = 0; j < np; ++j) {
+    const int idx = pop_page(c);
+    if (idx < 0) {
+      atomicCAS(&c->error, kErrNone, kErrOutOfKV);
+      m.g_npages[g] = j;
+      return;
+    }
+    gb[j] = m.free_pages[idx];
+  }
+  m.g_npages[g] = np;
+  m.g_ctx[g] = len;
+  m.g_last_tok[g] = last_tok[k];
+}
+
+__global__ void k_group_release(EngineDev e, ModelDev m, int g) {
+  Ctl* c = e.ctl;
+  const int np = m.g_npages[g];
+  if (threadIdx.x != 0 || np <= 0) return;
+  const long long base =
+      (long long)atomicAdd(reinterpret_cast<unsigned long long*>(&c->kv_free_top), (unsigned long long)np);
+  for (int j = 0; j < np; ++j) m.free_pages[base + j] = m.bt[(size_t)(m.H + g) * m.MP + j];
+  m.g_npages[g] = 0;
+  m.g_ctx[g] = 0;
+}
+
+}  // namespace
+
+// ---------------------------------------------------------------------------
+// launchers
+// ---------------------------------------------------------------------------
+
+void launch_init_weights(bf16* w, size_t n, uint64_t seed, uint64_t tensor_id, float std, float constant,
+                         cudaStream_t s) {
+  const int mode = std > 0.f ? 0 : 1;
+  k_init_weights<<<4 * 148, 256, 0, s>>>(w, n, seed ^ 0x5DEECE66Dull, tensor_id, std, constant, mode);
+  AB_CUDA(cudaGetLastError());
+}
+
+void launch_rope_table(float2* rope, int max_pos, int hd, float theta, cudaStream_t s) {
+  k_rope_table<<<4 * 148, 256, 0, s>>>(rope, max_pos, hd, theta);
+  AB_CUDA(cudaGetLastError());
+}
+
+void launch_prep_decode(const EngineDev& e, const ModelDev& m, cudaStream_t s) {
+  k_prep_decode<<<ceil_div(e.S, 128), 128, 0, s>>>(e, m);
+}
+
+void launch_embed(const ModelDev& m, const bf16* emb, float* x, const int* rows_dev, int rows_cap, const int* stop,
+                  cudaStream_t s) {
+  k_embed<<<rows_cap, 128, 0, s>>>(m, emb, x, rows_dev, rows_cap, stop);
+}
+
+void launch_rmsnorm(const float* x, const bf16* w, bf16* out, int d, float eps, const int* rows_dev, int rows_cap,
+                    const int* stop, cudaStream_t s) {
+  k_rmsnorm<<<ceil_div(rows_cap, 8), 256, 0, s>>>(x, w, out, d, eps, rows_dev, rows_cap, stop);
+}
+
+void launch_rope_kv(const ModelDev& m, int layer, const bf16* qkv, const bf16* q_norm, const bf16* k_norm, bf16* q_out,
+                    const int* rows_dev, int rows_cap, const int* stop, cudaStream_t s) {
+  if (m.hd == 128)
+    k_rope_kv<128><<<rows_cap, 256, 0, s>>>(m, layer, qkv, q_norm, k_norm, q_out, rows_dev, rows_cap, stop);
+  else
+    k_rope_kv<64><<<rows_cap, 256, 0, s>>>(m, layer, qkv, q_norm, k_norm, q_out, rows_dev, rows_cap, stop);
+}
+
+template <int HD>
+static void decode_attn_t(const EngineDev& e, const ModelDev& m, int layer, const bf16* q, bf16* out, float* part_o,
+                          float* part_ml, int max_splits, int chunk, cudaStream_t s) {
+  const int smem = (16 * HD + 4 * kAttTok * HD) * 2 + (4 * 16 * 2 + 16 * HD) * 4;
+  static bool attr = false;
+  if (!attr) {
+    AB_CUDA(cudaFuncSetAttribute(k_decode_attn<HD>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    attr = true;
+  }
+  k_decode_attn<HD><<<dim3(e.S, m.hk, max_splits), kAttThreads, smem, s>>>(e, m, layer, q, part_o, part_ml,
+                                                                           max_splits, chunk);
+  k_attn_combine<HD><<<dim3(e.S, m.hq), HD, 0, s>>>(e, m, part_o, part_ml, out, max_splits, chunk);
+}
+
+void launch_decode_attention(const EngineDev& e, const ModelDev& m, int layer, const bf16* q, bf16* out,
+                             float* part_o, float* part_ml, int max_splits, int chunk, cudaStream_t s) {
+  if (m.hd == 128)
+    decode_attn_t<128>(e, m, layer, q, out, part_o, part_ml, max_splits, chunk, s);
+  else
+    decode_attn_t<64>(e, m, layer, q, out, part_o, part_ml, max_splits, chunk, s);
+}
+
+void launch_prefill_attention(const ModelDev& m, int layer, const bf16* q, bf16* out, const int* seg_start,
+                              const int* seg_group, int n_seg, int rows, int max_len, cudaStream_t s) {
+  (void)max_len;
+  dim3 grid(ceil_div(rows, 4), m.hq);
+  if (m.hd == 128)
+    k_prefill_attn<128><<<grid, 128, 0, s>>>(m, layer, q, out, seg_start, seg_group, n_seg, rows);
+  else
+    k_prefill_attn<64><<<grid, 128, 0, s>>>(m, layer, q, out, seg_start, seg_group, n_seg, rows);
+}
+
+void launch_fork_groups(const EngineDev& e, const ModelDev& m, const ab_sample_desc* descs, int n, cudaStream_t s) {
+  static int32_t* buf = nullptr;
+  static int cap = 0;
+  if (n > cap) {
+    if (buf) cudaFree(buf);
+    cap = n + 1024;
+    AB_CUDA(cudaMalloc(&buf, sizeof(int32_t) * 2 * cap));
+  }
+  k_fork_meta<<<ceil_div(n, 128), 128, 0, s>>>(e, m, descs, n, buf, buf + cap);
+  k_fork_copy<<<dim3(n, m.L), 256, 0, s>>>(m, buf, buf + cap);
+}
+
+void launch_release_handles(const EngineDev& e, const ModelDev& m, const int32_t* handles, int n, cudaStream_t s) {
+  k_release<<<ceil_div(n, 128), 128, 0, s>>>(e, m, handles, n);
+}
+
+void launch_group_alloc(const EngineDev& e, const ModelDev& m, const int* groups, const int* lens, const int* last_tok,
+                        int n, cudaStream_t s) {
+  k_group_alloc<<<ceil_div(n, 128), 128, 0, s>>>(e, m, groups, lens, last_tok, n);
+}
+
+void launch_group_release(const EngineDev& e, const ModelDev& m, int group, cudaStream_t s) {
+  k_group_release<<<1, 32, 0, s>>>(e, m, group);
+}
+
+}  // namespace ab

@@ -399,14 +399,34 @@ ScopedTimer::~ScopedTimer() {
 static void collect_timers(Engine& e) {
   if (e.pending.empty()) return;
   AB_CUDA(cudaStreamSynchronize(e.stream));
+  int64_t max_it = -1;
+  for (auto& p : e.pending) max_it = std::max(max_it, p.run_iter);
+  std::vector<int32_t> it_b;
+  std::vector<int64_t> it_ctx;
+  if (max_it >= 0) {
+    const int64_t n = std::min<int64_t>(max_it + 1, e.d.it_cap);
+    it_b.resize(n);
+    it_ctx.resize(n);
+    AB_CUDA(cudaMemcpy(it_b.data(), e.d.it_b, sizeof(int32_t) * n, cudaMemcpyDeviceToHost));
+    AB_CUDA(cudaMemcpy(it_ctx.data(), e.d.it_ctx, sizeof(int64_t) * n, cudaMemcpyDeviceToHost));
+  }
   for (auto& p : e.pending) {
     float ms = 0;
     AB_CUDA(cudaEventElapsedTime(&ms, p.a, p.b));
     auto& t = e.timers[p.timer];
-    t.launches += 1;
-    t.ms += ms;
-    t.bytes += p.bytes;
-    t.flops += p.flops;
+    double bytes = p.bytes, flops = p.flops;
+    bool live = true;
+    if (p.run_iter >= 0 && p.run_iter < (int64_t)it_b.size()) {
+      const double b = it_b[p.run_iter];
+      live = b > 0;  // iterations queued past the stop point are no-ops
+      if (e.model) model_kernel_cost(e.model, t.name, b, (double)it_ctx[p.run_iter], &bytes, &flops);
+    }
+    if (live) {
+      t.launches += 1;
+      t.ms += ms;
+      t.bytes += bytes;
+      t.flops += flops;
+    }
     e.event_pool.push_back(p.a);
     e.event_pool.push_back(p.b);
   }
@@ -532,6 +552,7 @@ static void destroy(Engine* e) {
   if (!e) return;
   cudaSetDevice(e->device);
   cudaStreamSynchronize(e->stream);
+  if (e->iter_graph) cudaGraphExecDestroy(e->iter_graph);
   if (e->model) model_destroy(e->model);
   EngineDev& d = e->d;
   void* ptrs[] = {d.ctl,     d.slot_handle, d.slot_tmp, d.slot_finish, d.slot_token, d.q_buf,  d.h_gen,
@@ -591,6 +612,7 @@ static void submit(Engine& e, const ab_sample_desc* descs, int n) {
 
 static void launch_iteration(Engine& e, int64_t run_iter) {
   const bool timed = e.profile && (run_iter % e.sample_every == 0);
+  e.launches += 2 + (e.model ? 5 + 9 * (int64_t)e.mcfg.n_layers : 1);
   {
     ScopedTimer t(e, timed, "admit", run_iter);
     k_admit<<<1, 256, 0, e.stream>>>(e.d);
@@ -607,18 +629,48 @@ static void launch_iteration(Engine& e, int64_t run_iter) {
   }
 }
 
+// Iterations are replayed from one captured CUDA graph: every kernel reads the
+// live batch size and the stop flag from the device control block, so the
+// same graph serves every batch size.  Profiled iterations launch directly
+// (their CUDA events are recorded between the kernels).
+static void launch_iteration_fast(Engine& e, int64_t run_iter) {
+  const bool timed = e.profile && (run_iter % e.sample_every == 0);
+  if (timed || !e.use_graphs || e.direct_launches < 1) {
+    launch_iteration(e, run_iter);
+    ++e.direct_launches;
+    return;
+  }
+  if (!e.iter_graph) {
+    const int64_t before = e.launches;
+    cudaGraph_t g;
+    AB_CUDA(cudaStreamBeginCapture(e.stream, cudaStreamCaptureModeThreadLocal));
+    launch_iteration(e, -1);
+    AB_CUDA(cudaStreamEndCapture(e.stream, &g));
+    AB_CUDA(cudaGraphInstantiate(&e.iter_graph, g, 0));
+    AB_CUDA(cudaGraphDestroy(g));
+    e.graph_kernels = e.launches - before;
+    e.launches = before;
+  }
+  AB_CUDA(cudaGraphLaunch(e.iter_graph, e.stream));
+  e.launches += e.graph_kernels;
+}
+
 static void run(Engine& e, const ab_run_args* a, ab_run_result* r, ab_event* ev, int ev_cap, ab_admit* adm,
                 int adm_cap) {
   AB_REQUIRE(a && r, AB_ERR_CONTRACT, "null run arguments");
   AB_REQUIRE(a->group_size >= 0, AB_ERR_CONTRACT, "group_size must be >= 0");
   k_run_begin<<<1, 1, 0, e.stream>>>(e.d, *a);
+  if (e.profile) {
+    AB_CUDA(cudaMemsetAsync(e.d.it_b, 0, sizeof(int32_t) * e.d.it_cap, e.stream));
+    AB_CUDA(cudaMemsetAsync(e.d.it_ctx, 0, sizeof(int64_t) * e.d.it_cap, e.stream));
+  }
   int64_t launched = 0;
   int chunk = 1;
   const int policy_chunk = 4;
   while (true) {
     int n = chunk;
     if (a->max_iters > 0) n = (int)std::min<int64_t>(n, std::max<int64_t>(1, a->max_iters - launched));
-    for (int i = 0; i < n; ++i) launch_iteration(e, launched + i);
+    for (int i = 0; i < n; ++i) launch_iteration_fast(e, launched + i);
     launched += n;
     sync_ctl(e);
     const Ctl& c = *e.ctl_host;
@@ -868,6 +920,7 @@ int ab_engine_stats(ab_engine* e, ab_stats* out) {
     out->kv_pages_total = g.model ? ab::model_pages_total(g.model) : 0;
     out->kv_pages_free = c.kv_free_top;
     out->prefill_tokens = g.prefill_tokens;
+    out->kernel_launches = g.launches;
   });
 }
 

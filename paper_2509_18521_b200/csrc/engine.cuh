@@ -89,6 +89,11 @@ struct Engine {
   int32_t* stage_i32_host = nullptr;
   size_t stage_i32_cap = 0;
   int64_t prefill_tokens = 0;
+  int64_t launches = 0;  // kernels launched (gpu_launches claim)
+  bool use_graphs = true;
+  int64_t direct_launches = 0;
+  cudaGraphExec_t iter_graph = nullptr;
+  int64_t graph_kernels = 0;
   // profiling
   bool profile = false;
   int sample_every = 8;
@@ -117,6 +122,7 @@ void model_submit(Engine& e, const ab_sample_desc* descs_dev, int n);  // after 
 void model_release(Engine& e, const int32_t* handles_dev, int n);
 void model_iteration(Engine& e, int64_t run_iter, bool timed);         // pages + forward + sampler
 int64_t model_pages_total(Model* m);
+void model_kernel_cost(Model* m, const std::string& name, double b, double sum_ctx, double* bytes, double* flops);
 
 // profiling helper (engine.cu)
 struct ScopedTimer {

@@ -129,6 +129,7 @@ class Engine:
         self._gfree = list(range(self.max_groups - 1, -1, -1))
         self._pending: list = []
         self.last_run = None
+        self._h2d = self._d2h = 0  # bytes crossing PCIe through this API (bench e2e accounting)
         if self._model_kind != capi.MODEL_CONTEXT_FREE:
             self._create()
 
@@ -244,6 +245,7 @@ class Engine:
                 self._flush()
                 prompt = np.ascontiguousarray(self.prompt_source(iid), dtype=np.int32)
                 capi.call("ab_engine_open_group", self._h, g, prompt.ctypes.data_as(capi.I32P), int(prompt.size))
+                self._h2d += prompt.nbytes
         self._grefs[iid] += 1
         return h
 
@@ -289,6 +291,7 @@ class Engine:
         arr = (capi.SampleDesc * n)(*[capi.SampleDesc(*p) for p in self._pending])
         self._pending = []
         capi.call("ab_engine_submit", self._h, arr, n)
+        self._h2d += C.sizeof(arr)
 
     # -- decode ------------------------------------------------------------------------
 
@@ -324,6 +327,7 @@ class Engine:
         res = capi.RunResult()
         cap = len(self._ev_buf)
         capi.call("ab_engine_run", self._h, C.byref(args), C.byref(res), self._ev_buf, cap, self._adm_buf, cap)
+        self._d2h += C.sizeof(res) + res.n_events * C.sizeof(capi.Event) + res.n_admits * C.sizeof(capi.Admit)
         self.last_run = res
         self.iteration_index = res.iteration_index
         self.cumulative_tokens = res.cumulative_tokens
@@ -390,6 +394,7 @@ class Engine:
             st[k] = s.total_tokens - seg.token_count
             ct[k] = seg.token_count
         total = sum(ct)
+        self._d2h += total * 12
         tok = np.empty(max(total, 1), dtype=np.int32)
         lp = np.empty(max(total, 1), dtype=np.float64)
         capi.call("ab_engine_read_payload", self._h, hs, st, ct, n, tok.ctypes.data_as(capi.I32P),
@@ -413,6 +418,7 @@ class Engine:
         gen = (C.c_int32 * max(cap, 1))()
         na, nq = C.c_int(), C.c_int()
         capi.call("ab_engine_abort", self._h, hs, gen, max(cap, 1), C.byref(na), C.byref(nq))
+        self._d2h += 8 * (na.value + nq.value)
         out: list[RolloutSample] = []
         paused = []
         for k in range(na.value):
@@ -435,9 +441,32 @@ class Engine:
         self._release(drained)  # zero-token samples hold no device state worth keeping
         return out
 
+    def io_bytes(self) -> tuple[int, int]:
+        """(host->device, device->host) bytes moved through the C-ABI so far."""
+        return self._h2d, self._d2h
+
     def discard(self, samples) -> None:
         """Release device state (handles, KV pages) of samples leaving the engine for good."""
         self._release(samples)
+
+    # -- weights ------------------------------------------------------------------------------
+
+    def export_weights(self) -> dict:
+        """Device bf16 parameters as CPU torch.bfloat16 tensors (for the oracle / checkpoints)."""
+        import torch
+
+        n = C.c_int()
+        capi.call("ab_engine_weight_count", self._h, C.byref(n))
+        out = {}
+        name = C.create_string_buffer(128)
+        for i in range(n.value):
+            r, c = C.c_int64(), C.c_int64()
+            capi.call("ab_engine_weight_info", self._h, i, name, 128, C.byref(r), C.byref(c))
+            buf = np.empty(r.value * c.value, dtype=np.uint16)
+            capi.call("ab_engine_get_weight", self._h, i, buf.ctypes.data_as(C.c_void_p), buf.nbytes)
+            out[name.value.decode()] = torch.from_numpy(buf.view(np.int16)).view(torch.bfloat16).view(r.value,
+                                                                                                    c.value)
+        return out
 
     # -- profiling ---------------------------------------------------------------------------
 

@@ -1,0 +1,163 @@
+"""Transformer decode path on the GPU vs the torch-CPU oracle (oracle/cpu_model.py).
+
+Greedy decoding: every generated token must be the oracle's argmax given the
+same prefix (teacher-forced), except where the oracle's own top-2 margin is
+below MARGIN_EPS (a near-tie that bf16 rounding may legitimately flip; such
+positions are counted and bounded).  Log-probs must agree within LOGP_TOL.
+"""
+
+import numpy as np
+import pytest
+
+import paper_2509_18521_b200 as pb
+from paper_2509_18521_b200.rollouts import RolloutSample
+
+torch = pytest.importorskip("torch")
+from oracle import rng_ref  # noqa: E402
+from oracle.cpu_model import CpuDecoder  # noqa: E402
+
+pytestmark = pytest.mark.gpu
+
+MARGIN_EPS = 0.05   # logit units
+LOGP_TOL = 0.05     # nats
+
+
+def _engine(spec, prompts, S=8, l_max=64, page=16, greedy=True, temperature=1.0, P=None):
+    P = P or len(next(iter(prompts.values())))
+    return pb.LengthDrivenEngine(
+        pb.EngineConfig(max_slots=S, l_max=l_max), global_seed=3, model=spec,
+        sampling=pb.SamplingConfig(temperature=temperature, greedy=greedy), prompt_len=P, page_size=page,
+        kv_pages=1024, max_handles=64, max_groups=16, prompt_source=lambda iid: prompts[iid])
+
+
+def _prompts(spec, n, P):
+    return {i: pb.synthetic_prompt(11, i, P, spec.vocab) for i in range(n)}
+
+
+def _drain(eng):
+    while not eng.idle:
+        eng.decode_until_event()
+
+
+def _check_greedy(dec, prompt, toks, logps):
+    sc = dec.score([int(t) for t in prompt], toks)
+    flips = 0
+    for k, (t, lp, r) in enumerate(zip(toks, logps, sc)):
+        if r["argmax"] != t:
+            flips += 1
+            assert r["margin"] < MARGIN_EPS, (k, r)
+        assert abs(lp - r["logp"]) < LOGP_TOL, (k, lp, r)
+    return flips
+
+
+@pytest.mark.parametrize("preset,layers", [("tiny", None), ("qwen2.5-1.5b", 2), ("qwen3-4b", 1)])
+def test_greedy_tokens_match_oracle(preset, layers):
+    spec = pb.PRESETS[preset]
+    if layers:
+        spec = spec.truncated(layers)
+    prompts = _prompts(spec, 2, 24)
+    eng = _engine(spec, prompts, page=16 if preset == "tiny" else 64)
+    eng.begin_step(0)
+    samples = []
+    for iid, lens in ((0, [5, 17, 30, 40]), (1, [9, 33])):
+        for j, L in enumerate(lens):
+            s = RolloutSample(iid, j)
+            s.target_length = L
+            eng.submit(s)
+            samples.append(s)
+    _drain(eng)
+    dec = CpuDecoder(spec, eng.export_weights())
+    flips = total = 0
+    for s in samples:
+        assert s.total_tokens == s.target_length and len(s.token_ids()) == s.target_length
+    # greedy + shared prompt: all samples of a group generate the same sequence, so
+    # the longest one is scored against the oracle and the others must be its prefixes
+    for iid in (0, 1):
+        grp = [s for s in samples if s.instance_id == iid]
+        top = max(grp, key=lambda s: s.total_tokens)
+        for s in grp:
+            assert s.token_ids() == top.token_ids()[: s.total_tokens]
+            np.testing.assert_allclose(s.behavior_logprob_trace(), top.behavior_logprob_trace()[: s.total_tokens],
+                                       rtol=0, atol=1e-5)
+        flips += _check_greedy(dec, prompts[iid], top.token_ids(), top.behavior_logprob_trace())
+        total += top.total_tokens
+    assert flips <= max(2, total // 25), f"{flips} near-tie flips over {total} tokens"
+    eng.close()
+
+
+def test_resume_across_steps_keeps_kv_and_matches_uninterrupted():
+    spec = pb.PRESETS["tiny"]
+    prompts = _prompts(spec, 1, 20)
+    eng = _engine(spec, prompts)
+    eng.begin_step(0)
+    s = RolloutSample(0, 0)
+    s.target_length = 50
+    eng.submit(s)
+    for _ in range(13):
+        eng.decode_iteration()
+    (p,) = eng.abort_active()
+    assert p.total_tokens == 13
+    eng.begin_step(1)
+    eng.submit(p)
+    _drain(eng)
+    assert [g.token_count for g in s.segments] == [13, 37]
+    dec = CpuDecoder(spec, eng.export_weights())
+    flips = _check_greedy(dec, prompts[0], s.token_ids(), s.behavior_logprob_trace())
+    assert flips <= 1
+    # identical to an uninterrupted run
+    eng2 = _engine(spec, prompts)
+    eng2.begin_step(0)
+    r = RolloutSample(0, 0)
+    r.target_length = 50
+    eng2.submit(r)
+    _drain(eng2)
+    assert r.token_ids() == s.token_ids()
+    np.testing.assert_allclose(r.behavior_logprob_trace(), s.behavior_logprob_trace(), rtol=0, atol=1e-6)
+
+
+def test_temperature_sampling_follows_philox_inverse_cdf():
+    spec = pb.PRESETS["tiny"]
+    prompts = _prompts(spec, 1, 16)
+    T = 0.8
+    eng = _engine(spec, prompts, greedy=False, temperature=T)
+    eng.begin_step(0)
+    s = RolloutSample(0, 2)
+    s.target_length = 40
+    eng.submit(s)
+    _drain(eng)
+    toks, lps = s.token_ids(), s.behavior_logprob_trace()
+    dec = CpuDecoder(spec, eng.export_weights())
+    key = rng_ref.stream_key(3, rng_ref.LANE_POLICY_TOKENS, 0, 2)
+    cache = dec.new_cache()
+    prompt = [int(t) for t in prompts[0]]
+    dec.forward(prompt[:-1], cache, 0, want_logits=False)
+    tok, pos, bad = prompt[-1], len(prompt) - 1, 0
+    for k, g in enumerate(toks):
+        z = dec.forward([tok], cache, pos)
+        p = torch.softmax(z.double() / T, -1)
+        cdf = torch.cumsum(p, 0)
+        u = rng_ref.raw_uniform(key, k)
+        lo = float(cdf[g - 1]) if g > 0 else 0.0
+        hi = float(cdf[g])
+        if not (lo - 1e-3 <= u <= hi + 1e-3):
+            bad += 1
+        assert abs(lps[k] - float(torch.log(p[g]))) < LOGP_TOL
+        tok, pos = g, pos + 1
+    assert bad == 0
+
+
+def test_kv_pages_are_recycled():
+    spec = pb.PRESETS["tiny"]
+    prompts = _prompts(spec, 4, 20)
+    eng = _engine(spec, prompts)
+    free0 = eng.stats().kv_pages_free
+    for step in range(3):
+        eng.begin_step(step)
+        for iid in range(4):
+            for j in range(2):
+                s = RolloutSample(iid + 10 * step, j)
+                s.target_length = 10 + 7 * j
+                prompts[iid + 10 * step] = prompts[iid]
+                eng.submit(s)
+        _drain(eng)
+    assert eng.stats().kv_pages_free == free0
