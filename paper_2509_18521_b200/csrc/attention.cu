@@ -1,0 +1,422 @@
+// K3: paged GQA decode attention, TMA-fed, warp-specialised flash-decoding.
+//
+// Work item = (live row, kv head, KV split of `chunk` tokens).  k_prep_decode
+// writes the (row, split) list each iteration; a persistent grid (2 CTAs per
+// SM) walks it.  Warp 4 is the producer: running up to kStages tiles ahead on
+// empty/full mbarriers, it issues per 64-token tile cp.async.bulk.tensor
+// loads of the kv head's K and V rows straight out of the paged pool (2-D
+// tensor map over kv[layer][page][k|v][head][slot][dim], 128-byte swizzle),
+// plus on an item's first tile a 1-D bulk copy of the GQA group's q rows, and
+// hands the item's metadata to the consumers through shared memory (all
+// global-memory latency of the work list lives in the producer).  Warps 0-3
+// consume: each owns 16 tokens of a tile, S = Q K^T and O += P V as mma.sync
+// m16n8k16 bf16 tiles with the q heads as the 16-row M side
+// (flash-attention-2 register layout, exp2 online softmax).  At an item's
+// end the 4 warps merge in a fixed order; rows with one split write the
+// output directly, multi-split rows are merged in split order by the last
+// CTA to finish (arrival counter, self-resetting): deterministic end to end.
+#include <cuda.h>
+#include <cuda_bf16.h>
+
+#include <cfloat>
+
+#include "model.cuh"
+
+namespace ab {
+
+namespace {
+
+constexpr float kLog2e = 1.4426950408889634f;
+constexpr int kTok = 64;        // tokens per tile
+constexpr int kCons = 4;        // consumer warps (16 tokens each)
+constexpr int kThreads = (kCons + 1) * 32;
+constexpr int kStages = 3;
+constexpr int kQSlots = 3;
+constexpr int kMergeRows = 8;   // GQA group <= 8
+
+struct Meta {
+  int row, kvh, sp, c0, c1, tile, ntiles, nsplit, qslot, done, pad0, pad1;
+};
+
+template <int HD>
+struct AttCfg {
+  static constexpr int kKV = kTok * HD * 2;  // K (or V) of one tile
+  static constexpr int kQ = kMergeRows * HD * 2;
+  static constexpr int oQ = kStages * 2 * kKV;
+  static constexpr int oZero = oQ + kQSlots * kQ;
+  static constexpr int oMerge = oZero + HD * 2;
+  static constexpr int oML = oMerge + kMergeRows * HD * 4;
+  static constexpr int oMeta = oML + kCons * 16 * 2 * 4;
+  static constexpr int oBar = oMeta + kStages * (int)sizeof(Meta);
+  static constexpr int kSmem = 1024 + oBar + 2 * kStages * 8;
+};
+
+__device__ __forceinline__ uint32_t su32(const void* p) { return static_cast<uint32_t>(__cvta_generic_to_shared(p)); }
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(su32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(su32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(su32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  uint32_t ok = 0;
+  do {
+    asm volatile(
+        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}"
+        : "=r"(ok)
+        : "r"(su32(bar)), "r"(parity)
+        : "memory");
+  } while (!ok);
+}
+__device__ __forceinline__ void tma_2d(const CUtensorMap* map, uint64_t* bar, void* dst, int x, int y) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];" ::"r"(
+          su32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(su32(bar)), "r"(x), "r"(y)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_1d(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   su32(dst)),
+               "l"(src), "r"(bytes), "r"(su32(bar))
+               : "memory");
+}
+__device__ __forceinline__ void cons_sync() { asm volatile("bar.sync 1, 128;" ::: "memory"); }
+
+__device__ __forceinline__ void ldsm_x4(uint32_t (&r)[4], uint32_t addr, bool trans) {
+  if (trans)
+    asm volatile("ldmatrix.sync.aligned.m8n8.x4.trans.shared.b16 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
+                 : "r"(addr));
+  else
+    asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
+                 : "r"(addr));
+}
+
+__device__ __forceinline__ void mma16816(float (&c)[4], const uint32_t (&a)[4], uint32_t b0, uint32_t b1) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+      "{%0,%1,%2,%3};"
+      : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
+      : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
+}
+
+__device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
+  const __nv_bfloat162 v = __floats2bfloat162_rn(lo, hi);
+  return *reinterpret_cast<const uint32_t*>(&v);
+}
+
+// byte offset of 16-byte chunk `ch` of row `r` in a TMA-swizzled [HD/64 halves][64 rows][128 B] tile
+__device__ __forceinline__ uint32_t tile_off(int r, int ch) {
+  return (uint32_t)((ch >> 3) * (kTok * 128) + r * 128 + (((ch & 7) ^ (r & 7)) << 4));
+}
+
+template <int HD>
+__global__ void __launch_bounds__(kThreads, 2)
+    k_decode_attn(const __grid_constant__ CUtensorMap kvmap, EngineDev e, ModelDev m, int layer,
+                  const bf16* __restrict__ q, bf16* __restrict__ out, float* __restrict__ part_o,
+                  float* __restrict__ part_ml, int max_splits, int chunk) {
+  using Cfg = AttCfg<HD>;
+  const Ctl* c = e.ctl;
+  if (c->stop) return;
+  const int b = c->b;
+  if (b <= 0) return;
+  const int total = m.split_prefix[b] * m.hk;
+  if ((int)blockIdx.x >= total) return;
+
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  float* sMerge = reinterpret_cast<float*>(base + Cfg::oMerge);  // [kMergeRows][HD]
+  float* sML = reinterpret_cast<float*>(base + Cfg::oML);        // [kCons][16][2]
+  Meta* meta = reinterpret_cast<Meta*>(base + Cfg::oMeta);
+  uint64_t* full = reinterpret_cast<uint64_t*>(base + Cfg::oBar);
+  uint64_t* empty = full + kStages;
+  __shared__ int s_last;
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int gq = m.gq;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kStages; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], kCons);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  for (int i = threadIdx.x; i < HD * 2 / 16; i += kThreads)
+    reinterpret_cast<uint4*>(base + Cfg::oZero)[i] = make_uint4(0, 0, 0, 0);
+  __syncthreads();
+
+  if (warp == kCons) {
+    // ------------------------------ producer ------------------------------
+    if (lane == 0) {
+      asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&kvmap)) : "memory");
+      const uint32_t qbytes = (uint32_t)(gq * HD * 2);
+      const int box_rows = m.P < kTok ? m.P : kTok;
+      int g = 0, k = 0;
+      for (int item = blockIdx.x; item < total; item += gridDim.x, ++k) {
+        const int rs = item / m.hk, kvh = item % m.hk;
+        const int packed = m.att_items[rs];
+        const int row = packed & 0xffff, sp = packed >> 16;
+        const int n = m.row_pos[row] + 1;
+        const int c0 = sp * chunk, c1 = min(n, c0 + chunk);
+        const int ntiles = (c1 - c0 + kTok - 1) / kTok;
+        const int32_t* bt = m.bt + (size_t)m.row_btrow[row] * m.MP;
+        const int qslot = k % kQSlots;
+        for (int t = 0; t < ntiles; ++t, ++g) {
+          const int st = g % kStages;
+          mbar_wait(&empty[st], ((g / kStages) & 1) ^ 1);
+          Meta mt;
+          mt.row = row;
+          mt.kvh = kvh;
+          mt.sp = sp;
+          mt.c0 = c0;
+          mt.c1 = c1;
+          mt.tile = t;
+          mt.ntiles = ntiles;
+          mt.nsplit = (n + chunk - 1) / chunk;
+          mt.qslot = qslot;
+          mt.done = 0;
+          meta[st] = mt;
+          uint8_t* sb = base + st * 2 * Cfg::kKV;
+          mbar_expect_tx(&full[st], 2 * Cfg::kKV + (t == 0 ? qbytes : 0u));
+          const int tok0 = c0 + t * kTok;
+          for (int r0 = 0; r0 < kTok; r0 += box_rows) {
+            const bool valid = tok0 + r0 < c1;
+            const int tok = valid ? tok0 + r0 : c1 - 1;  // past the end: reload a valid page (masked)
+            const int page = bt[tok / m.P];
+            const int slot = valid ? tok % m.P : 0;
+            const int64_t yk = ((((int64_t)layer * m.NP + page) * 2) * m.hk + kvh) * m.P + slot;
+            const int64_t yv = yk + (int64_t)m.hk * m.P;
+#pragma unroll
+            for (int h = 0; h < HD / 64; ++h) {
+              tma_2d(&kvmap, &full[st], sb + h * (kTok * 128) + r0 * 128, h * 64, (int)yk);
+              tma_2d(&kvmap, &full[st], sb + Cfg::kKV + h * (kTok * 128) + r0 * 128, h * 64, (int)yv);
+            }
+          }
+          if (t == 0)
+            bulk_1d(base + Cfg::oQ + qslot * Cfg::kQ, q + (size_t)row * m.qd + kvh * gq * HD, qbytes, &full[st]);
+        }
+      }
+      const int st = g % kStages;  // sentinel
+      mbar_wait(&empty[st], ((g / kStages) & 1) ^ 1);
+      meta[st].done = 1;
+      mbar_arrive(&full[st]);
+    }
+    return;
+  }
+
+  // ------------------------------ consumers ------------------------------
+  const int gr = lane >> 2, tq = lane & 3;
+  const float scale = rsqrtf((float)HD) * kLog2e;
+  float o[HD / 8][4];
+  float mrow[2] = {-FLT_MAX, -FLT_MAX}, lrow[2] = {0.f, 0.f};
+  uint32_t qa[HD / 16][4];
+  for (int g = 0;; ++g) {
+    const int st = g % kStages;
+    mbar_wait(&full[st], (g / kStages) & 1);
+    const Meta mt = meta[st];
+    if (mt.done) break;
+    const uint32_t K = su32(base + st * 2 * Cfg::kKV), V = K + Cfg::kKV;
+    if (mt.tile == 0) {
+#pragma unroll
+      for (int t = 0; t < HD / 8; ++t) o[t][0] = o[t][1] = o[t][2] = o[t][3] = 0.f;
+      mrow[0] = mrow[1] = -FLT_MAX;
+      lrow[0] = lrow[1] = 0.f;
+      const int r = lane & 15;
+      const uint32_t rowbase = r < gq ? su32(base + Cfg::oQ + mt.qslot * Cfg::kQ) + r * HD * 2
+                                      : su32(base + Cfg::oZero);
+#pragma unroll
+      for (int kk = 0; kk < HD / 16; ++kk) ldsm_x4(qa[kk], rowbase + (kk * 2 + (lane >> 4)) * 16, false);
+    }
+    const int tb = mt.c0 + mt.tile * kTok, wt = warp * 16;
+    float s[2][4] = {{0.f, 0.f, 0.f, 0.f}, {0.f, 0.f, 0.f, 0.f}};
+#pragma unroll
+    for (int kk = 0; kk < HD / 16; ++kk) {
+      const int mi = lane >> 3;
+      uint32_t bb[4];
+      ldsm_x4(bb, K + tile_off(wt + (mi >> 1) * 8 + (lane & 7), kk * 2 + (mi & 1)), false);
+      mma16816(s[0], qa[kk], bb[0], bb[1]);
+      mma16816(s[1], qa[kk], bb[2], bb[3]);
+    }
+    float mx[2] = {-FLT_MAX, -FLT_MAX};
+#pragma unroll
+    for (int j = 0; j < 2; ++j)
+#pragma unroll
+      for (int q4 = 0; q4 < 4; ++q4) {
+        const int tok = tb + wt + j * 8 + tq * 2 + (q4 & 1);
+        const float v = tok < mt.c1 ? s[j][q4] * scale : -FLT_MAX;
+        s[j][q4] = v;
+        mx[q4 >> 1] = fmaxf(mx[q4 >> 1], v);
+      }
+    float alpha[2];
+#pragma unroll
+    for (int r = 0; r < 2; ++r) {
+      mx[r] = fmaxf(mx[r], __shfl_xor_sync(0xffffffffu, mx[r], 1));
+      mx[r] = fmaxf(mx[r], __shfl_xor_sync(0xffffffffu, mx[r], 2));
+      const float mn = fmaxf(mrow[r], mx[r]);
+      alpha[r] = (mrow[r] == -FLT_MAX) ? 0.f : exp2f(mrow[r] - mn);
+      mrow[r] = mn;
+    }
+    float rsum[2] = {0.f, 0.f};
+#pragma unroll
+    for (int j = 0; j < 2; ++j)
+#pragma unroll
+      for (int q4 = 0; q4 < 4; ++q4) {
+        const int r = q4 >> 1;
+        const float p = (s[j][q4] == -FLT_MAX) ? 0.f : exp2f(s[j][q4] - mrow[r]);
+        s[j][q4] = p;
+        rsum[r] += p;
+      }
+#pragma unroll
+    for (int r = 0; r < 2; ++r) lrow[r] = lrow[r] * alpha[r] + rsum[r];
+#pragma unroll
+    for (int nt = 0; nt < HD / 8; ++nt) {
+      o[nt][0] *= alpha[0];
+      o[nt][1] *= alpha[0];
+      o[nt][2] *= alpha[1];
+      o[nt][3] *= alpha[1];
+    }
+    const uint32_t pa[4] = {pack_bf16(s[0][0], s[0][1]), pack_bf16(s[0][2], s[0][3]), pack_bf16(s[1][0], s[1][1]),
+                            pack_bf16(s[1][2], s[1][3])};
+#pragma unroll
+    for (int nt2 = 0; nt2 < HD / 16; ++nt2) {
+      const int mi = lane >> 3;
+      uint32_t bb[4];
+      ldsm_x4(bb, V + tile_off(wt + (mi & 1) * 8 + (lane & 7), nt2 * 2 + (mi >> 1)), true);
+      mma16816(o[2 * nt2], pa, bb[0], bb[1]);
+      mma16816(o[2 * nt2 + 1], pa, bb[2], bb[3]);
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[st]);  // this warp is done with the stage
+    if (mt.tile != mt.ntiles - 1) continue;
+
+    // ---- item complete: merge the 4 warps in a fixed order, then emit ----
+#pragma unroll
+    for (int r = 0; r < 2; ++r) {
+      lrow[r] += __shfl_xor_sync(0xffffffffu, lrow[r], 1);
+      lrow[r] += __shfl_xor_sync(0xffffffffu, lrow[r], 2);
+    }
+    if (tq == 0) {
+      sML[(warp * 16 + gr) * 2] = mrow[0];
+      sML[(warp * 16 + gr) * 2 + 1] = lrow[0];
+      sML[(warp * 16 + gr + 8) * 2] = mrow[1];
+      sML[(warp * 16 + gr + 8) * 2 + 1] = lrow[1];
+    }
+    cons_sync();
+    float sc = 0.f;
+    if (gr < gq) {
+      float M = -FLT_MAX;
+      for (int w = 0; w < kCons; ++w) M = fmaxf(M, sML[(w * 16 + gr) * 2]);
+      sc = mrow[0] == -FLT_MAX ? 0.f : exp2f(mrow[0] - M);
+    }
+    for (int w = 0; w < kCons; ++w) {
+      if (warp == w && gr < gq) {
+        float* dst = sMerge + gr * HD;
+#pragma unroll
+        for (int nt = 0; nt < HD / 8; ++nt) {
+          float2* p2 = reinterpret_cast<float2*>(dst + nt * 8 + tq * 2);
+          const float2 add = make_float2(o[nt][0] * sc, o[nt][1] * sc);
+          if (w == 0) {
+            *p2 = add;
+          } else {
+            float2 cur = *p2;
+            *p2 = make_float2(cur.x + add.x, cur.y + add.y);
+          }
+        }
+      }
+      cons_sync();
+    }
+    const int i = mt.row, kvh = mt.kvh, sp = mt.sp, nsplit = mt.nsplit;
+    for (int idx = threadIdx.x; idx < gq * HD; idx += kCons * 32) {
+      const int row = idx / HD, dcol = idx % HD;
+      float M = -FLT_MAX, L = 0.f;
+      for (int w = 0; w < kCons; ++w) M = fmaxf(M, sML[(w * 16 + row) * 2]);
+      for (int w = 0; w < kCons; ++w) {
+        const float mw = sML[(w * 16 + row) * 2];
+        if (mw != -FLT_MAX) L += sML[(w * 16 + row) * 2 + 1] * exp2f(mw - M);
+      }
+      const float acc = sMerge[row * HD + dcol];
+      const int head = kvh * gq + row;
+      if (nsplit == 1) {
+        out[(size_t)i * m.qd + head * HD + dcol] = __float2bfloat16(acc / L);
+      } else {
+        const size_t pb = ((size_t)i * m.hq + head) * max_splits + sp;
+        part_o[pb * HD + dcol] = acc;
+        if (dcol == 0) {
+          part_ml[pb * 2] = M;
+          part_ml[pb * 2 + 1] = L;
+        }
+      }
+    }
+    if (nsplit > 1) {
+      __threadfence();
+      cons_sync();
+      if (threadIdx.x == 0) {
+        const int old = atomicAdd(&m.att_counter[i * m.hk + kvh], 1);
+        s_last = (old == nsplit - 1);
+        if (s_last) m.att_counter[i * m.hk + kvh] = 0;
+      }
+      cons_sync();
+      if (s_last) {
+        __threadfence();
+        for (int idx = threadIdx.x; idx < gq * HD; idx += kCons * 32) {
+          const int row = idx / HD, dcol = idx % HD;
+          const int head = kvh * gq + row;
+          const size_t pb = ((size_t)i * m.hq + head) * max_splits;
+          float M = -FLT_MAX;
+          for (int s2 = 0; s2 < nsplit; ++s2) M = fmaxf(M, __ldcg(&part_ml[(pb + s2) * 2]));
+          float L = 0.f, acc = 0.f;
+          for (int s2 = 0; s2 < nsplit; ++s2) {
+            const float w = exp2f(__ldcg(&part_ml[(pb + s2) * 2]) - M);
+            L += __ldcg(&part_ml[(pb + s2) * 2 + 1]) * w;
+            acc += __ldcg(&part_o[(pb + s2) * HD + dcol]) * w;
+          }
+          out[(size_t)i * m.qd + head * HD + dcol] = __float2bfloat16(acc / L);
+        }
+      }
+    }
+    cons_sync();  // sML / sMerge are reused by the next item
+  }
+}
+
+template <int HD>
+void launch_t(const CUtensorMap& map, const EngineDev& e, const ModelDev& m, int layer, const bf16* q, bf16* out,
+              float* part_o, float* part_ml, int max_splits, int chunk, cudaStream_t s) {
+  static int grid = 0;
+  if (!grid) {
+    AB_CUDA(cudaFuncSetAttribute(k_decode_attn<HD>, cudaFuncAttributeMaxDynamicSharedMemorySize, AttCfg<HD>::kSmem));
+    int per_sm = 0, dev = 0, sms = 0;
+    AB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_decode_attn<HD>, kThreads, AttCfg<HD>::kSmem));
+    AB_CUDA(cudaGetDevice(&dev));
+    AB_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    grid = sms * (per_sm > 0 ? per_sm : 1);
+  }
+  k_decode_attn<HD><<<grid, kThreads, AttCfg<HD>::kSmem, s>>>(map, e, m, layer, q, out, part_o, part_ml, max_splits,
+                                                              chunk);
+}
+
+}  // namespace
+
+void make_kv_tmap(CUtensorMap* map, const ModelDev& m) {
+  AB_REQUIRE(m.gq <= kMergeRows, AB_ERR_CONFIG, "decode attention supports GQA groups of at most 8");
+  AB_REQUIRE(m.P % 8 == 0 && (m.P <= kTok ? kTok % m.P == 0 : m.P % kTok == 0), AB_ERR_CONFIG,
+             "page_size must divide 64 or be a multiple of 64");
+  const int64_t rows = (int64_t)m.L * m.NP * 2 * m.hk * m.P;
+  AB_REQUIRE(rows < (int64_t(1) << 31), AB_ERR_CONFIG, "KV pool too large for 32-bit TMA coordinates");
+  make_tmap_bf16(map, m.kv, rows, m.hd, m.hd, 64, m.P < kTok ? m.P : kTok);
+}
+
+void launch_decode_attention(const CUtensorMap& map, const EngineDev& e, const ModelDev& m, int layer, const bf16* q,
+                             bf16* out, float* part_o, float* part_ml, int max_splits, int chunk, cudaStream_t s) {
+  if (m.hd == 128)
+    launch_t<128>(map, e, m, layer, q, out, part_o, part_ml, max_splits, chunk, s);
+  else
+    launch_t<64>(map, e, m, layer, q, out, part_o, part_ml, max_splits, chunk, s);
+}
+
+}  // namespace ab

@@ -96,7 +96,10 @@ struct Cfg {
   static constexpr int kWBytes = kBM * kBK * 2;
   static constexpr int kABytes = BN * kBK * 2;
   static constexpr int kStageBytes = kWBytes + kABytes;
-  static constexpr int kStages = (kSmemBudget - 2048) / kStageBytes > 8 ? 8 : (kSmemBudget - 2048) / kStageBytes;
+  // decode tiles (BN <= 128) fit two CTAs per SM; prefill tiles take the whole SM for a deep ring
+  static constexpr int kBudget = kSmemBudget;
+  static constexpr int kMinBlocks = 1;
+  static constexpr int kStages = (kBudget - 2048) / kStageBytes > 8 ? 8 : (kBudget - 2048) / kStageBytes;
   static constexpr int kTmemCols = BN <= 32 ? 32 : BN <= 64 ? 64 : BN <= 128 ? 128 : 256;
   static constexpr int kSmem = kStages * kStageBytes + 1024 /*align*/ + 256 /*barriers*/;
   // kind::f16: D=f32 (bit 4), A=bf16 (bits 7-9 = 1), B=bf16 (bits 10-12 = 1), K-major both,
@@ -108,17 +111,30 @@ struct Cfg {
 __device__ __forceinline__ float silu(float x) { return x / (1.f + __expf(-x)); }
 
 template <int BN, int EPI>
-__global__ void __launch_bounds__(kThreads, 1)
+__global__ void __launch_bounds__(kThreads, Cfg<BN>::kMinBlocks)
     k_gemm_tc(const __grid_constant__ CUtensorMap tw, const __grid_constant__ CUtensorMap ta, int N, int K,
               int M_cap, const int* __restrict__ rows_dev, const int* __restrict__ stop_dev, void* __restrict__ out,
-              int64_t ldo, const __nv_bfloat16* __restrict__ bias) {
+              int64_t ldo, const __nv_bfloat16* __restrict__ bias, float* __restrict__ ws, int* __restrict__ cnt,
+              int max_splits, int target_ctas) {
   using C = Cfg<BN>;
   if (stop_dev && *stop_dev) return;
   const int rows = rows_dev ? min(*rows_dev, M_cap) : M_cap;
   const int n0 = blockIdx.x * kBM, m0 = blockIdx.y * BN;
   if (m0 >= rows) return;
+  // split-K sized from the live row count: enough CTAs to cover the SMs,
+  // at least two 64-wide K blocks per split
+  const int nk_all = K / kBK;
+  const int tiles = gridDim.x * ((rows + BN - 1) / BN);
+  // split only when the tiles leave most SMs idle (floor: never more CTAs than SMs)
+  int splits = max(1, target_ctas / tiles);
+  splits = min(splits, min(max_splits, max(1, nk_all / 2)));
+  while (splits > 1 && (int64_t)splits * rows * N > kGemmWsElems) --splits;
+  if ((int)blockIdx.z >= splits) return;
+  const int kb0 = (int)(((int64_t)nk_all * blockIdx.z) / splits);
+  const int kb1 = (int)(((int64_t)nk_all * (blockIdx.z + 1)) / splits);
 
   extern __shared__ uint8_t smem_raw[];
+  __shared__ int s_last_split;
   uint8_t* base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sW = base;
   uint8_t* sA = base + C::kStages * C::kWBytes;
@@ -147,7 +163,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   const uint32_t tmem = *tmem_slot;
-  const int nk = K / kBK;
+  const int nk = kb1 - kb0;
 
   if (warp == 0) {
     if (lane == 0) {
@@ -156,8 +172,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         const uint32_t ph = (kb / C::kStages) & 1;
         mbar_wait(&empty[s], ph ^ 1);
         mbar_expect_tx(&full[s], C::kStageBytes);
-        tma_load_2d(&tw, &full[s], sW + s * C::kWBytes, kb * kBK, n0);
-        tma_load_2d(&ta, &full[s], sA + s * C::kABytes, kb * kBK, m0);
+        tma_load_2d(&tw, &full[s], sW + s * C::kWBytes, (kb0 + kb) * kBK, n0);
+        tma_load_2d(&ta, &full[s], sA + s * C::kABytes, (kb0 + kb) * kBK, m0);
       }
     }
   } else if (warp == 1) {
@@ -182,13 +198,56 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int quad = warp & 3;
     const int lrow = quad * 32 + lane;  // TMEM lane = weight row within the tile
     const uint32_t taddr = tmem + ((uint32_t)(quad * 32) << 16);
-    if constexpr (EPI == kEpiSwiGLU) {
+    const bool split = splits > 1;
+    bool do_epi = true;
+    if (split) {
+      // deterministic split-K: partial tile -> workspace[split]; the last CTA of
+      // the tile sums the partials in split order and runs the epilogue
+      const int n = n0 + lrow;
+      for (int c0 = 0; c0 < BN; c0 += 32) {
+        float v[32];
+        tmem_ld32(taddr + c0, v);
+#pragma unroll
+        for (int c = 0; c < 32; ++c) {
+          const int m = m0 + c0 + c;
+          if (m < rows) ws[((int64_t)blockIdx.z * rows + m) * N + n] = v[c];
+        }
+      }
+      __threadfence();
+      asm volatile("bar.sync 1, 128;" ::: "memory");
+      if (threadIdx.x == 64) {
+        const int tile = blockIdx.y * gridDim.x + blockIdx.x;
+        const int old = atomicAdd(&cnt[tile], 1);
+        s_last_split = (old == splits - 1);
+        if (s_last_split) cnt[tile] = 0;
+      }
+      asm volatile("bar.sync 1, 128;" ::: "memory");
+      do_epi = s_last_split != 0;
+      if (do_epi) __threadfence();
+    }
+    auto fetch = [&](int c0, float (&v)[32]) {
+      if (!split) {
+        tmem_ld32(taddr + c0, v);
+        return;
+      }
+      const int n = n0 + lrow;
+#pragma unroll 4
+      for (int c = 0; c < 32; ++c) {
+        const int m = m0 + c0 + c;
+        float acc = 0.f;
+        if (m < rows)
+          for (int z = 0; z < splits; ++z) acc += __ldcg(&ws[((int64_t)z * rows + m) * N + n]);
+        v[c] = acc;
+      }
+    };
+    if (!do_epi) {
+    } else if constexpr (EPI == kEpiSwiGLU) {
       // lanes 0-63: gate rows, lanes 64-127: up rows of the same 64 features
       float* xchg = reinterpret_cast<float*>(sW);  // pipeline smem is idle now
       const int j = (n0 >> 1) + (lrow & 63);
       for (int c0 = 0; c0 < BN; c0 += 32) {
         float v[32];
-        tmem_ld32(taddr + c0, v);
+        fetch(c0, v);
         if (lrow >= 64) {
 #pragma unroll
           for (int c = 0; c < 32; ++c) xchg[c * 64 + (lrow - 64)] = v[c];
@@ -210,18 +269,32 @@ __global__ void __launch_bounds__(kThreads, 1)
       if (EPI == kEpiBF16 && bias != nullptr && n < N) bv = __bfloat162float(bias[n]);
       for (int c0 = 0; c0 < BN; c0 += 32) {
         float v[32];
-        tmem_ld32(taddr + c0, v);
+        fetch(c0, v);
         if (n < N) {
+          if constexpr (EPI == kEpiAddF32) {
+            // residual add: issue all 32 loads before any store (independent, in flight together)
+            float* o = reinterpret_cast<float*>(out);
+            float old[32];
 #pragma unroll
-          for (int c = 0; c < 32; ++c) {
-            const int m = m0 + c0 + c;
-            if (m < rows) {
-              if constexpr (EPI == kEpiBF16) {
-                reinterpret_cast<__nv_bfloat16*>(out)[(int64_t)m * ldo + n] = __float2bfloat16(v[c] + bv);
-              } else if constexpr (EPI == kEpiF32) {
-                reinterpret_cast<float*>(out)[(int64_t)m * ldo + n] = v[c];
-              } else {
-                reinterpret_cast<float*>(out)[(int64_t)m * ldo + n] += v[c];
+            for (int c = 0; c < 32; ++c) {
+              const int m = m0 + c0 + c;
+              old[c] = m < rows ? __ldcg(o + (int64_t)m * ldo + n) : 0.f;
+            }
+#pragma unroll
+            for (int c = 0; c < 32; ++c) {
+              const int m = m0 + c0 + c;
+              if (m < rows) o[(int64_t)m * ldo + n] = old[c] + v[c];
+            }
+          } else {
+#pragma unroll
+            for (int c = 0; c < 32; ++c) {
+              const int m = m0 + c0 + c;
+              if (m < rows) {
+                if constexpr (EPI == kEpiBF16) {
+                  reinterpret_cast<__nv_bfloat16*>(out)[(int64_t)m * ldo + n] = __float2bfloat16(v[c] + bv);
+                } else {
+                  reinterpret_cast<float*>(out)[(int64_t)m * ldo + n] = v[c];
+                }
               }
             }
           }
@@ -275,9 +348,17 @@ void launch_t(const GemmPlan& p, cudaStream_t s) {
     AB_CUDA(cudaFuncSetAttribute(k_gemm_tc<BN, EPI>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmem));
     attr = true;
   }
-  dim3 grid(ceil_div(p.N, kBM), ceil_div(p.M_cap, BN));
+  static int target = 0;
+  if (!target) {
+    int dev = 0, sms = 0;
+    AB_CUDA(cudaGetDevice(&dev));
+    AB_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    target = sms * C::kMinBlocks;
+  }
+  const int zs = (p.ws && p.cnt) ? p.max_splits : 1;
+  dim3 grid(ceil_div(p.N, kBM), ceil_div(p.M_cap, BN), zs);
   k_gemm_tc<BN, EPI><<<grid, kThreads, C::kSmem, s>>>(p.tw, p.ta, p.N, p.K, p.M_cap, p.rows_dev, p.stop_dev, p.out,
-                                                      p.ldo, p.bias);
+                                                      p.ldo, p.bias, p.ws, p.cnt, zs, target);
 }
 
 template <int BN>
@@ -294,8 +375,15 @@ void launch_bn(const GemmPlan& p, cudaStream_t s) {
 
 void gemm_plan(GemmPlan& p, const __nv_bfloat16* W, int N, int K, const __nv_bfloat16* A, int M_cap, int64_t lda,
                int BN, int epi, void* out, int64_t ldo, const __nv_bfloat16* bias, const int* rows_dev,
-               const int* stop_dev) {
+               const int* stop_dev, float* ws, int* cnt, int max_splits) {
   AB_REQUIRE(K % kBK == 0, AB_ERR_CONFIG, "GEMM K must be a multiple of 64");
+  AB_REQUIRE(max_splits >= 1 && max_splits <= 16, AB_ERR_CONFIG, "GEMM max_splits must be in [1, 16]");
+  AB_REQUIRE(max_splits == 1 || (ws && cnt), AB_ERR_CONFIG, "split-K needs a workspace");
+  AB_REQUIRE((int64_t)ceil_div(N, kBM) * ceil_div(M_cap, BN) <= kGemmCounters, AB_ERR_CONFIG,
+             "GEMM tile count exceeds the split-K counter array");
+  p.ws = ws;
+  p.cnt = cnt;
+  p.max_splits = max_splits;
   AB_REQUIRE(N % kBM == 0, AB_ERR_CONFIG, "GEMM N must be a multiple of 128");
   AB_REQUIRE(BN == 32 || BN == 64 || BN == 128 || BN == 256, AB_ERR_CONFIG, "GEMM BN must be 32/64/128/256");
   p.N = N;
@@ -312,6 +400,18 @@ void gemm_plan(GemmPlan& p, const __nv_bfloat16* W, int N, int K, const __nv_bfl
   make_map(&p.ta, A, M_cap, K, lda, BN);
 }
 
+void make_tmap_bf16(CUtensorMap* m, const void* ptr, int64_t rows, int64_t cols, int64_t ld, int box_cols,
+                    int box_rows) {
+  cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
+  cuuint64_t strides[1] = {(cuuint64_t)(ld * 2)};
+  cuuint32_t box[2] = {(cuuint32_t)box_cols, (cuuint32_t)box_rows};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = encode_fn()(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(ptr), dims, strides, box, estr,
+                           CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                           CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  AB_REQUIRE(r == CUDA_SUCCESS, AB_ERR_CUDA, "cuTensorMapEncodeTiled (KV) failed (" + std::to_string((int)r) + ")");
+}
+
 void gemm_launch(const GemmPlan& p, cudaStream_t s) {
   switch (p.BN) {
     case 32: launch_bn<32>(p, s); break;
@@ -326,10 +426,21 @@ void gemm_launch(const GemmPlan& p, cudaStream_t s) {
 // Test entry: one GEMM on caller-provided device buffers (tests/test_kernels_gpu.py).
 extern "C" int ab_debug_gemm(const void* W, const void* A, void* out, const void* bias, int N, int K, int M, int BN,
                              int epi) {
+  // epi >= 16: the same epilogue (epi - 16) with split-K enabled (up to 8 splits)
   try {
+    static float* ws = nullptr;
+    static int* cnt = nullptr;
+    const int max_splits = epi >= 16 ? 8 : 1;
+    epi &= 15;
+    if (max_splits > 1 && !ws) {
+      AB_CUDA(cudaMalloc(&ws, sizeof(float) * ab::kGemmWsElems));
+      AB_CUDA(cudaMalloc(&cnt, sizeof(int) * ab::kGemmCounters));
+      AB_CUDA(cudaMemset(cnt, 0, sizeof(int) * ab::kGemmCounters));
+    }
     ab::GemmPlan p;
     ab::gemm_plan(p, (const __nv_bfloat16*)W, N, K, (const __nv_bfloat16*)A, M, K, BN, epi, out,
-                  epi == ab::kEpiSwiGLU ? N / 2 : N, (const __nv_bfloat16*)bias, nullptr, nullptr);
+                  epi == ab::kEpiSwiGLU ? N / 2 : N, (const __nv_bfloat16*)bias, nullptr, nullptr,
+                  max_splits > 1 ? ws : nullptr, max_splits > 1 ? cnt : nullptr, max_splits);
     ab::gemm_launch(p, 0);
     AB_CUDA(cudaGetLastError());
     AB_CUDA(cudaDeviceSynchronize());

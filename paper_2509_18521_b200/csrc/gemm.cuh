@@ -29,12 +29,24 @@ struct GemmPlan {
   const __nv_bfloat16* bias = nullptr;
   const int* rows_dev = nullptr;  // live row count on device (nullptr: M_cap)
   const int* stop_dev = nullptr;  // engine stop flag (nullptr: never stop)
-  int splits = 1;                 // split-K factor (kEpiAddF32 / kEpiF32-atomic only)
+  // deterministic split-K (decode GEMMs whose tile count cannot fill the SMs):
+  // the kernel picks splits <= max_splits from the live row count on device
+  float* ws = nullptr;  // shared workspace (kWsElems fp32), stream-ordered
+  int* cnt = nullptr;   // per-tile arrival counters (>= N/128 * M_cap/BN, zeroed once)
+  int max_splits = 1;
 };
+
+constexpr int64_t kGemmWsElems = int64_t(32) << 20;
+constexpr int kGemmCounters = 1 << 16;
 
 void gemm_plan(GemmPlan& p, const __nv_bfloat16* W, int N, int K, const __nv_bfloat16* A, int M_cap, int64_t lda,
                int BN, int epi, void* out, int64_t ldo, const __nv_bfloat16* bias, const int* rows_dev,
-               const int* stop_dev);
+               const int* stop_dev, float* ws = nullptr, int* cnt = nullptr, int max_splits = 1);
 void gemm_launch(const GemmPlan& p, cudaStream_t s);
+
+// 2-D bf16 TMA map: [rows, cols] with leading dimension `ld` elements, box {box_cols, box_rows},
+// 128-byte swizzle (box_cols * 2 must be <= 128).
+void make_tmap_bf16(CUtensorMap* m, const void* ptr, int64_t rows, int64_t cols, int64_t ld, int box_cols,
+                    int box_rows);
 
 }  // namespace ab

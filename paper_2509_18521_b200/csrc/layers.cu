@@ -1,7 +1,8 @@
-// Decoder kernels around the tcgen05 GEMMs: weight init, embedding,
-// RMSNorm, q/k-norm + RoPE + paged KV write, paged GQA decode attention
-// (split-KV, mma.sync bf16 tiles staged by cp.async into swizzled smem),
-// causal prefill attention for prompt groups, and KV page management.
+// Decoder kernels around the tcgen05 GEMMs and the paged attention
+// (attention.cu): weight init, per-iteration row preparation + KV page
+// allocation + attention work list, embedding, RMSNorm, q/k-norm + RoPE +
+// paged KV write, causal prefill attention for prompt groups, and KV page
+// management.
 //
 // None of this has a reference counterpart (the reference decode engine is a
 // cost model, src/april_sim/engine.py:167-171); numerics are pinned by the
@@ -60,27 +61,72 @@ __device__ __forceinline__ int pop_page(Ctl* c) {
   return old - 1 >= 0 ? (int)(old - 1) : -1;
 }
 
-__global__ void k_prep_decode(EngineDev e, ModelDev m) {
+// Single block: per live row, gather (token, position, block-table row),
+// allocate a KV page when the row crosses a page boundary, and build the
+// attention work list (exclusive prefix of KV splits per row).
+constexpr int kPrepThreads = 1024;
+
+__global__ void __launch_bounds__(kPrepThreads) k_prep_decode(EngineDev e, ModelDev m, int chunk) {
   Ctl* c = e.ctl;
   if (c->stop) return;
-  const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= c->b) return;
-  const int h = e.slot_handle[i];
-  const int pos = m.h_ctx[h];
-  m.row_tok[i] = m.h_last_tok[h];
-  m.row_pos[i] = pos;
-  m.row_btrow[i] = h;
-  if (c->run_iters < e.it_cap)
-    atomicAdd(reinterpret_cast<unsigned long long*>(&e.it_ctx[c->run_iters]), (unsigned long long)(pos + 1));
-  if (pos % m.P == 0) {
-    const int idx = pop_page(c);
-    if (idx < 0 || pos / m.P >= m.MP) {
-      atomicCAS(&c->error, kErrNone, kErrOutOfKV);
-      c->stop = 1;
-      c->stop_reason = -2;
-      return;
+  const int b = c->b;
+  const int ipt = (b + kPrepThreads - 1) / kPrepThreads;
+  const int beg = min(b, (int)threadIdx.x * ipt), end = min(b, beg + ipt);
+  int nsp = 0;
+  unsigned long long ctx_sum = 0;
+  bool fail = false;
+  for (int i = beg; i < end; ++i) {
+    const int h = e.slot_handle[i];
+    const int pos = m.h_ctx[h];
+    m.row_tok[i] = m.h_last_tok[h];
+    m.row_pos[i] = pos;
+    m.row_btrow[i] = h;
+    ctx_sum += (unsigned long long)(pos + 1);
+    nsp += (pos + chunk) / chunk;  // ceil((pos + 1) / chunk)
+    if (pos % m.P == 0) {
+      const int idx = pop_page(c);
+      if (idx < 0 || pos / m.P >= m.MP) {
+        fail = true;
+      } else {
+        m.bt[(size_t)h * m.MP + pos / m.P] = m.free_pages[idx];
+      }
     }
-    m.bt[(size_t)h * m.MP + pos / m.P] = m.free_pages[idx];
+  }
+  // exclusive scan of split counts
+  __shared__ int s_w[32];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  int x = nsp;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x += y;
+  }
+  if (lane == 31) s_w[w] = x;
+  __syncthreads();
+  if (w == 0) {
+    int v = s_w[lane];
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu, v, o);
+      if (lane >= o) v += y;
+    }
+    s_w[lane] = v;
+  }
+  __syncthreads();
+  int run = (w ? s_w[w - 1] : 0) + x - nsp;
+  for (int i = beg; i < end; ++i) {
+    m.split_prefix[i] = run;
+    const int ns = (m.row_pos[i] + chunk) / chunk;
+    for (int s = 0; s < ns; ++s) m.att_items[run + s] = i | (s << 16);  // explicit (row, split) work list
+    run += ns;
+  }
+  if (threadIdx.x == kPrepThreads - 1) m.split_prefix[b] = s_w[31];
+  if (c->run_iters < e.it_cap && ctx_sum)
+    atomicAdd(reinterpret_cast<unsigned long long*>(&e.it_ctx[c->run_iters]), ctx_sum);
+  if (fail) {
+    atomicCAS(&c->error, kErrNone, kErrOutOfKV);
+    c->stop = 1;
+    c->stop_reason = -2;
   }
 }
 
@@ -198,280 +244,6 @@ __global__ void k_rope_kv(ModelDev m, int layer, const bf16* __restrict__ qkv, c
       dst[lane * NP + j + HD / 2] = __float2bfloat16(ob[j]);
     }
   }
-}
-
-// ---------------------------------------------------------------------------
-// paged GQA decode attention: one CTA per (slot, kv head, KV split)
-// ---------------------------------------------------------------------------
-
-__device__ __forceinline__ void cp_async16(void* dst, const void* src, bool valid) {
-  const uint32_t d = static_cast<uint32_t>(__cvta_generic_to_shared(dst));
-  const int n = valid ? 16 : 0;
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(d), "l"(src), "r"(n) : "memory");
-}
-__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
-template <int N>
-__device__ __forceinline__ void cp_wait() {
-  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
-}
-
-__device__ __forceinline__ void ldsm_x4(uint32_t& r0, uint32_t& r1, uint32_t& r2, uint32_t& r3, const void* p) {
-  const uint32_t a = static_cast<uint32_t>(__cvta_generic_to_shared(p));
-  asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];"
-               : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3)
-               : "r"(a));
-}
-__device__ __forceinline__ void ldsm_x4_t(uint32_t& r0, uint32_t& r1, uint32_t& r2, uint32_t& r3, const void* p) {
-  const uint32_t a = static_cast<uint32_t>(__cvta_generic_to_shared(p));
-  asm volatile("ldmatrix.sync.aligned.m8n8.x4.trans.shared.b16 {%0,%1,%2,%3}, [%4];"
-               : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3)
-               : "r"(a));
-}
-
-__device__ __forceinline__ void mma16816(float (&c)[4], const uint32_t (&a)[4], uint32_t b0, uint32_t b1) {
-  asm volatile(
-      "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
-      "{%0,%1,%2,%3};"
-      : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
-      : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
-}
-
-__device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
-  const __nv_bfloat162 v = __floats2bfloat162_rn(lo, hi);
-  return *reinterpret_cast<const uint32_t*>(&v);
-}
-
-constexpr int kAttTok = 64;     // tokens per smem tile
-constexpr int kAttThreads = 128;
-
-// swizzled offset (elements) of 16-byte chunk `ch` of row `row` in a [kAttTok][HD] bf16 tile
-template <int HD>
-__device__ __forceinline__ int swz(int row, int ch) {
-  return row * HD + ((ch ^ (row & 7)) << 3);
-}
-
-template <int HD>
-__device__ __forceinline__ void load_tile(const ModelDev& m, int layer, int kvh, const int32_t* bt, int tb, int te,
-                                          bf16* sK, bf16* sV) {
-  constexpr int CH = HD / 8;  // 16-byte chunks per row
-  for (int c = threadIdx.x; c < kAttTok * CH; c += kAttThreads) {
-    const int row = c / CH, ch = c % CH;
-    const int tok = tb + row;
-    const bool ok = tok < te;
-    const int t = ok ? tok : tb;
-    const int page = bt[t / m.P], slot = t % m.P;
-    const bf16* k = m.kv + m.kv_off(layer, page, 0, kvh, slot) + ch * 8;
-    const bf16* v = m.kv + m.kv_off(layer, page, 1, kvh, slot) + ch * 8;
-    cp_async16(sK + swz<HD>(row, ch), k, ok);
-    cp_async16(sV + swz<HD>(row, ch), v, ok);
-  }
-}
-
-template <int HD>
-__global__ void __launch_bounds__(kAttThreads) k_decode_attn(EngineDev e, ModelDev m, int layer,
-                                                           const bf16* __restrict__ q, float* __restrict__ part_o,
-                                                           float* __restrict__ part_ml, int max_splits, int chunk) {
-  const Ctl* c = e.ctl;
-  if (c->stop) return;
-  const int i = blockIdx.x;
-  if (i >= c->b) return;
-  const int kvh = blockIdx.y, sp = blockIdx.z;
-  const int n = m.row_pos[i] + 1;
-  const int c0 = sp * chunk;
-  if (c0 >= n) return;
-  const int c1 = min(n, c0 + chunk);
-  const int32_t* bt = m.bt + (size_t)m.row_btrow[i] * m.MP;
-
-  extern __shared__ __align__(128) uint8_t att_smem[];
-  bf16* sQ = reinterpret_cast<bf16*>(att_smem);  // [16][HD]
-  bf16* sK = sQ + 16 * HD;                        // [2][kAttTok][HD]
-  bf16* sV = sK + 2 * kAttTok * HD;
-  float* sRed = reinterpret_cast<float*>(sV + 2 * kAttTok * HD);  // [4 warps][16 rows][2] + [16][HD]
-
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int gq = m.gq;
-  // Q rows (gq valid, rest zero), unswizzled row-major [16][HD]
-  for (int idx = threadIdx.x; idx < 16 * HD / 8; idx += kAttThreads) {
-    const int row = idx / (HD / 8), ch = idx % (HD / 8);
-    uint4 v = make_uint4(0, 0, 0, 0);
-    if (row < gq) v = *reinterpret_cast<const uint4*>(q + (size_t)i * m.qd + (kvh * gq + row) * HD + ch * 8);
-    *reinterpret_cast<uint4*>(sQ + swz<HD>(row, ch)) = v;
-  }
-  const int ntiles = (c1 - c0 + kAttTok - 1) / kAttTok;
-  load_tile<HD>(m, layer, kvh, bt, c0, c1, sK, sV);
-  cp_commit();
-  __syncthreads();
-
-  // Q fragments (A operand, 16 x HD), held for the whole chunk
-  uint32_t qa[HD / 16][4];
-#pragma unroll
-  for (int kk = 0; kk < HD / 16; ++kk) {
-    const int row = (lane & 15), ch = kk * 2 + (lane >> 4);
-    ldsm_x4(qa[kk][0], qa[kk][1], qa[kk][2], qa[kk][3], sQ + swz<HD>(row, ch));
-  }
-  const float scale = rsqrtf((float)HD) * kLog2e;
-  float o[HD / 8][4];
-#pragma unroll
-  for (int t = 0; t < HD / 8; ++t) o[t][0] = o[t][1] = o[t][2] = o[t][3] = 0.f;
-  float mrow[2] = {-FLT_MAX, -FLT_MAX}, lrow[2] = {0.f, 0.f};
-  const int gr = lane >> 2, tq = lane & 3;
-
-  for (int t = 0; t < ntiles; ++t) {
-    const int tb = c0 + t * kAttTok;
-    if (t + 1 < ntiles) {
-      load_tile<HD>(m, layer, kvh, bt, tb + kAttTok, c1, sK + ((t + 1) & 1) * kAttTok * HD,
-                    sV + ((t + 1) & 1) * kAttTok * HD);
-      cp_commit();
-      cp_wait<1>();
-    } else {
-      cp_wait<0>();
-    }
-    __syncthreads();
-    const bf16* K = sK + (t & 1) * kAttTok * HD;
-    const bf16* Vt = sV + (t & 1) * kAttTok * HD;
-    // S = Q K^T for this warp's 16 tokens (two n-tiles of 8)
-    float s[2][4] = {{0.f, 0.f, 0.f, 0.f}, {0.f, 0.f, 0.f, 0.f}};
-    const int wt = warp * 16;
-#pragma unroll
-    for (int kk = 0; kk < HD / 16; ++kk) {
-      const int mi = lane >> 3, rr = lane & 7;
-      const int tok = wt + (mi >> 1) * 8 + rr, ch = kk * 2 + (mi & 1);
-      uint32_t b0, b1, b2, b3;
-      ldsm_x4(b0, b1, b2, b3, K + swz<HD>(tok, ch));
-      mma16816(s[0], qa[kk], b0, b1);
-      mma16816(s[1], qa[kk], b2, b3);
-    }
-    // scale + mask, online softmax over rows gr and gr+8
-    float mx[2] = {-FLT_MAX, -FLT_MAX};
-#pragma unroll
-    for (int j = 0; j < 2; ++j)
-#pragma unroll
-      for (int q4 = 0; q4 < 4; ++q4) {
-        const int tok = tb + wt + j * 8 + tq * 2 + (q4 & 1);
-        const float v = tok < c1 ? s[j][q4] * scale : -FLT_MAX;
-        s[j][q4] = v;
-        mx[q4 >> 1] = fmaxf(mx[q4 >> 1], v);
-      }
-    float alpha[2];
-#pragma unroll
-    for (int r = 0; r < 2; ++r) {
-      mx[r] = fmaxf(mx[r], __shfl_xor_sync(0xffffffffu, mx[r], 1));
-      mx[r] = fmaxf(mx[r], __shfl_xor_sync(0xffffffffu, mx[r], 2));
-      const float mn = fmaxf(mrow[r], mx[r]);
-      alpha[r] = (mrow[r] == -FLT_MAX) ? 0.f : exp2f(mrow[r] - mn);
-      mrow[r] = mn;
-    }
-    float rs[2] = {0.f, 0.f};
-#pragma unroll
-    for (int j = 0; j < 2; ++j)
-#pragma unroll
-      for (int q4 = 0; q4 < 4; ++q4) {
-        const int r = q4 >> 1;
-        const float p = (s[j][q4] == -FLT_MAX || mrow[r] == -FLT_MAX) ? 0.f : exp2f(s[j][q4] - mrow[r]);
-        s[j][q4] = p;
-        rs[r] += p;
-      }
-#pragma unroll
-    for (int r = 0; r < 2; ++r) lrow[r] = lrow[r] * alpha[r] + rs[r];
-#pragma unroll
-    for (int nt = 0; nt < HD / 8; ++nt) {
-      o[nt][0] *= alpha[0];
-      o[nt][1] *= alpha[0];
-      o[nt][2] *= alpha[1];
-      o[nt][3] *= alpha[1];
-    }
-    // O += P V  (A = P from the S accumulators, B = V via ldmatrix.trans)
-    uint32_t pa[4];
-    pa[0] = pack_bf16(s[0][0], s[0][1]);
-    pa[1] = pack_bf16(s[0][2], s[0][3]);
-    pa[2] = pack_bf16(s[1][0], s[1][1]);
-    pa[3] = pack_bf16(s[1][2], s[1][3]);
-#pragma unroll
-    for (int nt2 = 0; nt2 < HD / 16; ++nt2) {
-      const int mi = lane >> 3, rr = lane & 7;
-      const int tok = wt + (mi & 1) * 8 + rr, ch = nt2 * 2 + (mi >> 1);
-      uint32_t b0, b1, b2, b3;
-      ldsm_x4_t(b0, b1, b2, b3, Vt + swz<HD>(tok, ch));
-      mma16816(o[2 * nt2], pa, b0, b1);
-      mma16816(o[2 * nt2 + 1], pa, b2, b3);
-    }
-    __syncthreads();  // the buffer is refilled next round
-  }
-  // row sums across the quad
-#pragma unroll
-  for (int r = 0; r < 2; ++r) {
-    lrow[r] += __shfl_xor_sync(0xffffffffu, lrow[r], 1);
-    lrow[r] += __shfl_xor_sync(0xffffffffu, lrow[r], 2);
-  }
-  // combine the 4 warps (each saw a different 16-token slice of every tile)
-  float* sML = sRed;                 // [4][16][2]
-  float* sO = sRed + 4 * 16 * 2;     // [16][HD]
-  if (tq == 0) {
-    sML[(warp * 16 + gr) * 2 + 0] = mrow[0];
-    sML[(warp * 16 + gr) * 2 + 1] = lrow[0];
-    sML[(warp * 16 + gr + 8) * 2 + 0] = mrow[1];
-    sML[(warp * 16 + gr + 8) * 2 + 1] = lrow[1];
-  }
-  for (int idx = threadIdx.x; idx < 16 * HD; idx += kAttThreads) sO[idx] = 0.f;
-  __syncthreads();
-  float wsc[2];
-#pragma unroll
-  for (int r = 0; r < 2; ++r) {
-    const int row = gr + r * 8;
-    float M = -FLT_MAX;
-    for (int w = 0; w < 4; ++w) M = fmaxf(M, sML[(w * 16 + row) * 2]);
-    wsc[r] = mrow[r] == -FLT_MAX ? 0.f : exp2f(mrow[r] - M);
-  }
-#pragma unroll
-  for (int nt = 0; nt < HD / 8; ++nt) {
-    const int col = nt * 8 + tq * 2;
-    atomicAdd(&sO[gr * HD + col], o[nt][0] * wsc[0]);
-    atomicAdd(&sO[gr * HD + col + 1], o[nt][1] * wsc[0]);
-    atomicAdd(&sO[(gr + 8) * HD + col], o[nt][2] * wsc[1]);
-    atomicAdd(&sO[(gr + 8) * HD + col + 1], o[nt][3] * wsc[1]);
-  }
-  __syncthreads();
-  // partial (unnormalised O, m, l) for this split
-  for (int idx = threadIdx.x; idx < gq * HD; idx += kAttThreads) {
-    const int row = idx / HD, dcol = idx % HD;
-    const size_t base = ((size_t)i * m.hq + kvh * gq + row) * max_splits + sp;
-    part_o[base * HD + dcol] = sO[row * HD + dcol];
-  }
-  if (threadIdx.x < gq) {
-    const int row = threadIdx.x;
-    float M = -FLT_MAX, L = 0.f;
-    for (int w = 0; w < 4; ++w) M = fmaxf(M, sML[(w * 16 + row) * 2]);
-    for (int w = 0; w < 4; ++w) {
-      const float mw = sML[(w * 16 + row) * 2];
-      if (mw != -FLT_MAX) L += sML[(w * 16 + row) * 2 + 1] * exp2f(mw - M);
-    }
-    const size_t base = ((size_t)i * m.hq + kvh * gq + row) * max_splits + sp;
-    part_ml[base * 2 + 0] = M;
-    part_ml[base * 2 + 1] = L;
-  }
-}
-
-template <int HD>
-__global__ void k_attn_combine(EngineDev e, ModelDev m, const float* __restrict__ part_o,
-                               const float* __restrict__ part_ml, bf16* __restrict__ out, int max_splits, int chunk) {
-  const Ctl* c = e.ctl;
-  if (c->stop) return;
-  const int i = blockIdx.x;
-  if (i >= c->b) return;
-  const int head = blockIdx.y;
-  const int n = m.row_pos[i] + 1;
-  const int ns = (n + chunk - 1) / chunk;
-  const size_t base = ((size_t)i * m.hq + head) * max_splits;
-  float M = -FLT_MAX;
-  for (int s = 0; s < ns; ++s) M = fmaxf(M, part_ml[(base + s) * 2]);
-  float L = 0.f, acc = 0.f;
-  const int dcol = threadIdx.x;
-  for (int s = 0; s < ns; ++s) {
-    const float w = exp2f(part_ml[(base + s) * 2] - M);
-    L += part_ml[(base + s) * 2 + 1] * w;
-    acc += part_o[(base + s) * HD + dcol] * w;
-  }
-  out[(size_t)i * m.qd + head * HD + dcol] = __float2bfloat16(acc / L);
 }
 
 // ---------------------------------------------------------------------------
@@ -639,8 +411,8 @@ void launch_rope_table(float2* rope, int max_pos, int hd, float theta, cudaStrea
   AB_CUDA(cudaGetLastError());
 }
 
-void launch_prep_decode(const EngineDev& e, const ModelDev& m, cudaStream_t s) {
-  k_prep_decode<<<ceil_div(e.S, 128), 128, 0, s>>>(e, m);
+void launch_prep_decode(const EngineDev& e, const ModelDev& m, int chunk, cudaStream_t s) {
+  k_prep_decode<<<1, kPrepThreads, 0, s>>>(e, m, chunk);
 }
 
 void launch_embed(const ModelDev& m, const bf16* emb, float* x, const int* rows_dev, int rows_cap, const int* stop,
@@ -659,28 +431,6 @@ void launch_rope_kv(const ModelDev& m, int layer, const bf16* qkv, const bf16* q
     k_rope_kv<128><<<rows_cap, 256, 0, s>>>(m, layer, qkv, q_norm, k_norm, q_out, rows_dev, rows_cap, stop);
   else
     k_rope_kv<64><<<rows_cap, 256, 0, s>>>(m, layer, qkv, q_norm, k_norm, q_out, rows_dev, rows_cap, stop);
-}
-
-template <int HD>
-static void decode_attn_t(const EngineDev& e, const ModelDev& m, int layer, const bf16* q, bf16* out, float* part_o,
-                          float* part_ml, int max_splits, int chunk, cudaStream_t s) {
-  const int smem = (16 * HD + 4 * kAttTok * HD) * 2 + (4 * 16 * 2 + 16 * HD) * 4;
-  static bool attr = false;
-  if (!attr) {
-    AB_CUDA(cudaFuncSetAttribute(k_decode_attn<HD>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-    attr = true;
-  }
-  k_decode_attn<HD><<<dim3(e.S, m.hk, max_splits), kAttThreads, smem, s>>>(e, m, layer, q, part_o, part_ml,
-                                                                           max_splits, chunk);
-  k_attn_combine<HD><<<dim3(e.S, m.hq), HD, 0, s>>>(e, m, part_o, part_ml, out, max_splits, chunk);
-}
-
-void launch_decode_attention(const EngineDev& e, const ModelDev& m, int layer, const bf16* q, bf16* out,
-                             float* part_o, float* part_ml, int max_splits, int chunk, cudaStream_t s) {
-  if (m.hd == 128)
-    decode_attn_t<128>(e, m, layer, q, out, part_o, part_ml, max_splits, chunk, s);
-  else
-    decode_attn_t<64>(e, m, layer, q, out, part_o, part_ml, max_splits, chunk, s);
 }
 
 void launch_prefill_attention(const ModelDev& m, int layer, const bf16* q, bf16* out, const int* seg_start,

@@ -40,6 +40,9 @@ struct Model {
   std::vector<Plans> dec, pf;
   GemmPlan lm_dec;
   int* pf_rows = nullptr;  // device row count for prefill GEMMs
+  CUtensorMap kvmap;         // TMA view of the KV pool for the decode attention
+  float* gemm_ws = nullptr;  // split-K partial tiles (shared by all decode GEMMs, stream-ordered)
+  int* gemm_cnt = nullptr;   // split-K arrival counters (self-resetting)
   int32_t *seg_start = nullptr, *seg_group = nullptr, *ga_g = nullptr, *ga_len = nullptr, *ga_last = nullptr;
   int32_t* host_stage = nullptr;
   size_t host_stage_cap = 0;
@@ -164,13 +167,16 @@ Model* model_create(Engine& e) {
   M->attn = dalloc<bf16>(R * m.qd);
   M->hbuf = dalloc<bf16>(R * m.f);
   M->logits = dalloc<float>((size_t)M->S * m.V);
-  M->chunk = (ec.max_prompt + ec.l_max) > 4608 ? 512 : 256;
+  M->chunk = 512;  // KV tokens per attention work item (8 tiles)
   M->max_splits = ceil_div(m.max_pos, M->chunk);
   M->part_o = dalloc<float>((size_t)M->S * m.hq * M->max_splits * m.hd);
   M->part_ml = dalloc<float>((size_t)M->S * m.hq * M->max_splits * 2);
   m.row_tok = dalloc<int32_t>(R);
   m.row_pos = dalloc<int32_t>(R);
   m.row_btrow = dalloc<int32_t>(R);
+  m.split_prefix = dalloc<int32_t>(M->S + 1);
+  m.att_counter = dalloc<int32_t>((size_t)M->S * m.hk);
+  m.att_items = dalloc<int32_t>((size_t)M->S * M->max_splits + 1);
   m.h_ctx = dalloc<int32_t>(m.H);
   m.h_last_tok = dalloc<int32_t>(m.H);
   m.h_shared = dalloc<int32_t>(m.H);
@@ -210,19 +216,27 @@ Model* model_create(Engine& e) {
     AB_CUDA(cudaMemcpy(m.free_pages, fp.data(), sizeof(int32_t) * np, cudaMemcpyHostToDevice));
   }
   AB_CUDA(cudaMemcpy(&e.d.ctl->kv_free_top, &np, sizeof(int64_t), cudaMemcpyHostToDevice));
+  make_kv_tmap(&M->kvmap, m);
   e.ctl_host->kv_free_top = np;
 
   // ---- GEMM plans ----
   const int* b = &e.d.ctl->b;
   const int* stop = &e.d.ctl->stop;
   const int bn_dec = pick_bn(M->S);
+  M->gemm_ws = dalloc<float>(kGemmWsElems);
+  M->gemm_cnt = dalloc<int>(kGemmCounters);
+  float* ws = M->gemm_ws;
+  int* cnt = M->gemm_cnt;
   for (int l = 0; l < m.L; ++l) {
     const LayerW& w = M->layers[l];
     Model::Plans d, p;
-    gemm_plan(d.qkv, w.wqkv, m.qkv_dim, m.d, M->xn, M->S, m.d, bn_dec, kEpiBF16, M->qkv, m.qkv_dim, w.bqkv, b, stop);
-    gemm_plan(d.o, w.wo, m.d, m.qd, M->attn, M->S, m.qd, bn_dec, kEpiAddF32, M->x, m.d, nullptr, b, stop);
-    gemm_plan(d.gu, w.wgu, 2 * m.f, m.d, M->xn, M->S, m.d, bn_dec, kEpiSwiGLU, M->hbuf, m.f, nullptr, b, stop);
-    gemm_plan(d.down, w.wd, m.d, m.f, M->hbuf, M->S, m.f, bn_dec, kEpiAddF32, M->x, m.d, nullptr, b, stop);
+    gemm_plan(d.qkv, w.wqkv, m.qkv_dim, m.d, M->xn, M->S, m.d, bn_dec, kEpiBF16, M->qkv, m.qkv_dim, w.bqkv, b, stop,
+              ws, cnt, 4);
+    gemm_plan(d.o, w.wo, m.d, m.qd, M->attn, M->S, m.qd, bn_dec, kEpiAddF32, M->x, m.d, nullptr, b, stop, ws, cnt, 4);
+    gemm_plan(d.gu, w.wgu, 2 * m.f, m.d, M->xn, M->S, m.d, bn_dec, kEpiSwiGLU, M->hbuf, m.f, nullptr, b, stop, ws,
+              cnt, 4);
+    gemm_plan(d.down, w.wd, m.d, m.f, M->hbuf, M->S, m.f, bn_dec, kEpiAddF32, M->x, m.d, nullptr, b, stop, ws, cnt,
+              8);
     gemm_plan(p.qkv, w.wqkv, m.qkv_dim, m.d, M->xn, M->M_pf, m.d, 256, kEpiBF16, M->qkv, m.qkv_dim, w.bqkv,
               M->pf_rows, nullptr);
     gemm_plan(p.o, w.wo, m.d, m.qd, M->attn, M->M_pf, m.qd, 256, kEpiAddF32, M->x, m.d, nullptr, M->pf_rows,
@@ -248,7 +262,7 @@ void model_destroy(Model* M) {
                   M->logits,   M->part_o,   M->part_ml,   m.row_tok,    m.row_pos,    m.row_btrow, m.h_ctx,
                   m.h_last_tok, m.h_shared, m.g_ctx,      m.g_last_tok, m.g_npages,   m.bt,        m.rope,
                   M->pf_rows,  M->seg_start, M->seg_group, M->ga_g,     M->ga_len,    M->ga_last,  m.kv,
-                  m.free_pages};
+                  m.free_pages, m.split_prefix, m.att_counter, M->gemm_ws, M->gemm_cnt};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   if (M->host_stage) cudaFreeHost(M->host_stage);
@@ -390,7 +404,7 @@ void model_iteration(Engine& e, int64_t run_iter, bool timed) {
   const int S = M->S;
   {
     ScopedTimer t(e, timed, "prep", run_iter);
-    launch_prep_decode(e.d, m, s);
+    launch_prep_decode(e.d, m, M->chunk, s);
   }
   {
     ScopedTimer t(e, timed, "embed", run_iter);
@@ -413,7 +427,8 @@ void model_iteration(Engine& e, int64_t run_iter, bool timed) {
     }
     {
       ScopedTimer t(e, timed, "attention", run_iter);
-      launch_decode_attention(e.d, m, l, M->qrot, M->attn, M->part_o, M->part_ml, M->max_splits, M->chunk, s);
+      launch_decode_attention(M->kvmap, e.d, m, l, M->qrot, M->attn, M->part_o, M->part_ml, M->max_splits, M->chunk,
+                              s);
     }
     {
       ScopedTimer t(e, timed, "gemm_o", run_iter);

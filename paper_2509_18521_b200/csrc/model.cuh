@@ -33,6 +33,9 @@ struct ModelDev {
   int32_t* row_tok;
   int32_t* row_pos;
   int32_t* row_btrow;
+  int32_t* split_prefix;  // [S+1] attention work list: exclusive prefix of KV splits per live row
+  int32_t* att_counter;   // [S * hk] split-combine arrival counters (self-resetting)
+  int32_t* att_items;     // [S * max_splits] work list: row | split << 16
 
   __device__ __forceinline__ size_t kv_off(int l, int page, int which, int head, int slot) const {
     return ((((size_t)l * NP + page) * 2 + which) * hk + head) * (size_t)P * hd + (size_t)slot * hd;
@@ -47,15 +50,17 @@ struct LayerW {
 void launch_init_weights(bf16* w, size_t n, uint64_t seed, uint64_t tensor_id, float std, float constant,
                          cudaStream_t s);
 void launch_rope_table(float2* rope, int max_pos, int hd, float theta, cudaStream_t s);
-void launch_prep_decode(const EngineDev& e, const ModelDev& m, cudaStream_t s);
+void launch_prep_decode(const EngineDev& e, const ModelDev& m, int chunk, cudaStream_t s);
 void launch_embed(const ModelDev& m, const bf16* emb, float* x, const int* rows_dev, int rows_cap,
                   const int* stop, cudaStream_t s);
 void launch_rmsnorm(const float* x, const bf16* w, bf16* out, int d, float eps, const int* rows_dev, int rows_cap,
                     const int* stop, cudaStream_t s);
 void launch_rope_kv(const ModelDev& m, int layer, const bf16* qkv, const bf16* q_norm, const bf16* k_norm, bf16* q_out,
                     const int* rows_dev, int rows_cap, const int* stop, cudaStream_t s);
-void launch_decode_attention(const EngineDev& e, const ModelDev& m, int layer, const bf16* q, bf16* out,
-                             float* part_o, float* part_ml, int max_splits, int chunk, cudaStream_t s);
+// attention.cu
+void make_kv_tmap(CUtensorMap* map, const ModelDev& m);
+void launch_decode_attention(const CUtensorMap& map, const EngineDev& e, const ModelDev& m, int layer, const bf16* q,
+                             bf16* out, float* part_o, float* part_ml, int max_splits, int chunk, cudaStream_t s);
 void launch_prefill_attention(const ModelDev& m, int layer, const bf16* q, bf16* out, const int* seg_start,
                               const int* seg_group, int n_seg, int rows, int max_len, cudaStream_t s);
 void launch_fork_groups(const EngineDev& e, const ModelDev& m, const ab_sample_desc* descs, int n, cudaStream_t s);

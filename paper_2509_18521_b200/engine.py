@@ -301,6 +301,10 @@ class Engine:
     def decode_until_event(self) -> list[Event]:
         return self._run(capi.RunArgs(stop_on_event=1))
 
+    def decode_iterations(self, k: int) -> list[Event]:
+        """Run up to k decode iterations in one device call (stops early only if drained)."""
+        return self._run(capi.RunArgs(max_iters=int(k)))
+
     def run_until_trigger(self, n: int, g: int, trigger: str, completed_groups: int, completed_samples: int,
                           group_done: dict[int, int] | None = None) -> list[Event]:
         """Fused APRIL loop: decode until check_trigger(n, g, trigger) fires (scheduler.py:272-283)."""

@@ -1,0 +1,92 @@
+"""Time the tcgen05 GEMM (ab_debug_gemm) on decoder shapes, next to torch/cuBLAS.
+
+    python tools/gemm_bench.py [--m 1024 64] [--reps 20]
+"""
+
+import argparse
+import ctypes as C
+import json
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+
+import torch  # noqa: E402
+
+from paper_2509_18521_b200 import _capi  # noqa: E402
+
+SHAPES = {  # name: (N, K, epi)   Qwen2.5-1.5B decode projections
+    "qkv": (2048, 1536, 0),
+    "o": (1536, 1536, 2),
+    "gate_up": (17920, 1536, 3),
+    "down": (1536, 8960, 2),
+    "lm_head": (151936, 1536, 1),
+}
+
+
+def run(N, K, M, epi, bn, reps, split):
+    W = (torch.randn(N, K, device="cuda") * 0.02).to(torch.bfloat16)
+    A = torch.randn(M, K, device="cuda").to(torch.bfloat16)
+    bias = torch.zeros(N, device="cuda", dtype=torch.bfloat16) if epi == 0 else None
+    if epi == 3:
+        out = torch.empty(M, N // 2, device="cuda", dtype=torch.bfloat16)
+    elif epi == 0:
+        out = torch.empty(M, N, device="cuda", dtype=torch.bfloat16)
+    else:
+        out = torch.zeros(M, N, device="cuda", dtype=torch.float32)
+    code = epi + (16 if split else 0)
+    args = (C.c_void_p(W.data_ptr()), C.c_void_p(A.data_ptr()), C.c_void_p(out.data_ptr()),
+            C.c_void_p(bias.data_ptr()) if bias is not None else None, N, K, M, bn, code)
+    for _ in range(3):
+        _capi.call("ab_debug_gemm", *args)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+    ts = []
+    for _ in range(reps):
+        flush.zero_()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        _capi.call("ab_debug_gemm", *args)
+        b.record()
+        torch.cuda.synchronize()
+        ts.append(a.elapsed_time(b))
+    ts.sort()
+    ms = ts[len(ts) // 2]
+    # cuBLAS reference for the same contraction
+    for _ in range(3):
+        torch.matmul(A, W.t())
+    cts = []
+    for _ in range(reps):
+        flush.zero_()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        torch.matmul(A, W.t())
+        b.record()
+        torch.cuda.synchronize()
+        cts.append(a.elapsed_time(b))
+    cts.sort()
+    cms = cts[len(cts) // 2]
+    flops = 2.0 * M * N * K
+    wbytes = N * K * 2
+    return {"us": round(ms * 1e3, 1), "TFLOP/s": round(flops / ms / 1e9, 1), "W GB/s": round(wbytes / ms / 1e6, 1),
+            "cublas_us": round(cms * 1e3, 1), "cublas_TFLOP/s": round(flops / cms / 1e9, 1)}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--m", type=int, nargs="+", default=[1024, 256, 64, 8])
+    ap.add_argument("--reps", type=int, default=15)
+    ap.add_argument("--bn", type=int, nargs="+", default=[128])
+    ap.add_argument("--split", type=int, default=1)
+    args = ap.parse_args()
+    res = []
+    for name, (N, K, epi) in SHAPES.items():
+        for M in args.m:
+            for bn in args.bn:
+                r = run(N, K, M, epi, bn, args.reps, bool(args.split))
+                r.update({"shape": name, "M": M, "BN": bn})
+                res.append(r)
+                print(json.dumps(r), flush=True)
+
+
+if __name__ == "__main__":
+    main()
