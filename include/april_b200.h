@@ -187,6 +187,8 @@ int ab_engine_stats(ab_engine* e, ab_stats* out);
 int ab_engine_profile(ab_engine* e, int enable, int sample_every);
 int ab_engine_kernel_stats(ab_engine* e, ab_kernel_stat* out, int cap, int* n);
 int ab_engine_synchronize(ab_engine* e);
+/* data-parallel lockstep: align the device iteration counter with the global index */
+int ab_engine_set_iteration(ab_engine* e, int64_t iteration_index);
 
 /* K6: group-normalised advantages over contiguous groups of G rewards.
  * mode 0 = mean baseline, 1 = mean/std (GRPO), 2 = mean/std with a
@@ -196,6 +198,8 @@ int ab_group_advantages(const double* rewards, int n_groups, int group_size, int
 
 /* Test entry points (device pointers; used by tests/test_kernels_gpu.py). */
 int ab_debug_gemm(const void* W, const void* A, void* out, const void* bias, int N, int K, int M, int BN, int epi);
+int ab_debug_gemm_time(const void* W, const void* A, void* out, const void* bias, int N, int K, int M, int BN, int epi,
+                       int reps, float* ms_out);
 
 #ifdef __cplusplus
 }

@@ -507,3 +507,80 @@ def make_oracle(cfg: dict):
                           trigger=cfg.get("trigger", "groups"), dist=dist, rho=cfg.get("rho", 0.0),
                           seed=cfg.get("seed", 0))
     return eng, sch
+
+
+# --------------------------------------------------------------------------
+# composed k-engine oracle for the data-parallel path
+# --------------------------------------------------------------------------
+
+
+class KEngineOracle:
+    """k reference-semantics engines in lockstep behind the single-engine duck type.
+
+    Placement: an instance is placed at its first submit on the rank with the
+    fewest active + queued samples (ties to the lowest rank); later submits of
+    the same instance are sticky.  Every global iteration each rank admits
+    from its own FIFO and advances its own slots; events of one iteration are
+    merged rank-major, slot order within a rank.  iteration_index and
+    cumulative_tokens are global.  (No reference counterpart exists: the
+    reference is a single engine; this composes its semantics.)
+    """
+
+    def __init__(self, k, d0, d1, max_slots, l_max, mode="length", seed=0):
+        self.engines = [OracleEngine(d0, d1, max_slots, l_max, mode=mode, seed=seed) for _ in range(k)]
+        self.k = k
+        self.place: dict = {}
+        self.iteration_index = 0
+        self.cumulative_tokens = 0
+        self.clock = 0.0
+        self.event_log: list = []
+
+    @property
+    def idle(self):
+        return all(e.idle for e in self.engines)
+
+    def begin_step(self, version, params=None):
+        for e in self.engines:
+            e.begin_step(version, params)
+
+    def submit(self, s):
+        r = self.place.get(s.instance_id)
+        if r is None:
+            loads = [len(e.slots) + len(e._queue) for e in self.engines]
+            r = loads.index(min(loads))
+            self.place[s.instance_id] = r
+        self.engines[r].submit(s)
+
+    def decode_until_event(self):
+        while True:
+            for e in self.engines:
+                e._admit()
+            live = [e for e in self.engines if e.slots]
+            if not live:
+                return []
+            b = sum(len(e.slots) for e in live)
+            self.iteration_index += 1
+            self.cumulative_tokens += b
+            events = []
+            for e in self.engines:  # rank-major
+                if e.slots:
+                    for s, why in e._advance(1):
+                        events.append((s, why))
+                        self.event_log.append([self.iteration_index, s.instance_id, s.sample_index, s.total_tokens, why])
+            if events:
+                return events
+
+    def abort_active(self):
+        out = []
+        for e in self.engines:
+            out.extend(e.abort_active())
+        return out
+
+
+def make_k_oracle(cfg: dict, k: int):
+    eng = KEngineOracle(k, cfg.get("d0", 0.05), cfg.get("d1", 0.002), cfg["slots"], cfg["l_max"])
+    d = cfg["dist"]
+    sch = OracleScheduler(cfg["n"], cfg["g"], cfg["n_prime"], eng, mode=cfg.get("mode", "april"),
+                          trigger=cfg.get("trigger", "groups"), dist=TraceDist(d[0], cfg["l_max"], *d[1:]),
+                          rho=cfg.get("rho", 0.0), seed=cfg.get("seed", 0))
+    return eng, sch

@@ -112,8 +112,11 @@ _SIGS = {
     "ab_engine_profile": [P, C.c_int, C.c_int],
     "ab_engine_kernel_stats": [P, C.POINTER(KernelStat), C.c_int, C.POINTER(C.c_int)],
     "ab_engine_synchronize": [P],
+    "ab_engine_set_iteration": [P, C.c_int64],
     "ab_group_advantages": [F64P, C.c_int, C.c_int, C.c_int, C.c_double, F64P, I32P, C.c_int],
     "ab_debug_gemm": [P, P, P, P, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int],
+    "ab_debug_gemm_time": [P, P, P, P, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int,
+                           C.POINTER(C.c_float)],
 }
 EXPORTS = sorted(_SIGS) + ["ab_last_error", "ab_version"]
 

@@ -382,18 +382,45 @@ int Engine::timer_index(const char* name) {
   return (int)timers.size() - 1;
 }
 
+// Timed launches are only captured into the profiled iteration graph: the
+// event-record nodes sit between the kernel nodes, so the measured interval
+// is the kernel's device time with no host submission gap in it.
 ScopedTimer::ScopedTimer(Engine& eng, bool on, const char* name, int64_t run_iter_, double bytes_, double flops_)
     : e(eng), idx(-1), bytes(bytes_), flops(flops_), run_iter(run_iter_) {
-  if (!on || !e.profile) return;
+  if (!on || !e.capturing_prof) return;
   idx = e.timer_index(name);
   a = e.take_event();
-  AB_CUDA(cudaEventRecord(a, e.stream));
+  AB_CUDA(cudaEventRecordWithFlags(a, e.stream, cudaEventRecordExternal));
 }
 ScopedTimer::~ScopedTimer() {
   if (idx < 0) return;
   cudaEvent_t b = e.take_event();
-  cudaEventRecord(b, e.stream);
-  e.pending.push_back(Engine::PendingTime{idx, a, b, run_iter, bytes, flops});
+  cudaEventRecordWithFlags(b, e.stream, cudaEventRecordExternal);
+  e.prof_slots.push_back(Engine::ProfSlot{idx, a, b});
+}
+
+// Accumulate the profiled graph's event intervals for launch `run_iter`.
+static void collect_prof(Engine& e) {
+  if (e.prof_pending < 0) return;
+  const int64_t it = e.prof_pending;
+  e.prof_pending = -1;
+  if (it >= e.d.it_cap) return;
+  int32_t b = 0;
+  int64_t ctx = 0;
+  AB_CUDA(cudaMemcpy(&b, e.d.it_b + it, sizeof(int32_t), cudaMemcpyDeviceToHost));
+  AB_CUDA(cudaMemcpy(&ctx, e.d.it_ctx + it, sizeof(int64_t), cudaMemcpyDeviceToHost));
+  if (b <= 0) return;  // iteration queued past the stop point: all kernels were no-ops
+  for (auto& s : e.prof_slots) {
+    float ms = 0;
+    AB_CUDA(cudaEventElapsedTime(&ms, s.a, s.b));
+    auto& t = e.timers[s.timer];
+    double bytes = 0, flops = 0;
+    if (e.model) model_kernel_cost(e.model, t.name, (double)b, (double)ctx, &bytes, &flops);
+    t.launches += 1;
+    t.ms += ms;
+    t.bytes += bytes;
+    t.flops += flops;
+  }
 }
 
 static void collect_timers(Engine& e) {
@@ -553,6 +580,11 @@ static void destroy(Engine* e) {
   cudaSetDevice(e->device);
   cudaStreamSynchronize(e->stream);
   if (e->iter_graph) cudaGraphExecDestroy(e->iter_graph);
+  if (e->prof_graph) cudaGraphExecDestroy(e->prof_graph);
+  for (auto& s : e->prof_slots) {
+    cudaEventDestroy(s.a);
+    cudaEventDestroy(s.b);
+  }
   if (e->model) model_destroy(e->model);
   EngineDev& d = e->d;
   void* ptrs[] = {d.ctl,     d.slot_handle, d.slot_tmp, d.slot_finish, d.slot_token, d.q_buf,  d.h_gen,
@@ -610,8 +642,7 @@ static void submit(Engine& e, const ab_sample_desc* descs, int n) {
   AB_CUDA(cudaStreamSynchronize(e.stream));
 }
 
-static void launch_iteration(Engine& e, int64_t run_iter) {
-  const bool timed = e.profile && (run_iter % e.sample_every == 0);
+static void launch_iteration(Engine& e, int64_t run_iter, bool timed = false) {
   e.launches += 2 + (e.model ? 5 + 9 * (int64_t)e.mcfg.n_layers : 1);
   {
     ScopedTimer t(e, timed, "admit", run_iter);
@@ -631,27 +662,41 @@ static void launch_iteration(Engine& e, int64_t run_iter) {
 
 // Iterations are replayed from one captured CUDA graph: every kernel reads the
 // live batch size and the stop flag from the device control block, so the
-// same graph serves every batch size.  Profiled iterations launch directly
-// (their CUDA events are recorded between the kernels).
-static void launch_iteration_fast(Engine& e, int64_t run_iter) {
-  const bool timed = e.profile && (run_iter % e.sample_every == 0);
-  if (timed || !e.use_graphs || e.direct_launches < 1) {
+// same graph serves every batch size.  When profiling, the first iteration of
+// every `sample_every`-th host chunk replays a second graph that also holds
+// event-record nodes around each kernel class.
+static cudaGraphExec_t capture_iteration(Engine& e, bool timed) {
+  const int64_t before = e.launches;
+  cudaGraph_t g;
+  cudaGraphExec_t x;
+  e.capturing_prof = timed;
+  AB_CUDA(cudaStreamBeginCapture(e.stream, cudaStreamCaptureModeThreadLocal));
+  launch_iteration(e, -1, timed);
+  AB_CUDA(cudaStreamEndCapture(e.stream, &g));
+  e.capturing_prof = false;
+  AB_CUDA(cudaGraphInstantiate(&x, g, 0));
+  AB_CUDA(cudaGraphDestroy(g));
+  e.graph_kernels = e.launches - before;
+  e.launches = before;
+  return x;
+}
+
+static void launch_iteration_fast(Engine& e, int64_t run_iter, bool first_in_chunk) {
+  if (!e.use_graphs || e.direct_launches < 1) {  // first call: plain launches set up kernel attributes
     launch_iteration(e, run_iter);
     ++e.direct_launches;
     return;
   }
-  if (!e.iter_graph) {
-    const int64_t before = e.launches;
-    cudaGraph_t g;
-    AB_CUDA(cudaStreamBeginCapture(e.stream, cudaStreamCaptureModeThreadLocal));
-    launch_iteration(e, -1);
-    AB_CUDA(cudaStreamEndCapture(e.stream, &g));
-    AB_CUDA(cudaGraphInstantiate(&e.iter_graph, g, 0));
-    AB_CUDA(cudaGraphDestroy(g));
-    e.graph_kernels = e.launches - before;
-    e.launches = before;
+  if (!e.iter_graph) e.iter_graph = capture_iteration(e, false);
+  bool prof = false;
+  if (e.profile && first_in_chunk && e.prof_pending < 0) prof = (e.prof_count++ % e.sample_every) == 0;
+  if (prof) {
+    if (!e.prof_graph) e.prof_graph = capture_iteration(e, true);
+    AB_CUDA(cudaGraphLaunch(e.prof_graph, e.stream));
+    e.prof_pending = run_iter;
+  } else {
+    AB_CUDA(cudaGraphLaunch(e.iter_graph, e.stream));
   }
-  AB_CUDA(cudaGraphLaunch(e.iter_graph, e.stream));
   e.launches += e.graph_kernels;
 }
 
@@ -670,9 +715,10 @@ static void run(Engine& e, const ab_run_args* a, ab_run_result* r, ab_event* ev,
   while (true) {
     int n = chunk;
     if (a->max_iters > 0) n = (int)std::min<int64_t>(n, std::max<int64_t>(1, a->max_iters - launched));
-    for (int i = 0; i < n; ++i) launch_iteration_fast(e, launched + i);
+    for (int i = 0; i < n; ++i) launch_iteration_fast(e, launched + i, i == 0);
     launched += n;
     sync_ctl(e);
+    collect_prof(e);
     const Ctl& c = *e.ctl_host;
     if (c.stop) break;
     if (c.iters_to_next > 0)
@@ -929,7 +975,11 @@ int ab_engine_profile(ab_engine* e, int enable, int sample_every) {
     Engine& g = *e->impl;
     g.profile = enable != 0;
     g.sample_every = sample_every > 0 ? sample_every : 1;
-    if (!enable) g.timers.clear();
+    if (!enable)  // keep the names: captured profiling slots refer to timer indices
+      for (auto& t : g.timers) {
+        t.launches = 0;
+        t.ms = t.bytes = t.flops = 0;
+      }
   });
 }
 
@@ -945,6 +995,15 @@ int ab_engine_kernel_stats(ab_engine* e, ab_kernel_stat* out, int cap, int* n) {
       out[i].bytes = g.timers[i].bytes;
       out[i].flops = g.timers[i].flops;
     }
+  });
+}
+
+int ab_engine_set_iteration(ab_engine* e, int64_t iteration_index) {
+  return ab::guard([&] {
+    Engine& g = *e->impl;
+    AB_CUDA(cudaStreamSynchronize(g.stream));
+    AB_CUDA(cudaMemcpy(&g.d.ctl->iteration_index, &iteration_index, sizeof(int64_t), cudaMemcpyHostToDevice));
+    g.ctl_host->iteration_index = iteration_index;
   });
 }
 

@@ -94,6 +94,16 @@ struct Engine {
   int64_t direct_launches = 0;
   cudaGraphExec_t iter_graph = nullptr;
   int64_t graph_kernels = 0;
+  // profiling through a second captured graph with event-record nodes
+  cudaGraphExec_t prof_graph = nullptr;
+  bool capturing_prof = false;
+  struct ProfSlot {
+    int timer;
+    cudaEvent_t a, b;
+  };
+  std::vector<ProfSlot> prof_slots;
+  int64_t prof_pending = -1;
+  int64_t prof_count = 0;
   // profiling
   bool profile = false;
   int sample_every = 8;

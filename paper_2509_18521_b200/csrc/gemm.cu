@@ -12,7 +12,9 @@
 #include <cuda.h>
 #include <cuda_bf16.h>
 
+#include <algorithm>
 #include <mutex>
+#include <vector>
 
 #include "gemm.cuh"
 
@@ -422,6 +424,50 @@ void gemm_launch(const GemmPlan& p, cudaStream_t s) {
 }
 
 }  // namespace ab
+
+// Timing entry (tools/gemm_bench.py): median device time of `reps` launches,
+// L2 flushed (256 MB memset) between launches, plan built outside the timing.
+extern "C" int ab_debug_gemm_time(const void* W, const void* A, void* out, const void* bias, int N, int K, int M,
+                                  int BN, int epi, int reps, float* ms_out) {
+  try {
+    static float* ws = nullptr;
+    static int* cnt = nullptr;
+    static void* flush = nullptr;
+    const int max_splits = epi >= 16 ? 8 : 1;
+    epi &= 15;
+    if (!ws) {
+      AB_CUDA(cudaMalloc(&ws, sizeof(float) * ab::kGemmWsElems));
+      AB_CUDA(cudaMalloc(&cnt, sizeof(int) * ab::kGemmCounters));
+      AB_CUDA(cudaMemset(cnt, 0, sizeof(int) * ab::kGemmCounters));
+      AB_CUDA(cudaMalloc(&flush, size_t(256) << 20));
+    }
+    ab::GemmPlan p;
+    ab::gemm_plan(p, (const __nv_bfloat16*)W, N, K, (const __nv_bfloat16*)A, M, K, BN, epi, out,
+                  epi == ab::kEpiSwiGLU ? N / 2 : N, (const __nv_bfloat16*)bias, nullptr, nullptr,
+                  max_splits > 1 ? ws : nullptr, max_splits > 1 ? cnt : nullptr, max_splits);
+    ab::gemm_launch(p, 0);  // warm: kernel attributes, TMA descriptors
+    std::vector<float> t(reps);
+    cudaEvent_t a, b;
+    AB_CUDA(cudaEventCreate(&a));
+    AB_CUDA(cudaEventCreate(&b));
+    for (int r = 0; r < reps; ++r) {
+      AB_CUDA(cudaMemsetAsync(flush, r & 0xff, size_t(256) << 20, 0));
+      AB_CUDA(cudaEventRecord(a, 0));
+      ab::gemm_launch(p, 0);
+      AB_CUDA(cudaEventRecord(b, 0));
+      AB_CUDA(cudaEventSynchronize(b));
+      AB_CUDA(cudaEventElapsedTime(&t[r], a, b));
+    }
+    cudaEventDestroy(a);
+    cudaEventDestroy(b);
+    std::sort(t.begin(), t.end());
+    *ms_out = t[reps / 2];
+    return AB_OK;
+  } catch (const ab::Error& e) {
+    ab::set_last_error(e.what());
+    return e.code;
+  }
+}
 
 // Test entry: one GEMM on caller-provided device buffers (tests/test_kernels_gpu.py).
 extern "C" int ab_debug_gemm(const void* W, const void* A, void* out, const void* bias, int N, int K, int M, int BN,

@@ -130,6 +130,7 @@ class Engine:
         self._pending: list = []
         self.last_run = None
         self._h2d = self._d2h = 0  # bytes crossing PCIe through this API (bench e2e accounting)
+        self.last_admitted: list = []  # admissions of the last device call, in FIFO order
         if self._model_kind != capi.MODEL_CONTEXT_FREE:
             self._create()
 
@@ -301,6 +302,11 @@ class Engine:
     def decode_until_event(self) -> list[Event]:
         return self._run(capi.RunArgs(stop_on_event=1))
 
+    def set_iteration(self, iteration_index: int) -> None:
+        """Align the device iteration counter with a global (data-parallel) index."""
+        capi.call("ab_engine_set_iteration", self._h, int(iteration_index))
+        self.iteration_index = int(iteration_index)
+
     def decode_iterations(self, k: int) -> list[Event]:
         """Run up to k decode iterations in one device call (stops early only if drained)."""
         return self._run(capi.RunArgs(max_iters=int(k)))
@@ -346,6 +352,7 @@ class Engine:
         i = j = 0
         out: list[Event] = []
         finished: list[RolloutSample] = []
+        self.last_admitted = []
         with_tokens = self._record
         while i < na or j < ne:
             # admissions of iteration k (logged with index k) precede finishes of iteration k (index k+1)
@@ -357,6 +364,7 @@ class Engine:
                 s.status = ACTIVE
                 s.open_segment(self.version, with_tokens=with_tokens)
                 self._active[id(s)] = s
+                self.last_admitted.append(s)
                 i += 1
             else:
                 e = evs[j]

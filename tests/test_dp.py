@@ -1,0 +1,125 @@
+"""Data-parallel path on CPU: world_size 2 over gloo.
+
+Each rank runs the B200 build's replicated Scheduler over a DataParallelEngine
+whose local engine is the CPU oracle engine (the per-rank GPU engine is not
+available on a CPU box; the host logic under test — placement, lockstep
+counter exchange, log gather/merge, remote mirrors, abort merge — is the same).
+Rank 0's canonical step records must equal the composed k-engine oracle's
+(oracle/sim_ref.py KEngineOracle, k = 2) bit for bit.
+"""
+
+import os
+import socket
+import sys
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _worker(rank, world, port, name, mode, steps, fused, q):
+    sys.path.insert(0, ROOT)
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    import torch.distributed as dist
+
+    import canon
+    import paper_2509_18521_b200 as pb
+    from oracle import sim_ref
+    from paper_2509_18521_b200.dist import DataParallelEngine, OracleLocal, TorchComm
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        cfg = canon.CONFIGS[name]
+        local = OracleLocal(sim_ref.OracleEngine(0.05, 0.002, cfg["slots"], cfg["l_max"]))
+        eng = DataParallelEngine(local, TorchComm(), cfg["slots"])
+        d = cfg["dist"]
+        dist_obj = (pb.LengthDistribution.constant(int(d[1]), cfg["l_max"]) if d[0] == "constant"
+                    else pb.LengthDistribution.lognormal(d[1], d[2], cfg["l_max"]))
+        scfg = pb.SchedulerConfig(rollout_batch_size=cfg["n"], samples_per_prompt=cfg["g"],
+                                  over_sampling_batch_size=cfg["n_prime"], mode=mode,
+                                  trigger=cfg.get("trigger", "groups"))
+        sched = pb.Scheduler(scfg, eng, pb.InstanceSource(group_size=cfg["g"]),
+                             pb.LengthSampler(dist_obj, cfg["rho"], cfg["seed"]))
+        sched._fused = fused
+        sched.event_sink = []
+        recs = []
+        for k in range(steps):
+            out = sched.run_step(k)
+            evs = [[r["iteration_index"], *map(int, r["sample_id"].split(":")), r["tokens"], r["reason"]]
+                   for r in sched.event_sink if r["reason"] != "aborted"]
+            sched.event_sink.clear()
+            recs.append(canon.step_record(sched, out, evs))
+        if rank == 0:
+            q.put(recs)
+    finally:
+        dist.destroy_process_group()
+
+
+def _run_dp(name, mode, steps, fused):
+    import torch.multiprocessing as mp
+
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, name, mode, steps, fused, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    recs = q.get(timeout=300)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    return recs
+
+
+def _k_oracle(name, mode, steps):
+    import canon
+    from oracle import sim_ref
+
+    cfg = dict(canon.CONFIGS[name], mode=mode)
+    eng, sch = sim_ref.make_k_oracle(cfg, 2)
+    recs = []
+    for k in range(steps):
+        eng.event_log = []
+        out = sch.run_step(k)
+        recs.append(canon.step_record(sch, out, eng.event_log))
+    return recs
+
+
+@pytest.mark.parametrize("name,mode,steps,fused", [
+    ("C1", "april", 8, True),
+    ("E_samples", "april", 12, True),
+    ("E_cap", "april", 10, False),
+    ("C1", "baseline", 3, True),
+])
+def test_dp_world2_matches_k_engine_oracle(name, mode, steps, fused):
+    import canon
+
+    mine = _run_dp(name, mode, steps, fused)
+    ref = _k_oracle(name, mode, steps)
+    for a, b in zip(mine, ref):
+        assert a == b, canon.first_diff(a, b)
+
+
+def test_k_engine_oracle_k1_is_the_single_engine():
+    import canon
+    from oracle import sim_ref
+    from oracle_runs import oracle_replay
+
+    cfg = dict(canon.CONFIGS["C1"], mode="april")
+    eng, sch = sim_ref.make_k_oracle(cfg, 1)
+    recs = []
+    for k in range(6):
+        eng.event_log = []
+        out = sch.run_step(k)
+        recs.append(canon.step_record(sch, out, eng.event_log))
+    assert recs == oracle_replay(canon.CONFIGS["C1"], "april", 6)

@@ -37,20 +37,10 @@ def run(N, K, M, epi, bn, reps, split):
     code = epi + (16 if split else 0)
     args = (C.c_void_p(W.data_ptr()), C.c_void_p(A.data_ptr()), C.c_void_p(out.data_ptr()),
             C.c_void_p(bias.data_ptr()) if bias is not None else None, N, K, M, bn, code)
-    for _ in range(3):
-        _capi.call("ab_debug_gemm", *args)
+    msv = C.c_float()
+    _capi.call("ab_debug_gemm_time", *args, reps, C.byref(msv))  # device-timed, L2 flushed, median
+    ms = msv.value
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
-    ts = []
-    for _ in range(reps):
-        flush.zero_()
-        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        a.record()
-        _capi.call("ab_debug_gemm", *args)
-        b.record()
-        torch.cuda.synchronize()
-        ts.append(a.elapsed_time(b))
-    ts.sort()
-    ms = ts[len(ts) // 2]
     # cuBLAS reference for the same contraction
     for _ in range(3):
         torch.matmul(A, W.t())
