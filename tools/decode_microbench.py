@@ -29,6 +29,9 @@ def main():
     ap.add_argument("--iters", type=int, default=16)
     ap.add_argument("--page", type=int, default=64)
     ap.add_argument("--kv-pages", type=int, default=0)
+    ap.add_argument("--ncu", action="store_true",
+                    help="bracket only the profiled iterations with cudaProfilerStart/Stop "
+                         "(run under ncu --profile-from-start off)")
     args = ap.parse_args()
     spec = pb.PRESETS[args.model]
     if args.layers:
@@ -47,6 +50,16 @@ def main():
     warm = max(1, args.ctx - args.prompt)
     eng.decode_iterations(warm)
     t1 = time.perf_counter()
+    if args.ncu:
+        import torch
+
+        torch.cuda.synchronize()
+        torch.cuda.profiler.start()
+        eng.decode_iterations(args.iters)
+        eng.stats()
+        torch.cuda.profiler.stop()
+        print(json.dumps({"ncu_window_iters": args.iters, "batch": args.batch, "ctx": args.ctx}))
+        return
     eng.profile(True, 1)
     for _ in range(args.iters):  # one host chunk per iteration: each replays the profiled graph
         eng.decode_iterations(1)
