@@ -22,8 +22,8 @@ enum GemmEpi : int {
 // full 128-wide MMAs.
 struct GemmPlan {
   CUtensorMap tw;        // weights [N, K] bf16, box {64, 128}, 128B swizzle
-  CUtensorMap ta;        // activations [M_cap, K] bf16, box {64, BN}, 128B swizzle
-  int N = 0, K = 0, M_cap = 0, BN = 0, epi = 0;
+  CUtensorMap ta;        // activations [M_cap, K] bf16, box {64, 32}, 128B swizzle
+  int N = 0, K = 0, M_cap = 0, BN = 0, epi = 0;  // BN: largest activation tile the kernel may pick
   void* out = nullptr;
   int64_t ldo = 0;
   const __nv_bfloat16* bias = nullptr;
@@ -34,6 +34,7 @@ struct GemmPlan {
   float* ws = nullptr;  // shared workspace (kWsElems fp32), stream-ordered
   int* cnt = nullptr;   // per-tile arrival counters (>= N/128 * M_cap/BN, zeroed once)
   int max_splits = 1;
+  bool force_bn = false;  // BN is exact (tests) instead of the upper bound of the on-device choice
 };
 
 constexpr int64_t kGemmWsElems = int64_t(32) << 20;

@@ -64,10 +64,13 @@ T* dalloc(size_t n) {
   return p;
 }
 
+// Largest activation tile the decode GEMMs may use; the kernel picks the
+// actual width (and split-K) on the device from the live row count.
 int pick_bn(int rows) {
   if (rows <= 32) return 32;
   if (rows <= 64) return 64;
-  return 128;
+  if (rows <= 128) return 128;
+  return 256;
 }
 
 }  // namespace

@@ -59,3 +59,37 @@ def test_tcgen05_gemm_swiglu_epilogue(epi):
     t = acc.view(M, N // 128, 2, 64)
     ref = (torch.nn.functional.silu(t[:, :, 0]) * t[:, :, 1]).reshape(M, N // 2)
     torch.testing.assert_close(out.float(), ref, rtol=2e-2, atol=2e-2)
+
+
+@pytest.mark.parametrize("rows", [1, 17, 64, 200, 333, 1024])
+@pytest.mark.parametrize("shape_epi", [((1536, 1536), 2), ((2048, 1536), 0), ((512, 1024), 3), ((1536, 8960), 2),
+                                       ((384, 640), 1)])
+@pytest.mark.parametrize("split", [0, 16])
+def test_tcgen05_gemm_auto_schedule(rows, shape_epi, split):
+    """The decode configuration: tile width and split-K picked on the device from the row count."""
+    (N, K), epi = shape_epi
+    M = rows
+    g = torch.Generator(device="cuda").manual_seed(N + K + M)
+    W = (torch.randn(N, K, device="cuda", generator=g) * 0.05).to(torch.bfloat16)
+    A = torch.randn(M, K, device="cuda", generator=g).to(torch.bfloat16)
+    acc = A.float() @ W.float().t()
+    bias = None
+    if epi == 3:
+        out = torch.empty(M, N // 2, device="cuda", dtype=torch.bfloat16)
+        t = acc.view(M, N // 128, 2, 64)
+        ref = (torch.nn.functional.silu(t[:, :, 0]) * t[:, :, 1]).reshape(M, N // 2)
+    elif epi == 0:
+        bias = (torch.randn(N, device="cuda", generator=g) * 0.1).to(torch.bfloat16)
+        out = torch.empty(M, N, device="cuda", dtype=torch.bfloat16)
+        ref = acc + bias.float()
+    elif epi == 1:
+        out = torch.empty(M, N, device="cuda", dtype=torch.float32)
+        ref = acc
+    else:
+        base = torch.randn(M, N, device="cuda", generator=g)
+        out = base.clone()
+        ref = acc + base
+    _capi.call("ab_debug_gemm", _ptr(W), _ptr(A), _ptr(out), _ptr(bias), N, K, M, 256, epi + split + 32)
+    torch.cuda.synchronize()
+    tol = 2e-2 if epi in (0, 3) else 2e-3
+    torch.testing.assert_close(out.float(), ref, rtol=tol, atol=tol * max(1.0, ref.abs().max().item() * 0.01))

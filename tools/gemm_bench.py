@@ -34,9 +34,9 @@ def run(N, K, M, epi, bn, reps, split):
         out = torch.empty(M, N, device="cuda", dtype=torch.bfloat16)
     else:
         out = torch.zeros(M, N, device="cuda", dtype=torch.float32)
-    code = epi + (16 if split else 0)
+    code = epi + (16 if split else 0) + (32 if bn == 0 else 0)  # bn 0: on-device tile choice (decode path)
     args = (C.c_void_p(W.data_ptr()), C.c_void_p(A.data_ptr()), C.c_void_p(out.data_ptr()),
-            C.c_void_p(bias.data_ptr()) if bias is not None else None, N, K, M, bn, code)
+            C.c_void_p(bias.data_ptr()) if bias is not None else None, N, K, M, bn or 256, code)
     msv = C.c_float()
     _capi.call("ab_debug_gemm_time", *args, reps, C.byref(msv))  # device-timed, L2 flushed, median
     ms = msv.value
@@ -65,7 +65,7 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--m", type=int, nargs="+", default=[1024, 256, 64, 8])
     ap.add_argument("--reps", type=int, default=15)
-    ap.add_argument("--bn", type=int, nargs="+", default=[128])
+    ap.add_argument("--bn", type=int, nargs="+", default=[0], help="activation tile width; 0 = automatic (as the decode path)")
     ap.add_argument("--split", type=int, default=1)
     args = ap.parse_args()
     res = []
