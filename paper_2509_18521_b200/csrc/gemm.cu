@@ -1,19 +1,28 @@
 // K4: warp-specialised tcgen05 GEMM (sm_100a), TMA -> smem ring -> UMMA ->
-// TMEM -> fused epilogue.
+// TMEM -> fused epilogue.  Persistent (one CTA per SM), double-buffered TMEM
+// accumulator so the epilogue of one tile overlaps the main loop of the next.
 //
-//   warp 0      TMA producer (one elected lane), STAGES-deep mbarrier ring
+//   warp 0      TMA producer (one elected lane), mbarrier ring carved per launch
 //   warp 1      TMEM allocator + MMA issuer (one lane, tcgen05.mma kind::f16)
 //   warps 2-5   epilogue: tcgen05.ld 32x32b -> bias / residual / SwiGLU -> global
 //
-// D^T tile [128 weight rows x BN activation rows] accumulates in TMEM
-// (lane = weight row, column = activation row), so the epilogue thread that
-// owns TMEM lane t writes output feature n0+t for every activation row:
-// a warp stores 32 consecutive features of one row per instruction.
+// Two tile orientations, picked per launch from the live row count (schedule
+// table, see choose_sched): swap-AB (128 weight rows on the UMMA M side, the
+// activation rows on N) for small batches, activation rows on M for large ones.
+//
+// Split-K runs inside a thread-block cluster: the CS CTAs of a cluster each
+// reduce one K slice of the same tile into their own TMEM, park the partial
+// tile in their shared memory, and after a cluster barrier every rank sums
+// its share of the tile's columns over all ranks through distributed shared
+// memory (ld.shared::cluster, rank order: deterministic) and runs the
+// epilogue for it.  No global-memory round trip, no atomics.
 #include <cuda.h>
 #include <cuda_bf16.h>
 
 #include <algorithm>
+#include <map>
 #include <mutex>
+#include <tuple>
 #include <vector>
 
 #include "gemm.cuh"
@@ -103,69 +112,176 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, float (&v)[32]) {
   for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
 }
 
-__device__ __forceinline__ float silu(float x) { return x / (1.f + __expf(-x)); }
+__device__ __forceinline__ float silu(float x) { return __fdividef(x, 1.f + __expf(-x)); }
 
-// Per-launch schedule, chosen on the device from the live row count so one
-// captured graph serves every batch size: activation tile width BN (the UMMA
-// N), deterministic split-K factor, and the unit count of the persistent loop.
+__device__ __forceinline__ uint32_t pack_bf16x2(float lo, float hi) {
+  const __nv_bfloat162 v = __floats2bfloat162_rn(lo, hi);
+  return *reinterpret_cast<const uint32_t*>(&v);
+}
+
+__device__ __forceinline__ uint32_t cluster_ctarank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ uint32_t cluster_nctarank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_nctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+__device__ __forceinline__ uint32_t map_rank(uint32_t saddr, uint32_t rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(saddr), "r"(rank));
+  return r;
+}
+__device__ __forceinline__ float4 ld_dsmem_f4(uint32_t addr) {
+  float4 v;
+  asm volatile("ld.shared::cluster.v4.f32 {%0, %1, %2, %3}, [%4];"
+               : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+               : "r"(addr));
+  return v;
+}
+
+// Per-launch schedule.  The live row count is only known on the device (one
+// captured graph serves every batch size), so the host evaluates the cost
+// model for every possible row count when the plan is built and the kernel
+// reads its schedule from that table with one load.
+//   swap = 1: weights on the UMMA M side (128 weight rows per tile), the
+//             activation rows on the N side (an = 32..256): small batches
+//             still issue full 128-row MMAs.  TMEM lane = weight row.
+//   swap = 0: activation rows on the M side (an = 128), weights on the N side
+//             (wn = 128 or 256 weight rows).  TMEM lane = activation row, so
+//             the epilogue writes contiguous 16-byte vectors along a row.
+//   splits:   1, or the cluster size CS (cluster split-K, one tile per cluster).
 struct Sched {
-  int bn, splits, m_tiles, n_tiles, units, nk, stages, stage_bytes;
+  int swap, wn, an, splits, m_tiles, n_tiles, tiles, nk, stages, stage_bytes, w_bytes;
 };
 
-// Cost model (SM clocks per CTA-wave): a 64-deep K block costs the larger of
-// its MMA time (128 x BN x 64 MACs at ~4096 MAC/clk) and its operand fill
-// (16 KB weights + BN x 128 B activations at ~64 B/clk from L2); split-K adds
-// the partial-tile round trip; a CTA's last epilogue is exposed.
-__device__ __forceinline__ Sched choose_sched(int rows, int N, int K, int max_bn, int max_splits, bool force,
-                                              int grid, int64_t ws_cap) {
-  Sched best{};
-  best.units = 0;
-  const int n_tiles = N / kBM, nk = K / kBK;
+__host__ __device__ inline Sched sched_from(int code, int rows, int N, int K) {
+  Sched s;
+  s.swap = code & 1;
+  const int t = 1 << ((code >> 1) & 15);
+  s.splits = (code >> 5) & 31;
+  s.stages = (code >> 10) & 15;
+  s.wn = s.swap ? kBM : t;
+  s.an = s.swap ? t : kBM;
+  s.n_tiles = (N + s.wn - 1) / s.wn;
+  s.m_tiles = (rows + s.an - 1) / s.an;
+  s.tiles = s.n_tiles * s.m_tiles;
+  s.nk = K / kBK;
+  s.w_bytes = s.wn * kBK * 2;
+  s.stage_bytes = s.w_bytes + s.an * kBK * 2;
+  return s;
+}
+
+// Cost model (SM clocks per CTA): a 64-deep K block costs the larger of its
+// MMA time (~4096 MAC/clk) and its operand fill (~64 B/clk from L2); a tile
+// costs the larger of its main loop and its epilogue (the epilogue of tile t
+// overlaps the main loop of tile t+1); cluster split-K adds the partial park +
+// DSMEM reduction.  `cs` = cluster size of the launch, `ncl` = co-resident
+// clusters.  Returns the packed code (0 = no valid schedule).
+int choose_sched(int rows, int N, int K, int max_bn, int cs, int ncl, int force, int epi) {
+  const int nk = K / kBK;
+  const int grid = cs * ncl;
+  auto pack = [&](int swap, int t, int sp) {
+    int lg = 0;
+    while ((1 << lg) < t) ++lg;
+    const int wn = swap ? kBM : t, an = swap ? t : kBM;
+    const int stages = std::min(kMaxStages, kRingBytes / (wn * kBK * 2 + an * kBK * 2));
+    return swap | (lg << 1) | (sp << 5) | (stages << 10);
+  };
+  if (force > 0 && (force & 0x40000000)) {  // a fixed code (tools/gemm_bench.py --sweep)
+    const int code = force & 0x3ff;
+    const int swap = code & 1, t = 1 << ((code >> 1) & 15), sp = (code >> 5) & 31;
+    if (sp != 1 && sp != cs) return 0;
+    if (!swap && N % 128) return 0;
+    if (!swap && epi == kEpiSwiGLU && (t != 256 || N % 256)) return 0;
+    if (sp > 1) {
+      const int wn = swap ? kBM : t, an = swap ? t : kBM;
+      if ((int64_t)((N + wn - 1) / wn) * ((rows + an - 1) / an) > ncl || nk < sp) return 0;
+    }
+    return pack(swap, t, sp);
+  }
   int64_t best_cost = INT64_MAX;
-  for (int bn = max_bn; bn >= 32; bn >>= 1) {
-    const int m_tiles = (rows + bn - 1) / bn;
-    const int tiles = n_tiles * m_tiles;
-    for (int s = 1; s <= max_splits; ++s) {
-      if (s > 1 && (tiles * s > 2 * grid || nk / s < 2 || (int64_t)s * rows * N > ws_cap)) break;
-      const int units = tiles * s;
-      const int64_t waves = (units + grid - 1) / grid;
-      const int64_t kb = (nk + s - 1) / s;
-      const int64_t per_kb = max(2 * bn, (kWBytes + 128 * bn) / 64);
-      const int64_t split_cost = s > 1 ? (int64_t)bn * 40 : 0;
-      const int64_t epi = (int64_t)min(bn, rows) * 12;
-      const int64_t cost = waves * (kb * per_kb + 700 + split_cost) + epi;
-      if (cost < best_cost) {
-        best_cost = cost;
-        best.bn = bn;
-        best.splits = s;
-        best.m_tiles = m_tiles;
-        best.n_tiles = n_tiles;
-        best.units = units;
-        best.nk = nk;
+  int best = 0;
+  // force > 0: swap-AB with exactly an = force; force < 0: no swap with wn = -force
+  for (int mode = 0; mode < 2; ++mode) {
+    const int swap = mode == 0 ? 1 : 0;
+    if (force > 0 && !swap) continue;
+    if (force < 0 && swap) continue;
+    if (!swap && (epi == kEpiSwiGLU ? (N % 256) : (N % 128)) != 0) continue;
+    for (int t = swap ? max_bn : 256; t >= (swap ? 32 : 128); t >>= 1) {
+      if (force > 0 && t != force) continue;
+      if (force < 0 && t != -force) continue;
+      if (!swap && epi == kEpiSwiGLU && t != 256) continue;
+      const int wn = swap ? kBM : t, an = swap ? t : kBM;
+      const int tiles = ((N + wn - 1) / wn) * ((rows + an - 1) / an);
+      const int64_t mma = (int64_t)wn * an / 64;  // 128 x 256 x 64 -> 512 clk
+      const int64_t fill = (int64_t)(wn + an) * 128 / 64;
+      const int64_t per_kb = mma > fill ? mma : fill;
+      const int live = std::min(an, rows);
+      const int64_t epi_c = swap ? (int64_t)live * (epi == kEpiSwiGLU ? 96 : 48) : (int64_t)wn * 6 + 600;
+      for (int sp : {1, cs}) {
+        if (sp > 1 && (sp == 1 || tiles > ncl || nk < 2 * sp)) continue;
+        const int64_t waves = sp > 1 ? 1 : (tiles + grid - 1) / grid;
+        const int64_t main = (int64_t)((nk + sp - 1) / sp) * per_kb;
+        const int64_t split_cost = sp > 1 ? 1000 + (int64_t)(swap ? live : wn) * 26 : 0;  // DSMEM ~20 B/clk
+        const int64_t e = sp > 1 ? epi_c / sp : epi_c;
+        const int64_t cost = waves * ((main > e ? main : e) + 700) + split_cost + e;
+        if (cost < best_cost) {
+          best_cost = cost;
+          best = pack(swap, t, sp);
+        }
+        if (cs == 1) break;
       }
     }
-    if (force) break;
   }
-  best.stage_bytes = kWBytes + best.bn * kBK * 2;
-  best.stages = min(kMaxStages, kRingBytes / best.stage_bytes);
   return best;
+}
+
+// Debug timeline (ab_debug_gemm_trace): per CTA, %globaltimer at
+// [0] entry, [1] after setup, [2] first TMA issued, [3] first stage full at the MMA,
+// [4] last MMA committed, [5] epilogue sees the accumulator, [6] epilogue done, [7] exit,
+// [8] split: partial parked, [11] split: cluster barrier passed, [12] first chunk fetched.
+__device__ unsigned long long g_gemm_trace[160 * 16];
+__device__ __forceinline__ void trace_mark(int on, int k) {
+  if (on) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    g_gemm_trace[blockIdx.x * 16 + k] = t;
+  }
+}
+
+// Parked partial tile in the (idle) TMA ring: [chunk of 32 columns][TMEM lane][32 floats],
+// float4 index XOR-swizzled by lane so a warp's accesses are bank-conflict free.
+__device__ __forceinline__ uint32_t park_off(int chunk, int lane128, int q) {
+  return (uint32_t)(((chunk * 128 + lane128) * 8 + (q ^ (lane128 & 7))) * 16);
 }
 
 template <int EPI>
 __global__ void __launch_bounds__(kThreads, 1)
     k_gemm_tc(const __grid_constant__ CUtensorMap tw, const __grid_constant__ CUtensorMap ta, int N, int K,
               int M_cap, const int* __restrict__ rows_dev, const int* __restrict__ stop_dev, void* __restrict__ out,
-              int64_t ldo, const __nv_bfloat16* __restrict__ bias, float* __restrict__ ws, int* __restrict__ cnt,
-              int max_splits, int max_bn, int force_bn) {
+              int64_t ldo, const __nv_bfloat16* __restrict__ bias, const int* __restrict__ sched_tab, int trace) {
+  if (threadIdx.x == 0) trace_mark(trace, 0);
   if (stop_dev && *stop_dev) return;
   const int rows = rows_dev ? min(*rows_dev, M_cap) : M_cap;
   if (rows <= 0) return;
-  const Sched sc = choose_sched(rows, N, K, max_bn, (ws && cnt) ? max_splits : 1, force_bn != 0, gridDim.x,
-                                kGemmWsElems);
-  if ((int)blockIdx.x >= sc.units) return;
+  const int code = sched_tab[rows];
+  if (code == 0) return;
+  const Sched sc = sched_from(code, rows, N, K);
+  const int cs = (int)cluster_nctarank();
+  const bool split = sc.splits > 1;  // == cs: one tile per cluster, rank = K slice
+  const int rank = split ? (int)cluster_ctarank() : 0;
+  // work units: split -> tile blockIdx.x / cs (whole cluster); else tiles strided over the grid
+  const int u_first = split ? (int)blockIdx.x / cs : (int)blockIdx.x;
+  const int u_step = split ? (int)gridDim.x / cs : (int)gridDim.x;
+  if (u_first >= sc.tiles) return;  // split: uniform over the cluster
 
   extern __shared__ uint8_t smem_raw[];
-  __shared__ int s_last_split;
   uint8_t* ring = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   float* xchg = reinterpret_cast<float*>(ring + kRingBytes);
   uint64_t* full = reinterpret_cast<uint64_t*>(ring + kRingBytes + kXchgBytes);
@@ -175,7 +291,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tmem_empty + 2);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int nst = sc.stages, bn = sc.bn, per_n = sc.m_tiles * sc.splits;
+  const int nst = sc.stages;
   if (warp == 0 && lane == 0) {
     for (int s = 0; s < nst; ++s) {
       mbar_init(&full[s], 1);
@@ -198,14 +314,14 @@ __global__ void __launch_bounds__(kThreads, 1)
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   const uint32_t tmem = *tmem_slot;
+  if (threadIdx.x == 0) trace_mark(trace, 1);
 
-  auto unit_coords = [&](int u, int& n0, int& m0, int& z, int& kb0, int& kb1) {
-    const int nt = u / per_n, r = u % per_n;
-    n0 = nt * kBM;
-    m0 = (r / sc.splits) * bn;
-    z = r % sc.splits;
-    kb0 = (int)(((int64_t)sc.nk * z) / sc.splits);
-    kb1 = (int)(((int64_t)sc.nk * (z + 1)) / sc.splits);
+  auto unit_coords = [&](int u, int& n0, int& m0, int& kb0, int& kb1) {
+    const int nt = u / sc.m_tiles;
+    n0 = nt * sc.wn;
+    m0 = (u - nt * sc.m_tiles) * sc.an;
+    kb0 = (int)(((int64_t)sc.nk * rank) / sc.splits);
+    kb1 = (int)(((int64_t)sc.nk * (rank + 1)) / sc.splits);
   };
 
   if (warp == 0) {
@@ -218,31 +334,35 @@ __global__ void __launch_bounds__(kThreads, 1)
         asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol_w));
       asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol_a));
       int g = 0;
-      for (int u = blockIdx.x; u < sc.units; u += gridDim.x) {
-        int n0, m0, z, kb0, kb1;
-        unit_coords(u, n0, m0, z, kb0, kb1);
-        const int nbox = (min(bn, rows - m0) + 31) >> 5;  // skip activation boxes past the live rows
+      for (int u = u_first; u < sc.tiles; u += u_step) {
+        int n0, m0, kb0, kb1;
+        unit_coords(u, n0, m0, kb0, kb1);
+        const int nbox = (min(sc.an, rows - m0) + 31) >> 5;  // skip activation boxes past the live rows
+        const int wbox = (min(sc.wn, N - n0) + 127) >> 7;    // skip weight boxes past N
         for (int kb = kb0; kb < kb1; ++kb, ++g) {
           const int s = g % nst;
           const uint32_t ph = (g / nst) & 1;
           mbar_wait(&empty[s], ph ^ 1);
           uint8_t* st = ring + s * sc.stage_bytes;
-          mbar_expect_tx(&full[s], kWBytes + nbox * 32 * kBK * 2);
-          tma_load_2d(&tw, &full[s], st, kb * kBK, n0, pol_w);
+          mbar_expect_tx(&full[s], wbox * kWBytes + nbox * 32 * kBK * 2);
+          for (int j = 0; j < wbox; ++j)
+            tma_load_2d(&tw, &full[s], st + j * kWBytes, kb * kBK, n0 + 128 * j, pol_w);
           for (int j = 0; j < nbox; ++j)
-            tma_load_2d(&ta, &full[s], st + kWBytes + j * 32 * kBK * 2, kb * kBK, m0 + 32 * j, pol_a);
+            tma_load_2d(&ta, &full[s], st + sc.w_bytes + j * 32 * kBK * 2, kb * kBK, m0 + 32 * j, pol_a);
+          if (g == 0) trace_mark(trace, 2);
         }
       }
     }
   } else if (warp == 1) {
     if (lane == 0) {
-      const uint32_t idesc = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(bn >> 3) << 17) |
-                             ((uint32_t)(kBM >> 4) << 24);
+      const int um = sc.swap ? kBM : sc.an, un = sc.swap ? sc.an : sc.wn;
+      const uint32_t idesc =
+          (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(un >> 3) << 17) | ((uint32_t)(um >> 4) << 24);
       const uint32_t ring_s = smem_u32(ring);
       int g = 0, t = 0;
-      for (int u = blockIdx.x; u < sc.units; u += gridDim.x, ++t) {
-        int n0, m0, z, kb0, kb1;
-        unit_coords(u, n0, m0, z, kb0, kb1);
+      for (int u = u_first; u < sc.tiles; u += u_step, ++t) {
+        int n0, m0, kb0, kb1;
+        unit_coords(u, n0, m0, kb0, kb1);
         const int acc = t & 1;
         mbar_wait(&tmem_empty[acc], ((t >> 1) & 1) ^ 1);
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
@@ -251,8 +371,9 @@ __global__ void __launch_bounds__(kThreads, 1)
           const int s = g % nst;
           mbar_wait(&full[s], (g / nst) & 1);
           asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-          const uint32_t sa = ring_s + s * sc.stage_bytes;
-          const uint64_t da = umma_desc(sa), db = umma_desc(sa + kWBytes);
+          if (g == 0) trace_mark(trace, 3);
+          const uint32_t sw = ring_s + s * sc.stage_bytes, sa = sw + sc.w_bytes;
+          const uint64_t da = umma_desc(sc.swap ? sw : sa), db = umma_desc(sc.swap ? sa : sw);
 #pragma unroll
           for (int k = 0; k < kBK / 16; ++k)  // +32 bytes along K inside the swizzle atom
             umma_bf16(d, da + 2 * k, db + 2 * k, idesc, (kb != kb0 || k != 0) ? 1u : 0u);
@@ -260,134 +381,305 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         umma_commit(&tmem_full[acc]);
       }
+      trace_mark(trace, 4);
     }
   } else {
     // epilogue warps 2..5 -> TMEM lane quadrants 2,3,0,1
     const int quad = warp & 3;
-    const int lrow = quad * 32 + lane;  // TMEM lane = weight row within the tile
-    const bool split = sc.splits > 1;
+    const int lrow = quad * 32 + lane;  // TMEM lane
+    const uint32_t ring_s = smem_u32(ring);
+    const int te = threadIdx.x - 64;  // epilogue thread 0..127
+    // Cluster split-K epilogue (one tile per cluster): park this rank's partial tile in its
+    // own idle ring, cluster barrier, then reduce a 1/cs share of the tile's TMEM lanes over
+    // all ranks through DSMEM (rank order: deterministic), reading only the live columns,
+    // and run the epilogue for that share.  A second cluster barrier keeps every rank's
+    // smem alive until the others are done reading it.
+    //   swap park:    [col/4][lane]            (consecutive threads = consecutive lanes)
+    //   no-swap park: [lane][col/4 ^ (lane&7)] (consecutive threads = consecutive columns)
+    auto split_epilogue = [&](uint32_t taddr, int lrow, int ncols, int n0, int m0) {
+      const int swz = lrow & 7;
+      for (int c0 = 0; c0 < ncols; c0 += 32) {
+        float v[32];
+        tmem_ld32(taddr + c0, v);
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+          const int c4 = (c0 >> 2) + q;
+          const uint32_t off = sc.swap ? (uint32_t)((c4 * 128 + lrow) * 16) : (uint32_t)((lrow * 64 + (c4 ^ swz)) * 16);
+          *reinterpret_cast<float4*>(ring + off) = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
+        }
+      }
+      asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+      if (threadIdx.x == 64) trace_mark(trace, 8);
+      cluster_sync_all();
+      if (threadIdx.x == 64) trace_mark(trace, 11);
+      uint32_t rbase[8];
+#pragma unroll
+      for (int r = 0; r < 8; ++r) rbase[r] = map_rank(ring_s, (uint32_t)(r < cs ? r : 0));
+      auto gather = [&](uint32_t off) {
+        float4 x[8];
+#pragma unroll
+        for (int r = 0; r < 8; ++r)
+          if (r < cs) x[r] = ld_dsmem_f4(rbase[r] + off);
+        float4 a = x[0];
+#pragma unroll
+        for (int r = 1; r < 8; ++r)
+          if (r < cs) {
+            a.x += x[r].x;
+            a.y += x[r].y;
+            a.z += x[r].z;
+            a.w += x[r].w;
+          }
+        return a;
+      };
+      const int nc4 = (ncols + 3) >> 2;
+      if (sc.swap) {
+        const int lanes = EPI == kEpiSwiGLU ? 64 : 128;
+        const int nl = lanes / cs, L0 = rank * nl;
+        for (int i = te; i < nl * nc4; i += 128) {
+          const int ln = L0 + i % nl, c4 = i / nl;
+          const float4 a = gather((uint32_t)((c4 * 128 + ln) * 16));
+          const float av[4] = {a.x, a.y, a.z, a.w};
+          if constexpr (EPI == kEpiSwiGLU) {
+            const float4 b = gather((uint32_t)((c4 * 128 + ln + 64) * 16));
+            const float bv[4] = {b.x, b.y, b.z, b.w};
+            __nv_bfloat16* o = reinterpret_cast<__nv_bfloat16*>(out);
+            const int j = (n0 >> 1) + ln;
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+              const int m = m0 + 4 * c4 + e;
+              if (m < rows) o[(int64_t)m * ldo + j] = __float2bfloat16(silu(av[e]) * bv[e]);
+            }
+          } else {
+            const int n = n0 + ln;
+            const float bb = (EPI == kEpiBF16 && bias != nullptr) ? __bfloat162float(bias[n]) : 0.f;
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+              const int m = m0 + 4 * c4 + e;
+              if (m >= rows) continue;
+              if constexpr (EPI == kEpiAddF32) {
+                float* o = reinterpret_cast<float*>(out) + (int64_t)m * ldo + n;
+                *o = __ldcg(o) + av[e];
+              } else if constexpr (EPI == kEpiBF16) {
+                reinterpret_cast<__nv_bfloat16*>(out)[(int64_t)m * ldo + n] = __float2bfloat16(av[e] + bb);
+              } else {
+                reinterpret_cast<float*>(out)[(int64_t)m * ldo + n] = av[e];
+              }
+            }
+          }
+        }
+      } else {
+        const int nl = 128 / cs, L0 = rank * nl;
+        const int per = EPI == kEpiSwiGLU ? nc4 / 2 : nc4;  // SwiGLU: gate column groups only
+        for (int i = te; i < nl * per; i += 128) {
+          const int ln = L0 + i / per, k = i % per;
+          const int m = m0 + ln;
+          if (m >= rows) continue;
+          if constexpr (EPI == kEpiSwiGLU) {
+            // [gate 64 | up 64 | gate 64 | up 64]: gate group k -> column group (k/16)*32 + k%16
+            const int gc4 = (k >> 4) * 32 + (k & 15);
+            const float4 g = gather((uint32_t)((ln * 64 + (gc4 ^ (ln & 7))) * 16));
+            const float4 up = gather((uint32_t)((ln * 64 + ((gc4 + 16) ^ (ln & 7))) * 16));
+            const int j = (n0 >> 1) + (k >> 4) * 64 + (k & 15) * 4;
+            uint2 w;
+            w.x = pack_bf16x2(silu(g.x) * up.x, silu(g.y) * up.y);
+            w.y = pack_bf16x2(silu(g.z) * up.z, silu(g.w) * up.w);
+            *reinterpret_cast<uint2*>(reinterpret_cast<__nv_bfloat16*>(out) + (int64_t)m * ldo + j) = w;
+          } else {
+            float4 a = gather((uint32_t)((ln * 64 + (k ^ (ln & 7))) * 16));
+            const int n = n0 + 4 * k;
+            if constexpr (EPI == kEpiAddF32) {
+              float4* o = reinterpret_cast<float4*>(reinterpret_cast<float*>(out) + (int64_t)m * ldo + n);
+              const float4 old = __ldcg(o);
+              *o = make_float4(old.x + a.x, old.y + a.y, old.z + a.z, old.w + a.w);
+            } else if constexpr (EPI == kEpiBF16) {
+              if (bias != nullptr) {
+                const uint2 bb = __ldg(reinterpret_cast<const uint2*>(bias + n));
+                const __nv_bfloat16* b4 = reinterpret_cast<const __nv_bfloat16*>(&bb);
+                a.x += __bfloat162float(b4[0]);
+                a.y += __bfloat162float(b4[1]);
+                a.z += __bfloat162float(b4[2]);
+                a.w += __bfloat162float(b4[3]);
+              }
+              uint2 w;
+              w.x = pack_bf16x2(a.x, a.y);
+              w.y = pack_bf16x2(a.z, a.w);
+              *reinterpret_cast<uint2*>(reinterpret_cast<__nv_bfloat16*>(out) + (int64_t)m * ldo + n) = w;
+            } else {
+              *reinterpret_cast<float4*>(reinterpret_cast<float*>(out) + (int64_t)m * ldo + n) = a;
+            }
+          }
+        }
+      }
+      if (threadIdx.x == 64) trace_mark(trace, 12);
+      cluster_sync_all();  // no rank leaves while others still read its parked partial
+    };
     int t = 0;
-    for (int u = blockIdx.x; u < sc.units; u += gridDim.x, ++t) {
-      int n0, m0, z, kb0, kb1;
-      unit_coords(u, n0, m0, z, kb0, kb1);
+    for (int u = u_first; u < sc.tiles; u += u_step, ++t) {
+      int n0, m0, kb0, kb1;
+      unit_coords(u, n0, m0, kb0, kb1);
       const int acc = t & 1;
       mbar_wait(&tmem_full[acc], (t >> 1) & 1);
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      if (t == 0 && threadIdx.x == 64) trace_mark(trace, 5);
       const uint32_t taddr = tmem + ((uint32_t)(quad * 32) << 16) + (uint32_t)(acc * kMaxBN);
-      const int live = min(bn, rows - m0);  // activation rows of this tile that exist
-      auto release = [&]() {
-        asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+      // columns of the accumulator that carry data: live activation rows (swap) or weight rows
+      const int ncols = sc.swap ? min(sc.an, rows - m0) : min(sc.wn, N - n0);
+      if (split) {
+        split_epilogue(taddr, lrow, ncols, n0, m0);
         __syncwarp();
         if (lane == 0) mbar_arrive(&tmem_empty[acc]);
-      };
-      bool do_epi = true;
-      if (split) {
-        // deterministic split-K: partial tile -> workspace[split]; the last CTA of
-        // the tile sums the partials in split order and runs the epilogue
-        const int n = n0 + lrow;
-        for (int c0 = 0; c0 < live; c0 += 32) {
-          float v[32];
-          tmem_ld32(taddr + c0, v);
-#pragma unroll
-          for (int c = 0; c < 32; ++c) {
-            const int m = m0 + c0 + c;
-            if (m < rows) ws[((int64_t)z * rows + m) * N + n] = v[c];
-          }
-        }
-        release();
-        __threadfence();
-        asm volatile("bar.sync 1, 128;" ::: "memory");
-        if (threadIdx.x == 64) {
-          const int tile = u / sc.splits;
-          const int old = atomicAdd(&cnt[tile], 1);
-          s_last_split = (old == sc.splits - 1);
-          if (s_last_split) cnt[tile] = 0;
-        }
-        asm volatile("bar.sync 1, 128;" ::: "memory");
-        do_epi = s_last_split != 0;
-        asm volatile("bar.sync 1, 128;" ::: "memory");  // s_last_split is reused by the next unit
-        if (!do_epi) continue;
-        __threadfence();
+        continue;
       }
-      auto fetch = [&](int c0, float (&v)[32]) {
-        if (!split) {
-          tmem_ld32(taddr + c0, v);
-          return;
-        }
-        const int n = n0 + lrow;
+      auto fetch = [&](int c0, float (&v)[32]) { tmem_ld32(taddr + c0, v); };
+      const int c_first = 0, c_step = 32;
+      if (!sc.swap) {
+        // ---------------- lane = activation row, columns = weight rows ----------------
+        const int m = m0 + lrow;
+        const bool mine = m < rows;
+        if constexpr (EPI == kEpiSwiGLU) {
+          // 256 weight rows = two interleaved 128-row tiles: [gate 64 | up 64 | gate 64 | up 64]
+#pragma unroll 1
+          for (int h = c_first >> 5; h < 4; h += c_step >> 5) {
+            const int gc = (h >> 1) * 128 + (h & 1) * 32;  // gate chunk column; up = gc + 64
+            float g[32], up[32];
+            fetch(gc, g);
+            fetch(gc + 64, up);
+            if (mine) {
+              const int j0 = (n0 >> 1) + (h >> 1) * 64 + (h & 1) * 32;
+              uint4* dst = reinterpret_cast<uint4*>(reinterpret_cast<__nv_bfloat16*>(out) + (int64_t)m * ldo + j0);
 #pragma unroll
-        for (int c = 0; c < 32; ++c) {
-          const int m = m0 + c0 + c;
-          float a = 0.f;
-          if (m < rows)
-            for (int zz = 0; zz < sc.splits; ++zz) a += __ldcg(&ws[((int64_t)zz * rows + m) * N + n]);
-          v[c] = a;
-        }
-      };
-      if constexpr (EPI == kEpiSwiGLU) {
-        // lanes 0-63: gate rows, lanes 64-127: up rows of the same 64 features
-        const int j = (n0 >> 1) + (lrow & 63);
-        for (int c0 = 0; c0 < live; c0 += 32) {
-          float v[32];
-          fetch(c0, v);
-          if (lrow >= 64) {
-#pragma unroll
-            for (int c = 0; c < 32; ++c) xchg[c * 64 + (lrow - 64)] = v[c];
-          }
-          asm volatile("bar.sync 1, 128;" ::: "memory");
-          if (lrow < 64) {
-            __nv_bfloat16* o = reinterpret_cast<__nv_bfloat16*>(out);
-#pragma unroll
-            for (int c = 0; c < 32; ++c) {
-              const int m = m0 + c0 + c;
-              if (m < rows) o[(int64_t)m * ldo + j] = __float2bfloat16(silu(v[c]) * xchg[c * 64 + lrow]);
+              for (int q = 0; q < 4; ++q) {
+                uint4 w;
+                w.x = pack_bf16x2(silu(g[8 * q + 0]) * up[8 * q + 0], silu(g[8 * q + 1]) * up[8 * q + 1]);
+                w.y = pack_bf16x2(silu(g[8 * q + 2]) * up[8 * q + 2], silu(g[8 * q + 3]) * up[8 * q + 3]);
+                w.z = pack_bf16x2(silu(g[8 * q + 4]) * up[8 * q + 4], silu(g[8 * q + 5]) * up[8 * q + 5]);
+                w.w = pack_bf16x2(silu(g[8 * q + 6]) * up[8 * q + 6], silu(g[8 * q + 7]) * up[8 * q + 7]);
+                dst[q] = w;
+              }
             }
           }
-          asm volatile("bar.sync 1, 128;" ::: "memory");
+        } else {
+#pragma unroll 1
+          for (int c0 = c_first; c0 < ncols; c0 += c_step) {
+            float v[32];
+            fetch(c0, v);
+            if (!mine) continue;
+            const int n = n0 + c0;
+            if constexpr (EPI == kEpiBF16) {
+              if (bias != nullptr) {
+                const uint4* bp = reinterpret_cast<const uint4*>(bias + n);
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                  const uint4 bb = __ldg(bp + q);
+                  const __nv_bfloat16* b8 = reinterpret_cast<const __nv_bfloat16*>(&bb);
+#pragma unroll
+                  for (int e = 0; e < 8; ++e) v[8 * q + e] += __bfloat162float(b8[e]);
+                }
+              }
+              uint4* dst = reinterpret_cast<uint4*>(reinterpret_cast<__nv_bfloat16*>(out) + (int64_t)m * ldo + n);
+#pragma unroll
+              for (int q = 0; q < 4; ++q)
+                dst[q] = make_uint4(pack_bf16x2(v[8 * q], v[8 * q + 1]), pack_bf16x2(v[8 * q + 2], v[8 * q + 3]),
+                                    pack_bf16x2(v[8 * q + 4], v[8 * q + 5]), pack_bf16x2(v[8 * q + 6], v[8 * q + 7]));
+            } else {
+              float4* dst = reinterpret_cast<float4*>(reinterpret_cast<float*>(out) + (int64_t)m * ldo + n);
+              if constexpr (EPI == kEpiAddF32) {
+                float4 old[8];
+#pragma unroll
+                for (int q = 0; q < 8; ++q) old[q] = __ldcg(dst + q);
+#pragma unroll
+                for (int q = 0; q < 8; ++q)
+                  dst[q] = make_float4(old[q].x + v[4 * q], old[q].y + v[4 * q + 1], old[q].z + v[4 * q + 2],
+                                       old[q].w + v[4 * q + 3]);
+              } else {
+#pragma unroll
+                for (int q = 0; q < 8; ++q) dst[q] = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
+              }
+            }
+          }
         }
       } else {
+        // ---------------- swap-AB: lane = weight row, columns = activation rows ----------------
         const int n = n0 + lrow;
-        float bv = 0.f;
-        if (EPI == kEpiBF16 && bias != nullptr) bv = __bfloat162float(bias[n]);
-        for (int c0 = 0; c0 < live; c0 += 32) {
-          float v[32];
-          fetch(c0, v);
-          if constexpr (EPI == kEpiAddF32) {
-            // residual add: issue all 32 loads before any store (independent, in flight together)
-            float* o = reinterpret_cast<float*>(out);
-            float old[32];
+        if constexpr (EPI == kEpiSwiGLU) {
+          // lanes 0-63: gate rows, lanes 64-127: up rows of the same 64 features
+          const int j = (n0 >> 1) + (lrow & 63);
+          for (int c0 = c_first; c0 < ncols; c0 += c_step) {
+            float v[32];
+            fetch(c0, v);
+            if (lrow >= 64) {
 #pragma unroll
-            for (int c = 0; c < 32; ++c) {
-              const int m = m0 + c0 + c;
-              old[c] = m < rows ? __ldcg(o + (int64_t)m * ldo + n) : 0.f;
+              for (int c = 0; c < 32; ++c) xchg[c * 64 + (lrow - 64)] = v[c];
             }
+            asm volatile("bar.sync 1, 128;" ::: "memory");
+            if (lrow < 64) {
+              __nv_bfloat16* o = reinterpret_cast<__nv_bfloat16*>(out);
 #pragma unroll
-            for (int c = 0; c < 32; ++c) {
-              const int m = m0 + c0 + c;
-              if (m < rows) o[(int64_t)m * ldo + n] = old[c] + v[c];
+              for (int c = 0; c < 32; ++c) {
+                const int m = m0 + c0 + c;
+                if (m < rows) o[(int64_t)m * ldo + j] = __float2bfloat16(silu(v[c]) * xchg[c * 64 + lrow]);
+              }
             }
-          } else {
+            asm volatile("bar.sync 1, 128;" ::: "memory");
+          }
+        } else {
+          float bv = 0.f;
+          if (EPI == kEpiBF16 && bias != nullptr) bv = __bfloat162float(bias[n]);
+          for (int c0 = c_first; c0 < ncols; c0 += c_step) {
+            float v[32];
+            fetch(c0, v);
+            if constexpr (EPI == kEpiAddF32) {
+              // residual add: all 32 loads in flight before any store (clamped rows: unconditional loads)
+              float* o = reinterpret_cast<float*>(out);
+              float old[32];
 #pragma unroll
-            for (int c = 0; c < 32; ++c) {
-              const int m = m0 + c0 + c;
-              if (m < rows) {
-                if constexpr (EPI == kEpiBF16) {
-                  reinterpret_cast<__nv_bfloat16*>(out)[(int64_t)m * ldo + n] = __float2bfloat16(v[c] + bv);
-                } else {
-                  reinterpret_cast<float*>(out)[(int64_t)m * ldo + n] = v[c];
+              for (int c = 0; c < 32; ++c) old[c] = __ldcg(o + (int64_t)min(m0 + c0 + c, rows - 1) * ldo + n);
+#pragma unroll
+              for (int c = 0; c < 32; ++c) {
+                const int m = m0 + c0 + c;
+                if (m < rows) o[(int64_t)m * ldo + n] = old[c] + v[c];
+              }
+            } else {
+#pragma unroll
+              for (int c = 0; c < 32; ++c) {
+                const int m = m0 + c0 + c;
+                if (m < rows) {
+                  if constexpr (EPI == kEpiBF16) {
+                    reinterpret_cast<__nv_bfloat16*>(out)[(int64_t)m * ldo + n] = __float2bfloat16(v[c] + bv);
+                  } else {
+                    reinterpret_cast<float*>(out)[(int64_t)m * ldo + n] = v[c];
+                  }
                 }
               }
             }
           }
         }
       }
-      if (!split) release();
+      asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&tmem_empty[acc]);
     }
   }
+  if (split && warp < 2) {
+    // producer and MMA warps join the epilogue's two cluster barriers (one tile per cluster)
+    __syncwarp();
+    cluster_sync_all();
+    cluster_sync_all();
+  }
+  if (threadIdx.x == 64) trace_mark(trace, 6);
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   if (warp == 1) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(kTmemCols));
+  if (threadIdx.x == 0) trace_mark(trace, 7);
+}
+
+int g_trace_on = 0;
+
+__global__ void k_trace_mark(int slot) {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  g_gemm_trace[159 * 16 + slot] = t;
 }
 
 // ---------------------------------------------------------------------------
@@ -423,39 +715,86 @@ void make_map(CUtensorMap* m, const void* ptr, int64_t rows, int64_t cols, int64
 }
 
 template <int EPI>
-void launch_t(const GemmPlan& p, cudaStream_t s) {
-  static bool attr = false;
-  if (!attr) {
+void set_attr() {
+  static bool done = false;
+  if (!done) {
     AB_CUDA(cudaFuncSetAttribute(k_gemm_tc<EPI>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem));
-    attr = true;
+    AB_CUDA(cudaFuncSetAttribute(k_gemm_tc<EPI>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+    done = true;
   }
-  static int sms = 0;
-  if (!sms) {
-    int dev = 0;
-    AB_CUDA(cudaGetDevice(&dev));
-    AB_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+}
+
+// co-resident clusters of `cs` persistent CTAs (one CTA per SM)
+template <int EPI>
+int max_clusters(int cs) {
+  static std::mutex mu;
+  static std::map<int, int> memo;
+  std::lock_guard<std::mutex> lock(mu);
+  auto it = memo.find(cs);
+  if (it != memo.end()) return it->second;
+  set_attr<EPI>();
+  int dev = 0, sms = 0;
+  AB_CUDA(cudaGetDevice(&dev));
+  AB_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  int n = sms;
+  if (cs > 1) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(cs * (sms / cs));
+    cfg.blockDim = dim3(kThreads);
+    cfg.dynamicSmemBytes = kSmem;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = cs;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    AB_CUDA(cudaOccupancyMaxActiveClusters(&n, k_gemm_tc<EPI>, &cfg));
+    AB_REQUIRE(n >= 1, AB_ERR_CONFIG, "GEMM cluster size does not fit on this device");
   }
-  const int zs = (p.ws && p.cnt) ? p.max_splits : 1;
-  // persistent: one CTA per SM (never more CTAs than the largest possible unit count)
-  const int64_t max_units = (int64_t)(p.N / kBM) * ceil_div(p.M_cap, 32) * zs;
-  const int grid = (int)std::min<int64_t>(sms, max_units);
-  k_gemm_tc<EPI><<<grid, kThreads, kSmem, s>>>(p.tw, p.ta, p.N, p.K, p.M_cap, p.rows_dev, p.stop_dev, p.out, p.ldo,
-                                               p.bias, p.ws, p.cnt, zs, p.BN, p.force_bn ? 1 : 0);
+  memo[cs] = n;
+  return n;
+}
+
+int max_clusters_epi(int epi, int cs) {
+  switch (epi) {
+    case kEpiBF16: return max_clusters<kEpiBF16>(cs);
+    case kEpiF32: return max_clusters<kEpiF32>(cs);
+    case kEpiAddF32: return max_clusters<kEpiAddF32>(cs);
+    default: return max_clusters<kEpiSwiGLU>(cs);
+  }
+}
+
+template <int EPI>
+void launch_t(const GemmPlan& p, cudaStream_t s) {
+  set_attr<EPI>();
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(p.grid);
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = kSmem;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = p.cluster;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  AB_CUDA(cudaLaunchKernelEx(&cfg, k_gemm_tc<EPI>, p.tw, p.ta, p.N, p.K, p.M_cap, p.rows_dev, p.stop_dev, p.out,
+                             p.ldo, p.bias, p.sched, g_trace_on));
 }
 
 }  // namespace
 
 void gemm_plan(GemmPlan& p, const __nv_bfloat16* W, int N, int K, const __nv_bfloat16* A, int M_cap, int64_t lda,
                int BN, int epi, void* out, int64_t ldo, const __nv_bfloat16* bias, const int* rows_dev,
-               const int* stop_dev, float* ws, int* cnt, int max_splits) {
+               const int* stop_dev, int cluster) {
   AB_REQUIRE(K % kBK == 0, AB_ERR_CONFIG, "GEMM K must be a multiple of 64");
-  AB_REQUIRE(max_splits >= 1 && max_splits <= 16, AB_ERR_CONFIG, "GEMM max_splits must be in [1, 16]");
-  AB_REQUIRE(max_splits == 1 || (ws && cnt), AB_ERR_CONFIG, "split-K needs a workspace");
-  p.ws = ws;
-  p.cnt = cnt;
-  p.max_splits = max_splits;
+  AB_REQUIRE(cluster == 1 || cluster == 2 || cluster == 4 || cluster == 8, AB_ERR_CONFIG,
+             "GEMM split-K cluster must be 1, 2, 4 or 8");
   AB_REQUIRE(N % kBM == 0, AB_ERR_CONFIG, "GEMM N must be a multiple of 128");
   AB_REQUIRE(BN == 32 || BN == 64 || BN == 128 || BN == 256, AB_ERR_CONFIG, "GEMM BN must be 32/64/128/256");
+  p.cluster = cluster;
   p.N = N;
   p.K = K;
   p.M_cap = M_cap;
@@ -468,6 +807,36 @@ void gemm_plan(GemmPlan& p, const __nv_bfloat16* W, int N, int K, const __nv_bfl
   p.stop_dev = stop_dev;
   make_map(&p.tw, W, N, K, K, kBM);
   make_map(&p.ta, A, M_cap, K, lda, 32);  // activation tiles are loaded as 32-row boxes
+  gemm_set_schedule(p, 0);
+}
+
+void gemm_set_schedule(GemmPlan& p, int force) {
+  // launch geometry: clusters of p.cluster CTAs, never more than the largest possible tile count needs
+  const int cs = p.cluster;
+  const int ncl_max = max_clusters_epi(p.epi, cs);
+  const int64_t max_tiles = (int64_t)ceil_div(p.N, kBM) * ceil_div(p.M_cap, 32);
+  const int ncl = (int)std::min<int64_t>(ncl_max, cs > 1 ? max_tiles : ceil_div(max_tiles, 1));
+  p.grid = ncl * cs;
+  p.force = force;
+  // one device table per distinct (shape, geometry): the kernel reads sched[rows]
+  static std::mutex mu;
+  static std::map<std::tuple<int, int, int, int, int, int, int, int>, int*> cache;
+  int dev = 0;
+  AB_CUDA(cudaGetDevice(&dev));
+  const auto key = std::make_tuple(p.N, p.K, p.M_cap, p.BN, cs, force, p.epi, ncl * 16 + dev);
+  std::lock_guard<std::mutex> lock(mu);
+  auto it = cache.find(key);
+  if (it != cache.end()) {
+    p.sched = it->second;
+    return;
+  }
+  std::vector<int> tab(p.M_cap + 1, 0);
+  for (int r = 1; r <= p.M_cap; ++r) tab[r] = choose_sched(r, p.N, p.K, p.BN, cs, ncl, force, p.epi);
+  int* d = nullptr;
+  AB_CUDA(cudaMalloc(&d, sizeof(int) * tab.size()));
+  AB_CUDA(cudaMemcpy(d, tab.data(), sizeof(int) * tab.size(), cudaMemcpyHostToDevice));
+  cache[key] = d;
+  p.sched = d;
 }
 
 void make_tmap_bf16(CUtensorMap* m, const void* ptr, int64_t rows, int64_t cols, int64_t ld, int box_cols,
@@ -498,24 +867,18 @@ void gemm_launch(const GemmPlan& p, cudaStream_t s) {
 extern "C" int ab_debug_gemm_time(const void* W, const void* A, void* out, const void* bias, int N, int K, int M,
                                   int BN, int epi, int reps, float* ms_out) {
   try {
-    static float* ws = nullptr;
-    static int* cnt = nullptr;
     static void* flush = nullptr;
-    // epi bit 4: split-K allowed (up to 8 splits); bit 5: automatic tile width (BN = max)
+    // epi bit 4: cluster split-K allowed (cluster of 8); bit 5: automatic schedule (BN = max activation
+    // tile); bit 6: forced no-swap schedule with BN weight rows; bit 7: BN is a fixed schedule code;
+    // else forced swap-AB with BN activation rows
     const int max_splits = (epi & 16) ? 8 : 1;
-    const bool force = (epi & 32) == 0;
+    const int force = (epi & 128) ? (0x40000000 | BN) : (epi & 32) ? 0 : (epi & 64) ? -BN : BN;
     epi &= 15;
-    if (!ws) {
-      AB_CUDA(cudaMalloc(&ws, sizeof(float) * ab::kGemmWsElems));
-      AB_CUDA(cudaMalloc(&cnt, sizeof(int) * ab::kGemmCounters));
-      AB_CUDA(cudaMemset(cnt, 0, sizeof(int) * ab::kGemmCounters));
-      AB_CUDA(cudaMalloc(&flush, size_t(256) << 20));
-    }
+    if (!flush) AB_CUDA(cudaMalloc(&flush, size_t(256) << 20));
     ab::GemmPlan p;
-    ab::gemm_plan(p, (const __nv_bfloat16*)W, N, K, (const __nv_bfloat16*)A, M, K, BN, epi, out,
-                  epi == ab::kEpiSwiGLU ? N / 2 : N, (const __nv_bfloat16*)bias, nullptr, nullptr,
-                  max_splits > 1 ? ws : nullptr, max_splits > 1 ? cnt : nullptr, max_splits);
-    p.force_bn = force;
+    ab::gemm_plan(p, (const __nv_bfloat16*)W, N, K, (const __nv_bfloat16*)A, M, K, (force > 0 && (force & 0x40000000)) ? 256 : BN, epi, out,
+                  epi == ab::kEpiSwiGLU ? N / 2 : N, (const __nv_bfloat16*)bias, nullptr, nullptr, max_splits);
+    ab::gemm_set_schedule(p, force);
     ab::gemm_launch(p, 0);  // warm: kernel attributes, TMA descriptors
     std::vector<float> t(reps);
     cudaEvent_t a, b;
@@ -545,25 +908,53 @@ extern "C" int ab_debug_gemm(const void* W, const void* A, void* out, const void
                              int epi) {
   // epi >= 16: the same epilogue (epi - 16) with split-K enabled (up to 8 splits)
   try {
-    static float* ws = nullptr;
-    static int* cnt = nullptr;
-    // epi bit 4: split-K allowed (up to 8 splits); bit 5: automatic tile width (BN = max)
+    // epi bit 4: cluster split-K allowed (cluster of 8); bit 5: automatic schedule (BN = max activation
+    // tile); bit 6: forced no-swap schedule with BN weight rows; bit 7: BN is a fixed schedule code;
+    // else forced swap-AB with BN activation rows
     const int max_splits = (epi & 16) ? 8 : 1;
-    const bool force = (epi & 32) == 0;
+    const int force = (epi & 128) ? (0x40000000 | BN) : (epi & 32) ? 0 : (epi & 64) ? -BN : BN;
     epi &= 15;
-    if (max_splits > 1 && !ws) {
-      AB_CUDA(cudaMalloc(&ws, sizeof(float) * ab::kGemmWsElems));
-      AB_CUDA(cudaMalloc(&cnt, sizeof(int) * ab::kGemmCounters));
-      AB_CUDA(cudaMemset(cnt, 0, sizeof(int) * ab::kGemmCounters));
-    }
     ab::GemmPlan p;
-    ab::gemm_plan(p, (const __nv_bfloat16*)W, N, K, (const __nv_bfloat16*)A, M, K, BN, epi, out,
-                  epi == ab::kEpiSwiGLU ? N / 2 : N, (const __nv_bfloat16*)bias, nullptr, nullptr,
-                  max_splits > 1 ? ws : nullptr, max_splits > 1 ? cnt : nullptr, max_splits);
-    p.force_bn = force;
+    ab::gemm_plan(p, (const __nv_bfloat16*)W, N, K, (const __nv_bfloat16*)A, M, K, (force > 0 && (force & 0x40000000)) ? 256 : BN, epi, out,
+                  epi == ab::kEpiSwiGLU ? N / 2 : N, (const __nv_bfloat16*)bias, nullptr, nullptr, max_splits);
+    ab::gemm_set_schedule(p, force);
     ab::gemm_launch(p, 0);
     AB_CUDA(cudaGetLastError());
     AB_CUDA(cudaDeviceSynchronize());
+    return AB_OK;
+  } catch (const ab::Error& e) {
+    ab::set_last_error(e.what());
+    return e.code;
+  }
+}
+
+// Debug: run the next ab_debug_gemm with the per-CTA timeline enabled and copy
+// it out ([160][8] ns timestamps, 0 = not reached).
+extern "C" int ab_debug_gemm_trace(int on, unsigned long long* out) {
+  try {
+    if (on) {
+      unsigned long long z[160 * 16] = {};
+      AB_CUDA(cudaMemcpyToSymbol(ab::g_gemm_trace, z, sizeof(z)));
+    }
+    ab::g_trace_on = on;
+    if (out) AB_CUDA(cudaMemcpyFromSymbol(out, ab::g_gemm_trace, sizeof(unsigned long long) * 160 * 16));
+    return AB_OK;
+  } catch (const ab::Error& e) {
+    ab::set_last_error(e.what());
+    return e.code;
+  }
+}
+
+// Debug: one-thread kernel writing %globaltimer into trace row 159, column `slot`.
+extern "C" int ab_debug_trace_mark(int slot) {
+  ab::k_trace_mark<<<1, 1>>>(slot);
+  return cudaGetLastError() == cudaSuccess ? AB_OK : AB_ERR_CUDA;
+}
+
+// Debug: co-resident persistent clusters of `cs` GEMM CTAs on this device.
+extern "C" int ab_debug_gemm_clusters(int cs, int* out) {
+  try {
+    *out = ab::max_clusters_epi(ab::kEpiF32, cs);
     return AB_OK;
   } catch (const ab::Error& e) {
     ab::set_last_error(e.what());

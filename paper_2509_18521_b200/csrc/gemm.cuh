@@ -29,21 +29,22 @@ struct GemmPlan {
   const __nv_bfloat16* bias = nullptr;
   const int* rows_dev = nullptr;  // live row count on device (nullptr: M_cap)
   const int* stop_dev = nullptr;  // engine stop flag (nullptr: never stop)
-  // deterministic split-K (decode GEMMs whose tile count cannot fill the SMs):
-  // the kernel picks splits <= max_splits from the live row count on device
-  float* ws = nullptr;  // shared workspace (kWsElems fp32), stream-ordered
-  int* cnt = nullptr;   // per-tile arrival counters (>= N/128 * M_cap/BN, zeroed once)
-  int max_splits = 1;
-  bool force_bn = false;  // BN is exact (tests) instead of the upper bound of the on-device choice
+  // deterministic split-K inside a thread-block cluster of `cluster` CTAs (1 = none):
+  // the schedule table picks split = cluster (one tile per cluster) or none per row count
+  int cluster = 1;
+  int grid = 0;  // persistent CTAs (a multiple of cluster)
+  // tests: > 0 forces swap-AB with exactly `force` activation rows per tile, < 0 forces the
+  // no-swap schedule with -force weight rows per tile, 0 = on-device choice
+  int force = 0;
+  const int* sched = nullptr;  // device table: packed schedule per live row count [0, M_cap]
 };
-
-constexpr int64_t kGemmWsElems = int64_t(32) << 20;
-constexpr int kGemmCounters = 1 << 16;
 
 void gemm_plan(GemmPlan& p, const __nv_bfloat16* W, int N, int K, const __nv_bfloat16* A, int M_cap, int64_t lda,
                int BN, int epi, void* out, int64_t ldo, const __nv_bfloat16* bias, const int* rows_dev,
-               const int* stop_dev, float* ws = nullptr, int* cnt = nullptr, int max_splits = 1);
+               const int* stop_dev, int cluster = 1);
 void gemm_launch(const GemmPlan& p, cudaStream_t s);
+// Rebuild the plan's schedule table (force: see GemmPlan::force).
+void gemm_set_schedule(GemmPlan& p, int force);
 
 // 2-D bf16 TMA map: [rows, cols] with leading dimension `ld` elements, box {box_cols, box_rows},
 // 128-byte swizzle (box_cols * 2 must be <= 128).

@@ -41,8 +41,6 @@ struct Model {
   GemmPlan lm_dec;
   int* pf_rows = nullptr;  // device row count for prefill GEMMs
   CUtensorMap kvmap;         // TMA view of the KV pool for the decode attention
-  float* gemm_ws = nullptr;  // split-K partial tiles (shared by all decode GEMMs, stream-ordered)
-  int* gemm_cnt = nullptr;   // split-K arrival counters (self-resetting)
   int32_t *seg_start = nullptr, *seg_group = nullptr, *ga_g = nullptr, *ga_len = nullptr, *ga_last = nullptr;
   int32_t* host_stage = nullptr;
   size_t host_stage_cap = 0;
@@ -226,20 +224,15 @@ Model* model_create(Engine& e) {
   const int* b = &e.d.ctl->b;
   const int* stop = &e.d.ctl->stop;
   const int bn_dec = pick_bn(M->S);
-  M->gemm_ws = dalloc<float>(kGemmWsElems);
-  M->gemm_cnt = dalloc<int>(kGemmCounters);
-  float* ws = M->gemm_ws;
-  int* cnt = M->gemm_cnt;
   for (int l = 0; l < m.L; ++l) {
     const LayerW& w = M->layers[l];
     Model::Plans d, p;
     gemm_plan(d.qkv, w.wqkv, m.qkv_dim, m.d, M->xn, M->S, m.d, bn_dec, kEpiBF16, M->qkv, m.qkv_dim, w.bqkv, b, stop,
-              ws, cnt, 4);
-    gemm_plan(d.o, w.wo, m.d, m.qd, M->attn, M->S, m.qd, bn_dec, kEpiAddF32, M->x, m.d, nullptr, b, stop, ws, cnt, 4);
-    gemm_plan(d.gu, w.wgu, 2 * m.f, m.d, M->xn, M->S, m.d, bn_dec, kEpiSwiGLU, M->hbuf, m.f, nullptr, b, stop, ws,
-              cnt, 4);
-    gemm_plan(d.down, w.wd, m.d, m.f, M->hbuf, M->S, m.f, bn_dec, kEpiAddF32, M->x, m.d, nullptr, b, stop, ws, cnt,
               8);
+    gemm_plan(d.o, w.wo, m.d, m.qd, M->attn, M->S, m.qd, bn_dec, kEpiAddF32, M->x, m.d, nullptr, b, stop, 8);
+    gemm_plan(d.gu, w.wgu, 2 * m.f, m.d, M->xn, M->S, m.d, bn_dec, kEpiSwiGLU, M->hbuf, m.f, nullptr, b, stop,
+              4);
+    gemm_plan(d.down, w.wd, m.d, m.f, M->hbuf, M->S, m.f, bn_dec, kEpiAddF32, M->x, m.d, nullptr, b, stop, 8);
     gemm_plan(p.qkv, w.wqkv, m.qkv_dim, m.d, M->xn, M->M_pf, m.d, 256, kEpiBF16, M->qkv, m.qkv_dim, w.bqkv,
               M->pf_rows, nullptr);
     gemm_plan(p.o, w.wo, m.d, m.qd, M->attn, M->M_pf, m.qd, 256, kEpiAddF32, M->x, m.d, nullptr, M->pf_rows,
@@ -265,7 +258,7 @@ void model_destroy(Model* M) {
                   M->logits,   M->part_o,   M->part_ml,   m.row_tok,    m.row_pos,    m.row_btrow, m.h_ctx,
                   m.h_last_tok, m.h_shared, m.g_ctx,      m.g_last_tok, m.g_npages,   m.bt,        m.rope,
                   M->pf_rows,  M->seg_start, M->seg_group, M->ga_g,     M->ga_len,    M->ga_last,  m.kv,
-                  m.free_pages, m.split_prefix, m.att_counter, M->gemm_ws, M->gemm_cnt};
+                  m.free_pages, m.split_prefix, m.att_counter};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   if (M->host_stage) cudaFreeHost(M->host_stage);

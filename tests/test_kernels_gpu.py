@@ -15,7 +15,7 @@ def _ptr(t):
     return C.c_void_p(t.data_ptr()) if t is not None else None
 
 
-@pytest.mark.parametrize("bn", [32, 64, 128, 256])
+@pytest.mark.parametrize("bn", [32, 64, 128, 256, -128, -256])  # < 0: no-swap schedule, -bn weight rows per tile
 @pytest.mark.parametrize("shape", [(256, 128, 1), (512, 1536, 37), (2048, 1536, 300), (384, 256, 1000)])
 @pytest.mark.parametrize("epi", [0, 1, 2, 16, 17, 18])  # +16: deterministic split-K enabled
 def test_tcgen05_gemm_matches_torch(bn, shape, epi):
@@ -36,6 +36,8 @@ def test_tcgen05_gemm_matches_torch(bn, shape, epi):
         base = torch.randn(M, N, device="cuda", generator=g)
         out = base.clone()
         ref = ref + base
+    if bn < 0:
+        bn, epi_code = -bn, epi_code + 64
     _capi.call("ab_debug_gemm", _ptr(W), _ptr(A), _ptr(out), _ptr(bias), N, K, M, bn, epi_code)
     torch.cuda.synchronize()
     if split:  # deterministic: a second run is bit-identical
@@ -47,14 +49,14 @@ def test_tcgen05_gemm_matches_torch(bn, shape, epi):
     torch.testing.assert_close(out.float(), ref, rtol=tol, atol=tol * max(1.0, ref.abs().max().item() * 0.01))
 
 
-@pytest.mark.parametrize("epi", [3, 19])
+@pytest.mark.parametrize("epi", [3, 19, 3 + 64, 19 + 64])  # +64: activation rows on the UMMA M side
 def test_tcgen05_gemm_swiglu_epilogue(epi):
     N, K, M = 512, 1024, 77  # N = 2 * features, rows interleaved in 64-row halves per 128-row tile
     g = torch.Generator(device="cuda").manual_seed(5)
     W = (torch.randn(N, K, device="cuda", generator=g) * 0.05).to(torch.bfloat16)
     A = torch.randn(M, K, device="cuda", generator=g).to(torch.bfloat16)
     out = torch.empty(M, N // 2, device="cuda", dtype=torch.bfloat16)
-    _capi.call("ab_debug_gemm", _ptr(W), _ptr(A), _ptr(out), None, N, K, M, 64, epi)
+    _capi.call("ab_debug_gemm", _ptr(W), _ptr(A), _ptr(out), None, N, K, M, 256 if epi & 64 else 64, epi)
     acc = A.float() @ W.float().t()
     t = acc.view(M, N // 128, 2, 64)
     ref = (torch.nn.functional.silu(t[:, :, 0]) * t[:, :, 1]).reshape(M, N // 2)

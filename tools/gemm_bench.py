@@ -24,9 +24,10 @@ SHAPES = {  # name: (N, K, epi)   Qwen2.5-1.5B decode projections
 }
 
 
-def run(N, K, M, epi, bn, reps, split):
+def run(N, K, M, epi, bn, reps, split, cublas=True):
     W = (torch.randn(N, K, device="cuda") * 0.02).to(torch.bfloat16)
     A = torch.randn(M, K, device="cuda").to(torch.bfloat16)
+    flags, epi = epi & ~15, epi & 15
     bias = torch.zeros(N, device="cuda", dtype=torch.bfloat16) if epi == 0 else None
     if epi == 3:
         out = torch.empty(M, N // 2, device="cuda", dtype=torch.bfloat16)
@@ -34,12 +35,14 @@ def run(N, K, M, epi, bn, reps, split):
         out = torch.empty(M, N, device="cuda", dtype=torch.bfloat16)
     else:
         out = torch.zeros(M, N, device="cuda", dtype=torch.float32)
-    code = epi + (16 if split else 0) + (32 if bn == 0 else 0)  # bn 0: on-device tile choice (decode path)
+    code = epi + flags + (16 if split else 0) + (32 if bn == 0 else 0)  # bn 0: schedule table (decode path)
     args = (C.c_void_p(W.data_ptr()), C.c_void_p(A.data_ptr()), C.c_void_p(out.data_ptr()),
             C.c_void_p(bias.data_ptr()) if bias is not None else None, N, K, M, bn or 256, code)
     msv = C.c_float()
     _capi.call("ab_debug_gemm_time", *args, reps, C.byref(msv))  # device-timed, L2 flushed, median
     ms = msv.value
+    if not cublas:
+        return {"us": round(ms * 1e3, 1)}
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
     # cuBLAS reference for the same contraction
     for _ in range(3):
@@ -61,13 +64,38 @@ def run(N, K, M, epi, bn, reps, split):
             "cublas_us": round(cms * 1e3, 1), "cublas_TFLOP/s": round(flops / cms / 1e9, 1)}
 
 
+def sweep(args):
+    """Time every fixed schedule (swap / tile / split-K) per shape and row count."""
+    for name, (N, K, epi) in SHAPES.items():
+        for M in args.m:
+            res = []
+            for swap in (1, 0):
+                for t in ((32, 64, 128, 256) if swap else (128, 256)):
+                    if not swap and (N % 128 or (epi == 3 and (t != 256 or N % 256))):
+                        continue
+                    for sp in (1, 8):  # split-K = the debug cluster size (8)
+                        if K // 64 < 2 * sp:
+                            continue
+                        lg = t.bit_length() - 1
+                        code = swap | (lg << 1) | (sp << 5)
+                        r = run(N, K, M, epi | 16 | 128, code, args.reps, False, cublas=False)
+                        res.append((r["us"], swap, t, sp))
+            auto = run(N, K, M, epi, 0, args.reps, True)
+            res.sort()
+            print(json.dumps({"shape": name, "M": M, "auto_us": auto["us"], "cublas_us": auto["cublas_us"],
+                              "best": res[:4]}), flush=True)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--m", type=int, nargs="+", default=[1024, 256, 64, 8])
     ap.add_argument("--reps", type=int, default=15)
     ap.add_argument("--bn", type=int, nargs="+", default=[0], help="activation tile width; 0 = automatic (as the decode path)")
     ap.add_argument("--split", type=int, default=1)
+    ap.add_argument("--sweep", action="store_true")
     args = ap.parse_args()
+    if args.sweep:
+        return sweep(args)
     res = []
     for name, (N, K, epi) in SHAPES.items():
         for M in args.m:
