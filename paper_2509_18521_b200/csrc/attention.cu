@@ -33,6 +33,7 @@ constexpr int kThreads = (kCons + 1) * 32;
 constexpr int kStages = 3;
 constexpr int kQSlots = 3;
 constexpr int kMergeRows = 8;   // GQA group <= 8
+constexpr int kMaxSplits = 64;  // KV splits per row (the model sizes the minimum split to respect it)
 
 struct Meta {
   int row, kvh, sp, c0, c1, tile, ntiles, nsplit, qslot, done, pad0, pad1;
@@ -44,11 +45,13 @@ struct AttCfg {
   static constexpr int kQ = kMergeRows * HD * 2;
   static constexpr int oQ = kStages * 2 * kKV;
   static constexpr int oZero = oQ + kQSlots * kQ;
-  static constexpr int oMerge = oZero + HD * 2;
-  static constexpr int oML = oMerge + kMergeRows * HD * 4;
-  static constexpr int oMeta = oML + kCons * 16 * 2 * 4;
+  static constexpr int oML = oZero + HD * 2;                       // [kCons][kMergeRows] (m, l)
+  static constexpr int oMLs = oML + kCons * kMergeRows * 8;        // [kMergeRows][kMaxSplits] split (m, l)
+  static constexpr int oMeta = oMLs + kMergeRows * kMaxSplits * 8;
   static constexpr int oBar = oMeta + kStages * (int)sizeof(Meta);
   static constexpr int kSmem = 1024 + oBar + 2 * kStages * 8;
+  // the 4 consumer warps' unscaled outputs are merged in the K half of the item's last stage
+  static_assert(kCons * kMergeRows * HD * 4 <= kKV, "merge buffer must fit in a K tile");
 };
 
 __device__ __forceinline__ uint32_t su32(const void* p) { return static_cast<uint32_t>(__cvta_generic_to_shared(p)); }
@@ -120,19 +123,18 @@ template <int HD>
 __global__ void __launch_bounds__(kThreads, 2)
     k_decode_attn(const __grid_constant__ CUtensorMap kvmap, EngineDev e, ModelDev m, int layer,
                   const bf16* __restrict__ q, bf16* __restrict__ out, float* __restrict__ part_o,
-                  float* __restrict__ part_ml, int max_splits, int chunk) {
+                  float* __restrict__ part_ml, int max_splits) {
   using Cfg = AttCfg<HD>;
   const Ctl* c = e.ctl;
   if (c->stop) return;
   const int b = c->b;
   if (b <= 0) return;
   const int total = m.split_prefix[b] * m.hk;
-  if ((int)blockIdx.x >= total) return;
 
   extern __shared__ uint8_t smem_raw[];
   uint8_t* base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  float* sMerge = reinterpret_cast<float*>(base + Cfg::oMerge);  // [kMergeRows][HD]
-  float* sML = reinterpret_cast<float*>(base + Cfg::oML);        // [kCons][16][2]
+  float2* sML = reinterpret_cast<float2*>(base + Cfg::oML);    // [kCons][kMergeRows]
+  float2* sMLs = reinterpret_cast<float2*>(base + Cfg::oMLs);  // [kMergeRows][kMaxSplits]
   Meta* meta = reinterpret_cast<Meta*>(base + Cfg::oMeta);
   uint64_t* full = reinterpret_cast<uint64_t*>(base + Cfg::oBar);
   uint64_t* empty = full + kStages;
@@ -155,10 +157,14 @@ __global__ void __launch_bounds__(kThreads, 2)
     // ------------------------------ producer ------------------------------
     if (lane == 0) {
       asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&kvmap)) : "memory");
+      const int chunk = m.att_ctl[0];
       const uint32_t qbytes = (uint32_t)(gq * HD * 2);
       const int box_rows = m.P < kTok ? m.P : kTok;
-      int g = 0, k = 0;
-      for (int item = blockIdx.x; item < total; item += gridDim.x, ++k) {
+      int g = 0;
+      for (int k = 0;; ++k) {
+        // work items are pulled dynamically (one cursor per layer, reset by the prep kernel)
+        const int item = atomicAdd(&m.att_ctl[1 + layer], 1);
+        if (item >= total) break;
         const int rs = item / m.hk, kvh = item % m.hk;
         const int packed = m.att_items[rs];
         const int row = packed & 0xffff, sp = packed >> 16;
@@ -212,6 +218,7 @@ __global__ void __launch_bounds__(kThreads, 2)
 
   // ------------------------------ consumers ------------------------------
   const int gr = lane >> 2, tq = lane & 3;
+  const int tid = threadIdx.x;  // 0..127
   const float scale = rsqrtf((float)HD) * kLog2e;
   float o[HD / 8][4];
   float mrow[2] = {-FLT_MAX, -FLT_MAX}, lrow[2] = {0.f, 0.f};
@@ -292,101 +299,115 @@ __global__ void __launch_bounds__(kThreads, 2)
       mma16816(o[2 * nt2 + 1], pa, bb[2], bb[3]);
     }
     __syncwarp();
-    if (lane == 0) mbar_arrive(&empty[st]);  // this warp is done with the stage
-    if (mt.tile != mt.ntiles - 1) continue;
+    if (mt.tile != mt.ntiles - 1) {
+      if (lane == 0) mbar_arrive(&empty[st]);  // this warp is done with the stage
+      continue;
+    }
 
-    // ---- item complete: merge the 4 warps in a fixed order, then emit ----
+    // ---- item complete: the item's last stage stays claimed; its K half holds the
+    // 4 warps' unscaled outputs, merged in one pass (fixed warp order: deterministic) ----
 #pragma unroll
     for (int r = 0; r < 2; ++r) {
       lrow[r] += __shfl_xor_sync(0xffffffffu, lrow[r], 1);
       lrow[r] += __shfl_xor_sync(0xffffffffu, lrow[r], 2);
     }
-    if (tq == 0) {
-      sML[(warp * 16 + gr) * 2] = mrow[0];
-      sML[(warp * 16 + gr) * 2 + 1] = lrow[0];
-      sML[(warp * 16 + gr + 8) * 2] = mrow[1];
-      sML[(warp * 16 + gr + 8) * 2 + 1] = lrow[1];
+    float* sO = reinterpret_cast<float*>(base + st * 2 * Cfg::kKV);  // [kCons][kMergeRows][HD]
+    cons_sync();  // every warp is done reading this stage's K / V
+    if (gr < gq) {
+      float* dst = sO + (warp * kMergeRows + gr) * HD;
+#pragma unroll
+      for (int nt = 0; nt < HD / 8; ++nt)
+        *reinterpret_cast<float2*>(dst + nt * 8 + tq * 2) = make_float2(o[nt][0], o[nt][1]);
+      if (tq == 0) sML[warp * kMergeRows + gr] = make_float2(mrow[0], lrow[0]);
     }
     cons_sync();
-    float sc = 0.f;
-    if (gr < gq) {
-      float M = -FLT_MAX;
-      for (int w = 0; w < kCons; ++w) M = fmaxf(M, sML[(w * 16 + gr) * 2]);
-      sc = mrow[0] == -FLT_MAX ? 0.f : exp2f(mrow[0] - M);
-    }
-    for (int w = 0; w < kCons; ++w) {
-      if (warp == w && gr < gq) {
-        float* dst = sMerge + gr * HD;
-#pragma unroll
-        for (int nt = 0; nt < HD / 8; ++nt) {
-          float2* p2 = reinterpret_cast<float2*>(dst + nt * 8 + tq * 2);
-          const float2 add = make_float2(o[nt][0] * sc, o[nt][1] * sc);
-          if (w == 0) {
-            *p2 = add;
-          } else {
-            float2 cur = *p2;
-            *p2 = make_float2(cur.x + add.x, cur.y + add.y);
-          }
-        }
-      }
-      cons_sync();
-    }
     const int i = mt.row, kvh = mt.kvh, sp = mt.sp, nsplit = mt.nsplit;
-    for (int idx = threadIdx.x; idx < gq * HD; idx += kCons * 32) {
-      const int row = idx / HD, dcol = idx % HD;
-      float M = -FLT_MAX, L = 0.f;
-      for (int w = 0; w < kCons; ++w) M = fmaxf(M, sML[(w * 16 + row) * 2]);
+    for (int idx = tid; idx < gq * (HD / 4); idx += kCons * 32) {
+      const int row = idx / (HD / 4), d4 = idx % (HD / 4);
+      float M = -FLT_MAX;
+#pragma unroll
+      for (int w = 0; w < kCons; ++w) M = fmaxf(M, sML[w * kMergeRows + row].x);
+      float L = 0.f;
+      float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
       for (int w = 0; w < kCons; ++w) {
-        const float mw = sML[(w * 16 + row) * 2];
-        if (mw != -FLT_MAX) L += sML[(w * 16 + row) * 2 + 1] * exp2f(mw - M);
+        const float2 ml = sML[w * kMergeRows + row];
+        const float wgt = ml.x == -FLT_MAX ? 0.f : exp2f(ml.x - M);
+        L += ml.y * wgt;
+        const float4 v = *reinterpret_cast<const float4*>(sO + (w * kMergeRows + row) * HD + d4 * 4);
+        acc.x += v.x * wgt;
+        acc.y += v.y * wgt;
+        acc.z += v.z * wgt;
+        acc.w += v.w * wgt;
       }
-      const float acc = sMerge[row * HD + dcol];
       const int head = kvh * gq + row;
       if (nsplit == 1) {
-        out[(size_t)i * m.qd + head * HD + dcol] = __float2bfloat16(acc / L);
+        const float inv = 1.f / L;
+        uint2 w2;
+        w2.x = pack_bf16(acc.x * inv, acc.y * inv);
+        w2.y = pack_bf16(acc.z * inv, acc.w * inv);
+        *reinterpret_cast<uint2*>(out + (size_t)i * m.qd + head * HD + d4 * 4) = w2;
       } else {
         const size_t pb = ((size_t)i * m.hq + head) * max_splits + sp;
-        part_o[pb * HD + dcol] = acc;
-        if (dcol == 0) {
-          part_ml[pb * 2] = M;
-          part_ml[pb * 2 + 1] = L;
-        }
+        *reinterpret_cast<float4*>(part_o + pb * HD + d4 * 4) = acc;
+        if (d4 == 0) *reinterpret_cast<float2*>(part_ml + pb * 2) = make_float2(M, L);
       }
     }
+    cons_sync();  // merge reads of the stage are done: hand it back to the producer
+    if (lane == 0) mbar_arrive(&empty[st]);
     if (nsplit > 1) {
-      __threadfence();
-      cons_sync();
-      if (threadIdx.x == 0) {
+      // split combine by the last CTA to finish a split of this (row, kv head): split order, deterministic
+      if (tid == 0) {
+        __threadfence();
         const int old = atomicAdd(&m.att_counter[i * m.hk + kvh], 1);
-        s_last = (old == nsplit - 1);
-        if (s_last) m.att_counter[i * m.hk + kvh] = 0;
+        const int last = old == nsplit - 1;
+        if (last) {
+          m.att_counter[i * m.hk + kvh] = 0;
+          __threadfence();
+        }
+        s_last = last;
       }
       cons_sync();
       if (s_last) {
-        __threadfence();
-        for (int idx = threadIdx.x; idx < gq * HD; idx += kCons * 32) {
-          const int row = idx / HD, dcol = idx % HD;
+        for (int idx = tid; idx < gq * nsplit; idx += kCons * 32) {
+          const int row = idx / nsplit, s2 = idx % nsplit;
+          const size_t pb = ((size_t)i * m.hq + kvh * gq + row) * max_splits + s2;
+          sMLs[row * kMaxSplits + s2] = __ldcg(reinterpret_cast<const float2*>(part_ml + pb * 2));
+        }
+        cons_sync();
+        for (int idx = tid; idx < gq * (HD / 4); idx += kCons * 32) {
+          const int row = idx / (HD / 4), d4 = idx % (HD / 4);
           const int head = kvh * gq + row;
-          const size_t pb = ((size_t)i * m.hq + head) * max_splits;
+          const float2* ml = sMLs + row * kMaxSplits;
           float M = -FLT_MAX;
-          for (int s2 = 0; s2 < nsplit; ++s2) M = fmaxf(M, __ldcg(&part_ml[(pb + s2) * 2]));
-          float L = 0.f, acc = 0.f;
+          for (int s2 = 0; s2 < nsplit; ++s2) M = fmaxf(M, ml[s2].x);
+          const float4* src = reinterpret_cast<const float4*>(part_o + ((size_t)i * m.hq + head) * max_splits * HD) + d4;
+          float L = 0.f;
+          float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll 4
           for (int s2 = 0; s2 < nsplit; ++s2) {
-            const float w = exp2f(__ldcg(&part_ml[(pb + s2) * 2]) - M);
-            L += __ldcg(&part_ml[(pb + s2) * 2 + 1]) * w;
-            acc += __ldcg(&part_o[(pb + s2) * HD + dcol]) * w;
+            const float wgt = exp2f(ml[s2].x - M);
+            const float4 v = __ldcg(src + (size_t)s2 * (HD / 4));
+            L += ml[s2].y * wgt;
+            acc.x += v.x * wgt;
+            acc.y += v.y * wgt;
+            acc.z += v.z * wgt;
+            acc.w += v.w * wgt;
           }
-          out[(size_t)i * m.qd + head * HD + dcol] = __float2bfloat16(acc / L);
+          const float inv = 1.f / L;
+          uint2 w2;
+          w2.x = pack_bf16(acc.x * inv, acc.y * inv);
+          w2.y = pack_bf16(acc.z * inv, acc.w * inv);
+          *reinterpret_cast<uint2*>(out + (size_t)i * m.qd + head * HD + d4 * 4) = w2;
         }
       }
+      cons_sync();  // s_last / sMLs are reused by the next item
     }
-    cons_sync();  // sML / sMerge are reused by the next item
   }
 }
 
 template <int HD>
-void launch_t(const CUtensorMap& map, const EngineDev& e, const ModelDev& m, int layer, const bf16* q, bf16* out,
-              float* part_o, float* part_ml, int max_splits, int chunk, cudaStream_t s) {
+int grid_t() {
   static int grid = 0;
   if (!grid) {
     AB_CUDA(cudaFuncSetAttribute(k_decode_attn<HD>, cudaFuncAttributeMaxDynamicSharedMemorySize, AttCfg<HD>::kSmem));
@@ -396,8 +417,14 @@ void launch_t(const CUtensorMap& map, const EngineDev& e, const ModelDev& m, int
     AB_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
     grid = sms * (per_sm > 0 ? per_sm : 1);
   }
-  k_decode_attn<HD><<<grid, kThreads, AttCfg<HD>::kSmem, s>>>(map, e, m, layer, q, out, part_o, part_ml, max_splits,
-                                                              chunk);
+  return grid;
+}
+
+template <int HD>
+void launch_t(const CUtensorMap& map, const EngineDev& e, const ModelDev& m, int layer, const bf16* q, bf16* out,
+              float* part_o, float* part_ml, int max_splits, cudaStream_t s) {
+  k_decode_attn<HD><<<grid_t<HD>(), kThreads, AttCfg<HD>::kSmem, s>>>(map, e, m, layer, q, out, part_o, part_ml,
+                                                                      max_splits);
 }
 
 }  // namespace
@@ -411,12 +438,16 @@ void make_kv_tmap(CUtensorMap* map, const ModelDev& m) {
   make_tmap_bf16(map, m.kv, rows, m.hd, m.hd, 64, m.P < kTok ? m.P : kTok);
 }
 
+int decode_attention_ctas(const ModelDev& m) { return m.hd == 128 ? grid_t<128>() : grid_t<64>(); }
+
 void launch_decode_attention(const CUtensorMap& map, const EngineDev& e, const ModelDev& m, int layer, const bf16* q,
                              bf16* out, float* part_o, float* part_ml, int max_splits, int chunk, cudaStream_t s) {
+  (void)chunk;  // the split size of this iteration is on the device (ModelDev::att_ctl[0])
+  AB_REQUIRE(max_splits <= kMaxSplits, AB_ERR_CONFIG, "too many KV splits per row for the decode attention");
   if (m.hd == 128)
-    launch_t<128>(map, e, m, layer, q, out, part_o, part_ml, max_splits, chunk, s);
+    launch_t<128>(map, e, m, layer, q, out, part_o, part_ml, max_splits, s);
   else
-    launch_t<64>(map, e, m, layer, q, out, part_o, part_ml, max_splits, chunk, s);
+    launch_t<64>(map, e, m, layer, q, out, part_o, part_ml, max_splits, s);
 }
 
 }  // namespace ab

@@ -66,13 +66,17 @@ __device__ __forceinline__ int pop_page(Ctl* c) {
 // attention work list (exclusive prefix of KV splits per row).
 constexpr int kPrepThreads = 1024;
 
-__global__ void __launch_bounds__(kPrepThreads) k_prep_decode(EngineDev e, ModelDev m, int chunk) {
+// Per-iteration decode prologue: gather the live rows, allocate KV pages for the
+// token about to be written, and build the attention work list.  The KV split
+// size is picked here from the iteration's total context so that the work list
+// has about 4 items per attention CTA (long rows split, short rows whole; the
+// attention CTAs then pull items dynamically), never below `min_chunk` tokens.
+__global__ void __launch_bounds__(kPrepThreads) k_prep_decode(EngineDev e, ModelDev m, int min_chunk, int att_ctas) {
   Ctl* c = e.ctl;
   if (c->stop) return;
   const int b = c->b;
   const int ipt = (b + kPrepThreads - 1) / kPrepThreads;
   const int beg = min(b, (int)threadIdx.x * ipt), end = min(b, beg + ipt);
-  int nsp = 0;
   unsigned long long ctx_sum = 0;
   bool fail = false;
   for (int i = beg; i < end; ++i) {
@@ -82,7 +86,6 @@ __global__ void __launch_bounds__(kPrepThreads) k_prep_decode(EngineDev e, Model
     m.row_pos[i] = pos;
     m.row_btrow[i] = h;
     ctx_sum += (unsigned long long)(pos + 1);
-    nsp += (pos + chunk) / chunk;  // ceil((pos + 1) / chunk)
     if (pos % m.P == 0) {
       const int idx = pop_page(c);
       if (idx < 0 || pos / m.P >= m.MP) {
@@ -92,9 +95,30 @@ __global__ void __launch_bounds__(kPrepThreads) k_prep_decode(EngineDev e, Model
       }
     }
   }
-  // exclusive scan of split counts
   __shared__ int s_w[32];
+  __shared__ unsigned long long s_u[32];
+  __shared__ int s_chunk;
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  unsigned long long cs = ctx_sum;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) cs += __shfl_xor_sync(0xffffffffu, cs, o);
+  if (lane == 0) s_u[w] = cs;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    unsigned long long tot = 0;
+    for (int k = 0; k < kPrepThreads / 32; ++k) tot += s_u[k];
+    const unsigned long long per = (tot * (unsigned long long)m.hk + 4ull * att_ctas - 1) / (4ull * att_ctas);
+    int ch = (int)min(per, (unsigned long long)(1 << 30));
+    ch = (ch + 63) & ~63;
+    s_chunk = max(ch, min_chunk);
+    m.att_ctl[0] = s_chunk;
+  }
+  for (int l = threadIdx.x; l < m.L; l += kPrepThreads) m.att_ctl[1 + l] = 0;  // per-layer item cursors
+  __syncthreads();
+  const int chunk = s_chunk;
+  int nsp = 0;
+  for (int i = beg; i < end; ++i) nsp += (m.row_pos[i] + chunk) / chunk;  // ceil((pos + 1) / chunk)
+  // exclusive scan of split counts
   int x = nsp;
 #pragma unroll
   for (int o = 1; o < 32; o <<= 1) {
@@ -412,7 +436,9 @@ void launch_rope_table(float2* rope, int max_pos, int hd, float theta, cudaStrea
 }
 
 void launch_prep_decode(const EngineDev& e, const ModelDev& m, int chunk, cudaStream_t s) {
-  k_prep_decode<<<1, kPrepThreads, 0, s>>>(e, m, chunk);
+  static int att_ctas = 0;
+  if (!att_ctas) att_ctas = decode_attention_ctas(m);
+  k_prep_decode<<<1, kPrepThreads, 0, s>>>(e, m, chunk, att_ctas);
 }
 
 void launch_embed(const ModelDev& m, const bf16* emb, float* x, const int* rows_dev, int rows_cap, const int* stop,

@@ -168,7 +168,9 @@ Model* model_create(Engine& e) {
   M->attn = dalloc<bf16>(R * m.qd);
   M->hbuf = dalloc<bf16>(R * m.f);
   M->logits = dalloc<float>((size_t)M->S * m.V);
-  M->chunk = 512;  // KV tokens per attention work item (8 tiles)
+  // smallest KV split of an attention work item (the prep kernel picks the split per iteration);
+  // at most 64 splits per row
+  M->chunk = std::max(256, (ceil_div(m.max_pos, 64) + 63) / 64 * 64);
   M->max_splits = ceil_div(m.max_pos, M->chunk);
   M->part_o = dalloc<float>((size_t)M->S * m.hq * M->max_splits * m.hd);
   M->part_ml = dalloc<float>((size_t)M->S * m.hq * M->max_splits * 2);
@@ -178,6 +180,7 @@ Model* model_create(Engine& e) {
   m.split_prefix = dalloc<int32_t>(M->S + 1);
   m.att_counter = dalloc<int32_t>((size_t)M->S * m.hk);
   m.att_items = dalloc<int32_t>((size_t)M->S * M->max_splits + 1);
+  m.att_ctl = dalloc<int32_t>(1 + m.L);
   m.h_ctx = dalloc<int32_t>(m.H);
   m.h_last_tok = dalloc<int32_t>(m.H);
   m.h_shared = dalloc<int32_t>(m.H);
@@ -258,7 +261,7 @@ void model_destroy(Model* M) {
                   M->logits,   M->part_o,   M->part_ml,   m.row_tok,    m.row_pos,    m.row_btrow, m.h_ctx,
                   m.h_last_tok, m.h_shared, m.g_ctx,      m.g_last_tok, m.g_npages,   m.bt,        m.rope,
                   M->pf_rows,  M->seg_start, M->seg_group, M->ga_g,     M->ga_len,    M->ga_last,  m.kv,
-                  m.free_pages, m.split_prefix, m.att_counter};
+                  m.free_pages, m.split_prefix, m.att_counter, m.att_ctl};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   if (M->host_stage) cudaFreeHost(M->host_stage);

@@ -36,6 +36,7 @@ struct ModelDev {
   int32_t* split_prefix;  // [S+1] attention work list: exclusive prefix of KV splits per live row
   int32_t* att_counter;   // [S * hk] split-combine arrival counters (self-resetting)
   int32_t* att_items;     // [S * max_splits] work list: row | split << 16
+  int32_t* att_ctl;       // [1 + L]: KV split size of this iteration, per-layer work-list cursors
 
   __device__ __forceinline__ size_t kv_off(int l, int page, int which, int head, int slot) const {
     return ((((size_t)l * NP + page) * 2 + which) * hk + head) * (size_t)P * hd + (size_t)slot * hd;
@@ -59,6 +60,7 @@ void launch_rope_kv(const ModelDev& m, int layer, const bf16* qkv, const bf16* q
                     const int* rows_dev, int rows_cap, const int* stop, cudaStream_t s);
 // attention.cu
 void make_kv_tmap(CUtensorMap* map, const ModelDev& m);
+int decode_attention_ctas(const ModelDev& m);  // persistent grid of the decode attention kernel
 void launch_decode_attention(const CUtensorMap& map, const EngineDev& e, const ModelDev& m, int layer, const bf16* q,
                              bf16* out, float* part_o, float* part_ml, int max_splits, int chunk, cudaStream_t s);
 void launch_prefill_attention(const ModelDev& m, int layer, const bf16* q, bf16* out, const int* seg_start,
