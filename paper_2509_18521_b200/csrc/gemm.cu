@@ -92,6 +92,33 @@ __device__ __forceinline__ void umma_bf16(uint32_t tmem_d, uint64_t a, uint64_t 
       "l"(a), "l"(b), "r"(idesc), "r"(acc));
 }
 
+// cta_group::2 (CTA pair, UMMA M = 256): issued by the even CTA of the pair only.
+__device__ __forceinline__ void umma_bf16_pair(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
+  asm volatile(
+      "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n"
+      " tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, {%5, %5, %5, %5, %5, %5, %5, %5}, p;\n}" ::"r"(tmem_d),
+      "l"(a), "l"(b), "r"(idesc), "r"(acc), "r"(0u));
+}
+// commit the pair's outstanding MMAs to the barrier at the same offset in every CTA of `mask`
+__device__ __forceinline__ void umma_commit_pair(uint64_t* bar, uint16_t mask) {
+  asm volatile("tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+                   smem_u32(bar)),
+               "h"(mask)
+               : "memory");
+}
+// TMA load whose completion is counted on the pair leader's barrier (cluster address)
+__device__ __forceinline__ void tma_load_2d_pair(const CUtensorMap* map, uint32_t bar_cluster, void* dst, int x, int y,
+                                                 uint64_t policy) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], "
+      "[%1, {%3, %4}], [%2], %5;" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(bar_cluster), "r"(x), "r"(y), "l"(policy)
+      : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_cluster(uint32_t bar_cluster) {
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(bar_cluster) : "memory");
+}
+
 __device__ __forceinline__ void umma_commit(uint64_t* bar) {
   asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
                : "memory");
@@ -155,9 +182,11 @@ __device__ __forceinline__ float4 ld_dsmem_f4(uint32_t addr) {
 //   swap = 0: activation rows on the M side (an = 128), weights on the N side
 //             (wn = 128 or 256 weight rows).  TMEM lane = activation row, so
 //             the epilogue writes contiguous 16-byte vectors along a row.
-//   splits:   1, or the cluster size CS (cluster split-K, one tile per cluster).
+//   splits:   1, or a power of two <= the cluster size CS (cluster split-K: each group of
+//             `splits` consecutive ranks of a cluster reduces one tile, CS/splits tiles per
+//             cluster, one round).
 struct Sched {
-  int swap, wn, an, splits, m_tiles, n_tiles, tiles, nk, stages, stage_bytes, w_bytes;
+  int swap, pair, wn, an, splits, m_tiles, n_tiles, tiles, nk, stages, stage_bytes, w_bytes;
 };
 
 __host__ __device__ inline Sched sched_from(int code, int rows, int N, int K) {
@@ -166,14 +195,16 @@ __host__ __device__ inline Sched sched_from(int code, int rows, int N, int K) {
   const int t = 1 << ((code >> 1) & 15);
   s.splits = (code >> 5) & 31;
   s.stages = (code >> 10) & 15;
-  s.wn = s.swap ? kBM : t;
-  s.an = s.swap ? t : kBM;
+  s.pair = (code >> 14) & 1;
+  // pair: one 256 x 256 tile per CTA pair; each CTA stages 128 activation + 128 weight rows
+  s.wn = s.pair ? 256 : s.swap ? kBM : t;
+  s.an = s.pair ? 256 : s.swap ? t : kBM;
   s.n_tiles = (N + s.wn - 1) / s.wn;
   s.m_tiles = (rows + s.an - 1) / s.an;
   s.tiles = s.n_tiles * s.m_tiles;
   s.nk = K / kBK;
-  s.w_bytes = s.wn * kBK * 2;
-  s.stage_bytes = s.w_bytes + s.an * kBK * 2;
+  s.w_bytes = (s.pair ? 128 : s.wn) * kBK * 2;
+  s.stage_bytes = s.w_bytes + (s.pair ? 128 : s.an) * kBK * 2;
   return s;
 }
 
@@ -186,27 +217,38 @@ __host__ __device__ inline Sched sched_from(int code, int rows, int N, int K) {
 int choose_sched(int rows, int N, int K, int max_bn, int cs, int ncl, int force, int epi) {
   const int nk = K / kBK;
   const int grid = cs * ncl;
-  auto pack = [&](int swap, int t, int sp) {
+  auto pack = [&](int swap, int t, int sp, int pair = 0) {
     int lg = 0;
     while ((1 << lg) < t) ++lg;
-    const int wn = swap ? kBM : t, an = swap ? t : kBM;
+    const int wn = pair ? 128 : swap ? kBM : t, an = pair ? 128 : swap ? t : kBM;
     const int stages = std::min(kMaxStages, kRingBytes / (wn * kBK * 2 + an * kBK * 2));
-    return swap | (lg << 1) | (sp << 5) | (stages << 10);
+    return swap | (lg << 1) | (sp << 5) | (stages << 10) | (pair << 14);
   };
   if (force > 0 && (force & 0x40000000)) {  // a fixed code (tools/gemm_bench.py --sweep)
+    if (force & 0x4000) {  // CTA pair: a cluster of 2, no split
+      if (cs != 2 || (epi == kEpiSwiGLU && N % 256) || N % 128) return 0;
+      return pack(0, 256, 1, 1);
+    }
+    if (cs == 2) return 0;
     const int code = force & 0x3ff;
     const int swap = code & 1, t = 1 << ((code >> 1) & 15), sp = (code >> 5) & 31;
-    if (sp != 1 && sp != cs) return 0;
+    if (sp < 1 || sp > cs || (sp & (sp - 1))) return 0;
     if (!swap && N % 128) return 0;
     if (!swap && epi == kEpiSwiGLU && (t != 256 || N % 256)) return 0;
     if (sp > 1) {
       const int wn = swap ? kBM : t, an = swap ? t : kBM;
-      if ((int64_t)((N + wn - 1) / wn) * ((rows + an - 1) / an) > ncl || nk < sp) return 0;
+      if ((int64_t)((N + wn - 1) / wn) * ((rows + an - 1) / an) * sp > (int64_t)ncl * cs || nk < sp) return 0;
     }
     return pack(swap, t, sp);
   }
   int64_t best_cost = INT64_MAX;
   int best = 0;
+  if (cs == 2) {  // a pair plan: every row count runs the CTA-pair schedule
+    if (N % 128 || (epi == kEpiSwiGLU && N % 256)) return 0;
+    // CTA pair (cta_group::2, 256 x 256 tile): per CTA and K block the same 128 x 256 x 64 MMA
+    // as a 1-CTA 128 x 256 tile, but only 32 KB of operands instead of 48 KB
+    return pack(0, 256, 1, 1);
+  }
   // force > 0: swap-AB with exactly an = force; force < 0: no swap with wn = -force
   for (int mode = 0; mode < 2; ++mode) {
     const int swap = mode == 0 ? 1 : 0;
@@ -224,18 +266,18 @@ int choose_sched(int rows, int N, int K, int max_bn, int cs, int ncl, int force,
       const int64_t per_kb = mma > fill ? mma : fill;
       const int live = std::min(an, rows);
       const int64_t epi_c = swap ? (int64_t)live * (epi == kEpiSwiGLU ? 96 : 48) : (int64_t)wn * 6 + 600;
-      for (int sp : {1, cs}) {
-        if (sp > 1 && (sp == 1 || tiles > ncl || nk < 2 * sp)) continue;
+      for (int sp = 1; sp <= cs; sp <<= 1) {
+        if (sp > 1 && ((int64_t)tiles * sp > (int64_t)ncl * cs || nk < 2 * sp)) continue;
         const int64_t waves = sp > 1 ? 1 : (tiles + grid - 1) / grid;
         const int64_t main = (int64_t)((nk + sp - 1) / sp) * per_kb;
-        const int64_t split_cost = sp > 1 ? 1000 + (int64_t)(swap ? live : wn) * 26 : 0;  // DSMEM ~20 B/clk
+        // DSMEM gather ~20 B/clk: each rank pulls (sp-1)/sp of its 1/sp lane share from the others
+        const int64_t split_cost = sp > 1 ? 1000 + (int64_t)(swap ? live : wn) * 26 * (sp - 1) / sp : 0;
         const int64_t e = sp > 1 ? epi_c / sp : epi_c;
         const int64_t cost = waves * ((main > e ? main : e) + 700) + split_cost + e;
         if (cost < best_cost) {
           best_cost = cost;
           best = pack(swap, t, sp);
         }
-        if (cs == 1) break;
       }
     }
   }
@@ -248,20 +290,17 @@ int choose_sched(int rows, int N, int K, int max_bn, int cs, int ncl, int force,
 // [8] split: partial parked, [11] split: cluster barrier passed, [12] first chunk fetched.
 __device__ unsigned long long g_gemm_trace[160 * 16];
 __device__ __forceinline__ void trace_mark(int on, int k) {
-  if (on) {
+  if (on & 1) {
     unsigned long long t;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
     g_gemm_trace[blockIdx.x * 16 + k] = t;
   }
 }
 
-// Parked partial tile in the (idle) TMA ring: [chunk of 32 columns][TMEM lane][32 floats],
-// float4 index XOR-swizzled by lane so a warp's accesses are bank-conflict free.
-__device__ __forceinline__ uint32_t park_off(int chunk, int lane128, int q) {
-  return (uint32_t)(((chunk * 128 + lane128) * 8 + (q ^ (lane128 & 7))) * 16);
-}
-
-template <int EPI>
+// kPair: the CTA-pair instantiation (cluster of 2, every schedule is a pair schedule, every
+// tcgen05 allocation / MMA / commit is cta_group::2); the other one is all cta_group::1 and
+// runs the swap / no-swap / cluster split-K schedules.
+template <int EPI, bool kPair>
 __global__ void __launch_bounds__(kThreads, 1)
     k_gemm_tc(const __grid_constant__ CUtensorMap tw, const __grid_constant__ CUtensorMap ta, int N, int K,
               int M_cap, const int* __restrict__ rows_dev, const int* __restrict__ stop_dev, void* __restrict__ out,
@@ -274,12 +313,21 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (code == 0) return;
   const Sched sc = sched_from(code, rows, N, K);
   const int cs = (int)cluster_nctarank();
-  const bool split = sc.splits > 1;  // == cs: one tile per cluster, rank = K slice
-  const int rank = split ? (int)cluster_ctarank() : 0;
-  // work units: split -> tile blockIdx.x / cs (whole cluster); else tiles strided over the grid
-  const int u_first = split ? (int)blockIdx.x / cs : (int)blockIdx.x;
-  const int u_step = split ? (int)gridDim.x / cs : (int)gridDim.x;
-  if (u_first >= sc.tiles) return;  // split: uniform over the cluster
+  const bool split = sc.splits > 1;
+  constexpr bool pair = kPair;  // CTA pair (cta_group::2): even cluster rank leads
+  if (kPair != (sc.pair != 0)) return;  // the host never builds such a table
+  const int crank = (split || pair) ? (int)cluster_ctarank() : 0;
+  const int prank = pair ? (crank & 1) : 0;
+  const int rank = split ? crank % sc.splits : 0;  // K slice within the tile's rank group
+  const int grp0 = crank - rank;                   // first cluster rank of the group
+  // work units: split -> one tile per rank group (one round); pair -> tiles strided over the
+  // pairs; else tiles strided over the grid
+  const int per_cl = split ? cs / sc.splits : pair ? cs / 2 : 1;
+  const int u_first = split ? ((int)blockIdx.x / cs) * per_cl + crank / sc.splits
+                      : pair ? (int)blockIdx.x / 2 : (int)blockIdx.x;
+  const int u_step = split ? ((int)gridDim.x / cs) * per_cl : pair ? (int)gridDim.x / 2 : (int)gridDim.x;
+  if ((split || pair) ? ((int)blockIdx.x / cs) * per_cl >= sc.tiles : u_first >= sc.tiles)
+    return;  // uniform per cluster
 
   extern __shared__ uint8_t smem_raw[];
   uint8_t* ring = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -299,21 +347,29 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(&tmem_full[a], 1);
-      mbar_init(&tmem_empty[a], 4);
+      mbar_init(&tmem_empty[a], pair ? 8 : 4);  // pair: both CTAs' epilogue warps release the leader
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tw)) : "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&ta)) : "memory");
   }
   if (warp == 1) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
-                 "r"(kTmemCols));
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    if constexpr (kPair) {
+      asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                   "r"(kTmemCols));
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+    } else {
+      asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                   "r"(kTmemCols));
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
+  if (pair) cluster_sync_all();  // the peer signals the leader's barriers: inits must be visible
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   const uint32_t tmem = *tmem_slot;
+  const uint32_t leader = (uint32_t)(crank & ~1);
   if (threadIdx.x == 0) trace_mark(trace, 1);
 
   auto unit_coords = [&](int u, int& n0, int& m0, int& kb0, int& kb1) {
@@ -334,9 +390,37 @@ __global__ void __launch_bounds__(kThreads, 1)
         asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol_w));
       asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol_a));
       int g = 0;
+      const uint32_t full_lead = pair ? map_rank(smem_u32(full), leader) : 0u;
       for (int u = u_first; u < sc.tiles; u += u_step) {
         int n0, m0, kb0, kb1;
         unit_coords(u, n0, m0, kb0, kb1);
+        if (pair) {
+          // each CTA of the pair stages its 128 activation rows and its 128 weight rows; the
+          // leader's full barrier counts both CTAs' bytes
+          auto boxes = [&](int p, int& nb, int& wb) {
+            nb = max(0, min(4, (rows - (m0 + 128 * p) + 31) >> 5));
+            wb = N - (n0 + 128 * p) > 0 ? 1 : 0;
+          };
+          int nb_me, wb_me, nb0, wb0, nb1, wb1;
+          boxes(prank, nb_me, wb_me);
+          boxes(0, nb0, wb0);
+          boxes(1, nb1, wb1);
+          const uint32_t tx = (uint32_t)((wb0 + wb1) * kWBytes + (nb0 + nb1) * 32 * kBK * 2);
+          for (int kb = kb0; kb < kb1; ++kb, ++g) {
+            const int s = g % nst;
+            mbar_wait(&empty[s], ((g / nst) & 1) ^ 1);
+            uint8_t* st = ring + s * sc.stage_bytes;
+            if (prank == 0) mbar_expect_tx(&full[s], tx);
+            if constexpr (kPair) {
+              const uint32_t fb = full_lead + s * 8;
+              if (wb_me) tma_load_2d_pair(&tw, fb, st, kb * kBK, n0 + 128 * prank, pol_w);
+              for (int j = 0; j < nb_me; ++j)
+                tma_load_2d_pair(&ta, fb, st + sc.w_bytes + j * 32 * kBK * 2, kb * kBK, m0 + 128 * prank + 32 * j,
+                                 pol_a);
+            }
+          }
+          continue;
+        }
         const int nbox = (min(sc.an, rows - m0) + 31) >> 5;  // skip activation boxes past the live rows
         const int wbox = (min(sc.wn, N - n0) + 127) >> 7;    // skip weight boxes past N
         for (int kb = kb0; kb < kb1; ++kb, ++g) {
@@ -344,16 +428,55 @@ __global__ void __launch_bounds__(kThreads, 1)
           const uint32_t ph = (g / nst) & 1;
           mbar_wait(&empty[s], ph ^ 1);
           uint8_t* st = ring + s * sc.stage_bytes;
+          if (trace & 4) {  // debug: MMA-only timing (no operand loads)
+            mbar_arrive(&full[s]);
+            continue;
+          }
           mbar_expect_tx(&full[s], wbox * kWBytes + nbox * 32 * kBK * 2);
-          for (int j = 0; j < wbox; ++j)
-            tma_load_2d(&tw, &full[s], st + j * kWBytes, kb * kBK, n0 + 128 * j, pol_w);
-          for (int j = 0; j < nbox; ++j)
-            tma_load_2d(&ta, &full[s], st + sc.w_bytes + j * 32 * kBK * 2, kb * kBK, m0 + 32 * j, pol_a);
+          if constexpr (!kPair) {
+            for (int j = 0; j < wbox; ++j)
+              tma_load_2d(&tw, &full[s], st + j * kWBytes, kb * kBK, n0 + 128 * j, pol_w);
+            for (int j = 0; j < nbox; ++j)
+              tma_load_2d(&ta, &full[s], st + sc.w_bytes + j * 32 * kBK * 2, kb * kBK, m0 + 32 * j, pol_a);
+          }
           if (g == 0) trace_mark(trace, 2);
         }
       }
     }
   } else if (warp == 1) {
+    if constexpr (kPair) {
+    if (lane == 0 && pair && prank == 0) {
+      // pair leader: M = 256 (128 rows per CTA), N = 256 (128 weight rows per CTA)
+      const uint32_t idesc =
+          (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(256 >> 3) << 17) | ((uint32_t)(256 >> 4) << 24);
+      const uint16_t mask = (uint16_t)(3u << leader);
+      const uint32_t ring_s = smem_u32(ring);
+      int g = 0, t = 0;
+      for (int u = u_first; u < sc.tiles; u += u_step, ++t) {
+        int n0, m0, kb0, kb1;
+        unit_coords(u, n0, m0, kb0, kb1);
+        const int acc = t & 1;
+        mbar_wait(&tmem_empty[acc], ((t >> 1) & 1) ^ 1);
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        const uint32_t d = tmem + (uint32_t)(acc * kMaxBN);
+        for (int kb = kb0; kb < kb1; ++kb, ++g) {
+          const int s = g % nst;
+          mbar_wait(&full[s], (g / nst) & 1);
+          asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+          const uint32_t sw = ring_s + s * sc.stage_bytes, sa = sw + sc.w_bytes;
+          const uint64_t da = umma_desc(sa), db = umma_desc(sw);
+          if (!(trace & 2)) {
+#pragma unroll
+            for (int k = 0; k < kBK / 16; ++k)
+              umma_bf16_pair(d, da + 2 * k, db + 2 * k, idesc, (kb != kb0 || k != 0) ? 1u : 0u);
+          }
+          umma_commit_pair(&empty[s], mask);
+        }
+        umma_commit_pair(&tmem_full[acc], mask);
+      }
+    }
+    }
+    if constexpr (!kPair) {
     if (lane == 0) {
       const int um = sc.swap ? kBM : sc.an, un = sc.swap ? sc.an : sc.wn;
       const uint32_t idesc =
@@ -374,14 +497,17 @@ __global__ void __launch_bounds__(kThreads, 1)
           if (g == 0) trace_mark(trace, 3);
           const uint32_t sw = ring_s + s * sc.stage_bytes, sa = sw + sc.w_bytes;
           const uint64_t da = umma_desc(sc.swap ? sw : sa), db = umma_desc(sc.swap ? sa : sw);
+          if (!(trace & 2)) {  // debug bit 2: fill-only timing (no MMAs)
 #pragma unroll
-          for (int k = 0; k < kBK / 16; ++k)  // +32 bytes along K inside the swizzle atom
-            umma_bf16(d, da + 2 * k, db + 2 * k, idesc, (kb != kb0 || k != 0) ? 1u : 0u);
+            for (int k = 0; k < kBK / 16; ++k)  // +32 bytes along K inside the swizzle atom
+              umma_bf16(d, da + 2 * k, db + 2 * k, idesc, (kb != kb0 || k != 0) ? 1u : 0u);
+          }
           umma_commit(&empty[s]);
         }
         umma_commit(&tmem_full[acc]);
       }
       trace_mark(trace, 4);
+    }
     }
   } else {
     // epilogue warps 2..5 -> TMEM lane quadrants 2,3,0,1
@@ -414,16 +540,16 @@ __global__ void __launch_bounds__(kThreads, 1)
       if (threadIdx.x == 64) trace_mark(trace, 11);
       uint32_t rbase[8];
 #pragma unroll
-      for (int r = 0; r < 8; ++r) rbase[r] = map_rank(ring_s, (uint32_t)(r < cs ? r : 0));
+      for (int r = 0; r < 8; ++r) rbase[r] = map_rank(ring_s, (uint32_t)(grp0 + (r < sc.splits ? r : 0)));
       auto gather = [&](uint32_t off) {
         float4 x[8];
 #pragma unroll
         for (int r = 0; r < 8; ++r)
-          if (r < cs) x[r] = ld_dsmem_f4(rbase[r] + off);
+          if (r < sc.splits) x[r] = ld_dsmem_f4(rbase[r] + off);
         float4 a = x[0];
 #pragma unroll
         for (int r = 1; r < 8; ++r)
-          if (r < cs) {
+          if (r < sc.splits) {
             a.x += x[r].x;
             a.y += x[r].y;
             a.z += x[r].z;
@@ -434,7 +560,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int nc4 = (ncols + 3) >> 2;
       if (sc.swap) {
         const int lanes = EPI == kEpiSwiGLU ? 64 : 128;
-        const int nl = lanes / cs, L0 = rank * nl;
+        const int nl = lanes / sc.splits, L0 = rank * nl;
         for (int i = te; i < nl * nc4; i += 128) {
           const int ln = L0 + i % nl, c4 = i / nl;
           const float4 a = gather((uint32_t)((c4 * 128 + ln) * 16));
@@ -468,7 +594,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
         }
       } else {
-        const int nl = 128 / cs, L0 = rank * nl;
+        const int nl = 128 / sc.splits, L0 = rank * nl;
         const int per = EPI == kEpiSwiGLU ? nc4 / 2 : nc4;  // SwiGLU: gate column groups only
         for (int i = te; i < nl * per; i += 128) {
           const int ln = L0 + i / per, k = i % per;
@@ -517,14 +643,21 @@ __global__ void __launch_bounds__(kThreads, 1)
     for (int u = u_first; u < sc.tiles; u += u_step, ++t) {
       int n0, m0, kb0, kb1;
       unit_coords(u, n0, m0, kb0, kb1);
+      if (pair) m0 += 128 * prank;  // this CTA's TMEM holds rows [m0, m0 + 128) of the pair's tile
       const int acc = t & 1;
       mbar_wait(&tmem_full[acc], (t >> 1) & 1);
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
       if (t == 0 && threadIdx.x == 64) trace_mark(trace, 5);
       const uint32_t taddr = tmem + ((uint32_t)(quad * 32) << 16) + (uint32_t)(acc * kMaxBN);
       // columns of the accumulator that carry data: live activation rows (swap) or weight rows
-      const int ncols = sc.swap ? min(sc.an, rows - m0) : min(sc.wn, N - n0);
-      if (split) {
+      const int ncols = (trace & 8) ? 0 : sc.swap ? min(sc.an, rows - m0) : min(sc.wn, N - n0);  // 8: no epilogue
+      if (pair && m0 >= rows) {  // the peer half of the pair's last row tile can be empty
+        asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+        __syncwarp();
+        if (lane == 0) mbar_arrive_cluster(map_rank(smem_u32(&tmem_empty[acc]), leader));
+        continue;
+      }
+      if (!kPair && split) {
         split_epilogue(taddr, lrow, ncols, n0, m0);
         __syncwarp();
         if (lane == 0) mbar_arrive(&tmem_empty[acc]);
@@ -657,7 +790,16 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
       asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
       __syncwarp();
-      if (lane == 0) mbar_arrive(&tmem_empty[acc]);
+      if (lane == 0) {
+        if (pair)
+          mbar_arrive_cluster(map_rank(smem_u32(&tmem_empty[acc]), leader));
+        else
+          mbar_arrive(&tmem_empty[acc]);
+      }
+    }
+    if (split && u_first >= sc.tiles) {  // idle rank group of a working cluster
+      cluster_sync_all();
+      cluster_sync_all();
     }
   }
   if (split && warp < 2) {
@@ -669,8 +811,14 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (threadIdx.x == 64) trace_mark(trace, 6);
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
+  if (pair) cluster_sync_all();  // both CTAs of the pair are done with the pair's TMEM
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-  if (warp == 1) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(kTmemCols));
+  if (warp == 1) {
+    if constexpr (kPair)
+      asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(kTmemCols));
+    else
+      asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(kTmemCols));
+  }
   if (threadIdx.x == 0) trace_mark(trace, 7);
 }
 
@@ -718,8 +866,10 @@ template <int EPI>
 void set_attr() {
   static bool done = false;
   if (!done) {
-    AB_CUDA(cudaFuncSetAttribute(k_gemm_tc<EPI>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem));
-    AB_CUDA(cudaFuncSetAttribute(k_gemm_tc<EPI>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+    AB_CUDA(cudaFuncSetAttribute(k_gemm_tc<EPI, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem));
+    AB_CUDA(cudaFuncSetAttribute(k_gemm_tc<EPI, false>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+    AB_CUDA(cudaFuncSetAttribute(k_gemm_tc<EPI, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem));
+    AB_CUDA(cudaFuncSetAttribute(k_gemm_tc<EPI, true>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
     done = true;
   }
 }
@@ -749,7 +899,10 @@ int max_clusters(int cs) {
     at[0].val.clusterDim.z = 1;
     cfg.attrs = at;
     cfg.numAttrs = 1;
-    AB_CUDA(cudaOccupancyMaxActiveClusters(&n, k_gemm_tc<EPI>, &cfg));
+    if (cs == 2)
+      AB_CUDA(cudaOccupancyMaxActiveClusters(&n, k_gemm_tc<EPI, true>, &cfg));
+    else
+      AB_CUDA(cudaOccupancyMaxActiveClusters(&n, k_gemm_tc<EPI, false>, &cfg));
     AB_REQUIRE(n >= 1, AB_ERR_CONFIG, "GEMM cluster size does not fit on this device");
   }
   memo[cs] = n;
@@ -780,8 +933,12 @@ void launch_t(const GemmPlan& p, cudaStream_t s) {
   at[0].val.clusterDim.z = 1;
   cfg.attrs = at;
   cfg.numAttrs = 1;
-  AB_CUDA(cudaLaunchKernelEx(&cfg, k_gemm_tc<EPI>, p.tw, p.ta, p.N, p.K, p.M_cap, p.rows_dev, p.stop_dev, p.out,
-                             p.ldo, p.bias, p.sched, g_trace_on));
+  if (p.cluster == 2)
+    AB_CUDA(cudaLaunchKernelEx(&cfg, k_gemm_tc<EPI, true>, p.tw, p.ta, p.N, p.K, p.M_cap, p.rows_dev, p.stop_dev,
+                               p.out, p.ldo, p.bias, p.sched, g_trace_on));
+  else
+    AB_CUDA(cudaLaunchKernelEx(&cfg, k_gemm_tc<EPI, false>, p.tw, p.ta, p.N, p.K, p.M_cap, p.rows_dev, p.stop_dev,
+                               p.out, p.ldo, p.bias, p.sched, g_trace_on));
 }
 
 }  // namespace
@@ -871,7 +1028,7 @@ extern "C" int ab_debug_gemm_time(const void* W, const void* A, void* out, const
     // epi bit 4: cluster split-K allowed (cluster of 8); bit 5: automatic schedule (BN = max activation
     // tile); bit 6: forced no-swap schedule with BN weight rows; bit 7: BN is a fixed schedule code;
     // else forced swap-AB with BN activation rows
-    const int max_splits = (epi & 16) ? 8 : 1;
+    const int max_splits = (epi & 256) ? 2 : (epi & 16) ? 8 : 1;  // bit 8: a CTA-pair plan (cluster of 2)
     const int force = (epi & 128) ? (0x40000000 | BN) : (epi & 32) ? 0 : (epi & 64) ? -BN : BN;
     epi &= 15;
     if (!flush) AB_CUDA(cudaMalloc(&flush, size_t(256) << 20));
@@ -911,7 +1068,7 @@ extern "C" int ab_debug_gemm(const void* W, const void* A, void* out, const void
     // epi bit 4: cluster split-K allowed (cluster of 8); bit 5: automatic schedule (BN = max activation
     // tile); bit 6: forced no-swap schedule with BN weight rows; bit 7: BN is a fixed schedule code;
     // else forced swap-AB with BN activation rows
-    const int max_splits = (epi & 16) ? 8 : 1;
+    const int max_splits = (epi & 256) ? 2 : (epi & 16) ? 8 : 1;  // bit 8: a CTA-pair plan (cluster of 2)
     const int force = (epi & 128) ? (0x40000000 | BN) : (epi & 32) ? 0 : (epi & 64) ? -BN : BN;
     epi &= 15;
     ab::GemmPlan p;
@@ -928,8 +1085,9 @@ extern "C" int ab_debug_gemm(const void* W, const void* A, void* out, const void
   }
 }
 
-// Debug: run the next ab_debug_gemm with the per-CTA timeline enabled and copy
-// it out ([160][8] ns timestamps, 0 = not reached).
+// Debug: run the next GEMMs with the per-CTA timeline enabled (on & 1) and copy it out
+// ([160][16] ns timestamps, 0 = not reached); on & 2: skip the MMAs (operand fill only),
+// on & 4: skip the operand loads (MMA only).
 extern "C" int ab_debug_gemm_trace(int on, unsigned long long* out) {
   try {
     if (on) {

@@ -234,7 +234,7 @@ Model* model_create(Engine& e) {
               8);
     gemm_plan(d.o, w.wo, m.d, m.qd, M->attn, M->S, m.qd, bn_dec, kEpiAddF32, M->x, m.d, nullptr, b, stop, 8);
     gemm_plan(d.gu, w.wgu, 2 * m.f, m.d, M->xn, M->S, m.d, bn_dec, kEpiSwiGLU, M->hbuf, m.f, nullptr, b, stop,
-              4);
+              2);
     gemm_plan(d.down, w.wd, m.d, m.f, M->hbuf, M->S, m.f, bn_dec, kEpiAddF32, M->x, m.d, nullptr, b, stop, 8);
     gemm_plan(p.qkv, w.wqkv, m.qkv_dim, m.d, M->xn, M->M_pf, m.d, 256, kEpiBF16, M->qkv, m.qkv_dim, w.bqkv,
               M->pf_rows, nullptr);
@@ -247,7 +247,7 @@ Model* model_create(Engine& e) {
     M->dec.push_back(d);
     M->pf.push_back(p);
   }
-  gemm_plan(M->lm_dec, M->lm_head, m.V, m.d, M->xn, M->S, m.d, bn_dec, kEpiF32, M->logits, m.V, nullptr, b, stop);
+  gemm_plan(M->lm_dec, M->lm_head, m.V, m.d, M->xn, M->S, m.d, bn_dec, kEpiF32, M->logits, m.V, nullptr, b, stop, 2);
   M->inv_temp = ec.greedy ? 1.f / std::max(ec.temperature, 1e-6f) : 1.f / ec.temperature;
   if (ec.temperature <= 0.f) M->inv_temp = 1.f;
   AB_CUDA(cudaStreamSynchronize(s));

@@ -66,7 +66,7 @@ def test_tcgen05_gemm_swiglu_epilogue(epi):
 @pytest.mark.parametrize("rows", [1, 17, 64, 200, 333, 1024])
 @pytest.mark.parametrize("shape_epi", [((1536, 1536), 2), ((2048, 1536), 0), ((512, 1024), 3), ((1536, 8960), 2),
                                        ((384, 640), 1)])
-@pytest.mark.parametrize("split", [0, 16])
+@pytest.mark.parametrize("split", [0, 16, 256])  # 16: cluster split-K plan, 256: CTA-pair plan
 def test_tcgen05_gemm_auto_schedule(rows, shape_epi, split):
     """The decode configuration: tile width and split-K picked on the device from the row count."""
     (N, K), epi = shape_epi
@@ -92,6 +92,41 @@ def test_tcgen05_gemm_auto_schedule(rows, shape_epi, split):
         out = base.clone()
         ref = acc + base
     _capi.call("ab_debug_gemm", _ptr(W), _ptr(A), _ptr(out), _ptr(bias), N, K, M, 256, epi + split + 32)
+    torch.cuda.synchronize()
+    tol = 2e-2 if epi in (0, 3) else 2e-3
+    torch.testing.assert_close(out.float(), ref, rtol=tol, atol=tol * max(1.0, ref.abs().max().item() * 0.01))
+
+
+@pytest.mark.parametrize("shape", [(256, 128, 1), (512, 1536, 37), (2048, 1536, 300), (384, 256, 1000),
+                                   (1536, 8960, 600)])
+@pytest.mark.parametrize("epi", [0, 1, 2, 3])
+def test_tcgen05_gemm_cta_pair(shape, epi):
+    """The CTA-pair schedule (cta_group::2, 256 x 256 tile split over two SMs), forced."""
+    N, K, M = shape
+    if epi == 3 and N % 256:
+        pytest.skip("SwiGLU pair tiles need N % 256 == 0")
+    g = torch.Generator(device="cuda").manual_seed(N + 3 * K + M)
+    W = (torch.randn(N, K, device="cuda", generator=g) * 0.05).to(torch.bfloat16)
+    A = torch.randn(M, K, device="cuda", generator=g).to(torch.bfloat16)
+    acc = A.float() @ W.float().t()
+    bias = None
+    if epi == 3:
+        out = torch.empty(M, N // 2, device="cuda", dtype=torch.bfloat16)
+        t = acc.view(M, N // 128, 2, 64)
+        ref = (torch.nn.functional.silu(t[:, :, 0]) * t[:, :, 1]).reshape(M, N // 2)
+    elif epi == 0:
+        bias = (torch.randn(N, device="cuda", generator=g) * 0.1).to(torch.bfloat16)
+        out = torch.empty(M, N, device="cuda", dtype=torch.bfloat16)
+        ref = acc + bias.float()
+    elif epi == 1:
+        out = torch.empty(M, N, device="cuda", dtype=torch.float32)
+        ref = acc
+    else:
+        base = torch.randn(M, N, device="cuda", generator=g)
+        out = base.clone()
+        ref = acc + base
+    # bit 8: cluster of 2 (a pair plan), bit 7: fixed schedule code; 0x4000 = CTA pair
+    _capi.call("ab_debug_gemm", _ptr(W), _ptr(A), _ptr(out), _ptr(bias), N, K, M, 0x4000, epi + 256 + 128)
     torch.cuda.synchronize()
     tol = 2e-2 if epi in (0, 3) else 2e-3
     torch.testing.assert_close(out.float(), ref, rtol=tol, atol=tol * max(1.0, ref.abs().max().item() * 0.01))

@@ -73,15 +73,19 @@ def sweep(args):
                 for t in ((32, 64, 128, 256) if swap else (128, 256)):
                     if not swap and (N % 128 or (epi == 3 and (t != 256 or N % 256))):
                         continue
-                    for sp in (1, 8):  # split-K = the debug cluster size (8)
+                    for sp in (1, 2, 4, 8):  # split-K <= the debug cluster size (8)
                         if K // 64 < 2 * sp:
                             continue
                         lg = t.bit_length() - 1
                         code = swap | (lg << 1) | (sp << 5)
                         r = run(N, K, M, epi | 16 | 128, code, args.reps, False, cublas=False)
                         res.append((r["us"], swap, t, sp))
+            r = run(N, K, M, epi | 256 | 128, 0x4000, args.reps, False, cublas=False)  # CTA pair
+            res.append((r["us"], 2, 256, 1))  # swap column 2 = CTA pair
             auto = run(N, K, M, epi, 0, args.reps, True)
             res.sort()
+            floor = min(r[0] for r in res)  # invalid codes launch an empty kernel: drop them
+            res = [r for r in res if r[0] > floor + 0.5] or res
             print(json.dumps({"shape": name, "M": M, "auto_us": auto["us"], "cublas_us": auto["cublas_us"],
                               "best": res[:4]}), flush=True)
 
@@ -93,7 +97,10 @@ def main():
     ap.add_argument("--bn", type=int, nargs="+", default=[0], help="activation tile width; 0 = automatic (as the decode path)")
     ap.add_argument("--split", type=int, default=1)
     ap.add_argument("--sweep", action="store_true")
+    ap.add_argument("--mode", type=int, default=0, help="2: operand fill only, 4: MMA only (debug timing)")
     args = ap.parse_args()
+    if args.mode:
+        _capi.call("ab_debug_gemm_trace", args.mode, None)
     if args.sweep:
         return sweep(args)
     res = []
