@@ -204,9 +204,69 @@ __global__ void k_rmsnorm(const float* __restrict__ x, const bf16* __restrict__ 
   }
 }
 
+// One warp per row, the whole row in registers (NV float4 per lane, d = 128 * NV): one
+// coalesced read of x, 8-byte bf16 stores.  Same arithmetic as k_rmsnorm (fp32 sum of
+// squares in the same per-lane order, warp_sum, x * rs * w rounded once to bf16).
+template <int NV>
+__global__ void __launch_bounds__(256) k_rmsnorm_v(const float* __restrict__ x, const bf16* __restrict__ w,
+                                                   bf16* __restrict__ out, float eps, const int* rows_dev,
+                                                   int rows_cap, const int* stop) {
+  if (stopped(stop)) return;
+  const int rows = rows_dev ? min(*rows_dev, rows_cap) : rows_cap;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int r = blockIdx.x * (blockDim.x >> 5) + warp;
+  if (r >= rows) return;
+  constexpr int D = NV * 128;
+  const float4* xr = reinterpret_cast<const float4*>(x + (size_t)r * D);
+  float4 v[NV];
+#pragma unroll
+  for (int i = 0; i < NV; ++i) v[i] = xr[i * 32 + lane];
+  float ss = 0.f;
+#pragma unroll
+  for (int i = 0; i < NV; ++i) ss += v[i].x * v[i].x + v[i].y * v[i].y + v[i].z * v[i].z + v[i].w * v[i].w;
+  ss = warp_sum(ss);
+  const float rs = rsqrtf(ss / (float)D + eps);
+  const uint2* wv = reinterpret_cast<const uint2*>(w);
+  uint2* o = reinterpret_cast<uint2*>(out + (size_t)r * D);
+#pragma unroll
+  for (int i = 0; i < NV; ++i) {
+    const uint2 ww = __ldg(wv + i * 32 + lane);
+    const __nv_bfloat162 w01 = *reinterpret_cast<const __nv_bfloat162*>(&ww.x);
+    const __nv_bfloat162 w23 = *reinterpret_cast<const __nv_bfloat162*>(&ww.y);
+    const __nv_bfloat162 o01 = __floats2bfloat162_rn(v[i].x * rs * __low2float(w01), v[i].y * rs * __high2float(w01));
+    const __nv_bfloat162 o23 = __floats2bfloat162_rn(v[i].z * rs * __low2float(w23), v[i].w * rs * __high2float(w23));
+    uint2 ov;
+    ov.x = *reinterpret_cast<const uint32_t*>(&o01);
+    ov.y = *reinterpret_cast<const uint32_t*>(&o23);
+    o[i * 32 + lane] = ov;
+  }
+}
+
 // ---------------------------------------------------------------------------
 // q/k-norm + RoPE (rotate-half) + KV write into the row's page
 // ---------------------------------------------------------------------------
+
+// NP consecutive bf16 <-> fp32 (NP = 2: one 4-byte access)
+template <int NP>
+__device__ __forceinline__ void load_pairs(const bf16* p, float (&v)[NP]) {
+  if constexpr (NP == 2) {
+    const __nv_bfloat162 t = *reinterpret_cast<const __nv_bfloat162*>(p);
+    v[0] = __low2float(t);
+    v[1] = __high2float(t);
+  } else {
+#pragma unroll
+    for (int j = 0; j < NP; ++j) v[j] = __bfloat162float(p[j]);
+  }
+}
+template <int NP>
+__device__ __forceinline__ void store_pairs(bf16* p, const float (&v)[NP]) {
+  if constexpr (NP == 2) {
+    *reinterpret_cast<__nv_bfloat162*>(p) = __floats2bfloat162_rn(v[0], v[1]);
+  } else {
+#pragma unroll
+    for (int j = 0; j < NP; ++j) p[j] = __float2bfloat16(v[j]);
+  }
+}
 
 template <int HD>
 __global__ void k_rope_kv(ModelDev m, int layer, const bf16* __restrict__ qkv, const bf16* __restrict__ qn,
@@ -225,19 +285,13 @@ __global__ void k_rope_kv(ModelDev m, int layer, const bf16* __restrict__ qkv, c
   for (int head = warp; head < m.hq + 2 * m.hk; head += nw) {
     const bf16* hv = src + head * HD;
     float a[NP], b[NP];
-#pragma unroll
-    for (int j = 0; j < NP; ++j) {
-      a[j] = __bfloat162float(hv[lane * NP + j]);
-      b[j] = __bfloat162float(hv[lane * NP + j + HD / 2]);
-    }
+    load_pairs<NP>(hv + lane * NP, a);
+    load_pairs<NP>(hv + lane * NP + HD / 2, b);
     if (head >= m.hq + m.hk) {  // V: straight into the page
       const int kvh = head - m.hq - m.hk;
       bf16* dst = m.kv + m.kv_off(layer, page, 1, kvh, slot);
-#pragma unroll
-      for (int j = 0; j < NP; ++j) {
-        dst[lane * NP + j] = __float2bfloat16(a[j]);
-        dst[lane * NP + j + HD / 2] = __float2bfloat16(b[j]);
-      }
+      store_pairs<NP>(dst + lane * NP, a);
+      store_pairs<NP>(dst + lane * NP + HD / 2, b);
       continue;
     }
     const bool is_q = head < m.hq;
@@ -248,10 +302,13 @@ __global__ void k_rope_kv(ModelDev m, int layer, const bf16* __restrict__ qkv, c
       ss = warp_sum(ss);
       const float rs = rsqrtf(ss / (float)HD + m.eps);
       const bf16* nw_ = is_q ? qn : kn;
+      float wa[NP], wb[NP];
+      load_pairs<NP>(nw_ + lane * NP, wa);
+      load_pairs<NP>(nw_ + lane * NP + HD / 2, wb);
 #pragma unroll
       for (int j = 0; j < NP; ++j) {
-        a[j] = __bfloat162float(__float2bfloat16(a[j] * rs * __bfloat162float(nw_[lane * NP + j])));
-        b[j] = __bfloat162float(__float2bfloat16(b[j] * rs * __bfloat162float(nw_[lane * NP + j + HD / 2])));
+        a[j] = __bfloat162float(__float2bfloat16(a[j] * rs * wa[j]));
+        b[j] = __bfloat162float(__float2bfloat16(b[j] * rs * wb[j]));
       }
     }
     float oa[NP], ob[NP];
@@ -262,11 +319,8 @@ __global__ void k_rope_kv(ModelDev m, int layer, const bf16* __restrict__ qkv, c
       ob[j] = b[j] * cs.x + a[j] * cs.y;
     }
     bf16* dst = is_q ? qout + (size_t)r * m.qd + head * HD : m.kv + m.kv_off(layer, page, 0, head - m.hq, slot);
-#pragma unroll
-    for (int j = 0; j < NP; ++j) {
-      dst[lane * NP + j] = __float2bfloat16(oa[j]);
-      dst[lane * NP + j + HD / 2] = __float2bfloat16(ob[j]);
-    }
+    store_pairs<NP>(dst + lane * NP, oa);
+    store_pairs<NP>(dst + lane * NP + HD / 2, ob);
   }
 }
 
@@ -448,7 +502,19 @@ void launch_embed(const ModelDev& m, const bf16* emb, float* x, const int* rows_
 
 void launch_rmsnorm(const float* x, const bf16* w, bf16* out, int d, float eps, const int* rows_dev, int rows_cap,
                     const int* stop, cudaStream_t s) {
-  k_rmsnorm<<<ceil_div(rows_cap, 8), 256, 0, s>>>(x, w, out, d, eps, rows_dev, rows_cap, stop);
+  const dim3 g(ceil_div(rows_cap, 8)), t(256);
+  switch (d % 128 ? 0 : d / 128) {
+    case 2: k_rmsnorm_v<2><<<g, t, 0, s>>>(x, w, out, eps, rows_dev, rows_cap, stop); break;
+    case 4: k_rmsnorm_v<4><<<g, t, 0, s>>>(x, w, out, eps, rows_dev, rows_cap, stop); break;
+    case 8: k_rmsnorm_v<8><<<g, t, 0, s>>>(x, w, out, eps, rows_dev, rows_cap, stop); break;
+    case 12: k_rmsnorm_v<12><<<g, t, 0, s>>>(x, w, out, eps, rows_dev, rows_cap, stop); break;
+    case 16: k_rmsnorm_v<16><<<g, t, 0, s>>>(x, w, out, eps, rows_dev, rows_cap, stop); break;
+    case 20: k_rmsnorm_v<20><<<g, t, 0, s>>>(x, w, out, eps, rows_dev, rows_cap, stop); break;
+    case 24: k_rmsnorm_v<24><<<g, t, 0, s>>>(x, w, out, eps, rows_dev, rows_cap, stop); break;
+    case 28: k_rmsnorm_v<28><<<g, t, 0, s>>>(x, w, out, eps, rows_dev, rows_cap, stop); break;
+    case 32: k_rmsnorm_v<32><<<g, t, 0, s>>>(x, w, out, eps, rows_dev, rows_cap, stop); break;
+    default: k_rmsnorm<<<g, t, 0, s>>>(x, w, out, d, eps, rows_dev, rows_cap, stop); break;
+  }
 }
 
 void launch_rope_kv(const ModelDev& m, int layer, const bf16* qkv, const bf16* q_norm, const bf16* k_norm, bf16* q_out,
