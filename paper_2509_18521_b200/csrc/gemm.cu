@@ -107,12 +107,12 @@ __device__ __forceinline__ void umma_commit_pair(uint64_t* bar, uint16_t mask) {
                : "memory");
 }
 // TMA load whose completion is counted on the pair leader's barrier (cluster address)
-__device__ __forceinline__ void tma_load_2d_pair(const CUtensorMap* map, uint32_t bar_cluster, void* dst, int x, int y,
-                                                 uint64_t policy) {
+__device__ __forceinline__ void tma_load_3d_pair(const CUtensorMap* map, uint32_t bar_cluster, void* dst, int x, int y,
+                                                 int z, uint64_t policy) {
   asm volatile(
-      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], "
-      "[%1, {%3, %4}], [%2], %5;" ::"r"(smem_u32(dst)),
-      "l"(reinterpret_cast<uint64_t>(map)), "r"(bar_cluster), "r"(x), "r"(y), "l"(policy)
+      "cp.async.bulk.tensor.3d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], "
+      "[%1, {%3, %4, %5}], [%2], %6;" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(bar_cluster), "r"(x), "r"(y), "r"(z), "l"(policy)
       : "memory");
 }
 __device__ __forceinline__ void mbar_arrive_cluster(uint32_t bar_cluster) {
@@ -203,8 +203,8 @@ __host__ __device__ inline Sched sched_from(int code, int rows, int N, int K) {
   s.m_tiles = (rows + s.an - 1) / s.an;
   s.tiles = s.n_tiles * s.m_tiles;
   s.nk = K / kBK;
-  s.w_bytes = (s.pair ? 128 : s.wn) * kBK * 2;
-  s.stage_bytes = s.w_bytes + (s.pair ? 128 : s.an) * kBK * 2;
+  s.w_bytes = (s.pair ? 128 : s.wn) * kBK * 2;  // pair: per k-block slab (a stage holds two)
+  s.stage_bytes = s.pair ? 4 * kWBytes : s.w_bytes + s.an * kBK * 2;
   return s;
 }
 
@@ -221,12 +221,13 @@ int choose_sched(int rows, int N, int K, int max_bn, int cs, int ncl, int force,
     int lg = 0;
     while ((1 << lg) < t) ++lg;
     const int wn = pair ? 128 : swap ? kBM : t, an = pair ? 128 : swap ? t : kBM;
-    const int stages = std::min(kMaxStages, kRingBytes / (wn * kBK * 2 + an * kBK * 2));
+    // pair stages carry two 64-deep k-blocks (one 32 KB 3-D TMA box per operand)
+    const int stages = std::min(kMaxStages, kRingBytes / ((wn * kBK * 2 + an * kBK * 2) * (pair ? 2 : 1)));
     return swap | (lg << 1) | (sp << 5) | (stages << 10) | (pair << 14);
   };
   if (force > 0 && (force & 0x40000000)) {  // a fixed code (tools/gemm_bench.py --sweep)
     if (force & 0x4000) {  // CTA pair: a cluster of 2, no split
-      if (cs != 2 || (epi == kEpiSwiGLU && N % 256) || N % 128) return 0;
+      if (cs != 2 || (epi == kEpiSwiGLU && N % 256) || N % 128 || nk % 2) return 0;
       return pack(0, 256, 1, 1);
     }
     if (cs == 2) return 0;
@@ -244,7 +245,7 @@ int choose_sched(int rows, int N, int K, int max_bn, int cs, int ncl, int force,
   int64_t best_cost = INT64_MAX;
   int best = 0;
   if (cs == 2) {  // a pair plan: every row count runs the CTA-pair schedule
-    if (N % 128 || (epi == kEpiSwiGLU && N % 256)) return 0;
+    if (N % 128 || (epi == kEpiSwiGLU && N % 256) || nk % 2) return 0;
     // CTA pair (cta_group::2, 256 x 256 tile): per CTA and K block the same 128 x 256 x 64 MMA
     // as a 1-CTA 128 x 256 tile, but only 32 KB of operands instead of 48 KB
     return pack(0, 256, 1, 1);
@@ -302,7 +303,9 @@ __device__ __forceinline__ void trace_mark(int on, int k) {
 // runs the swap / no-swap / cluster split-K schedules.
 template <int EPI, bool kPair>
 __global__ void __launch_bounds__(kThreads, 1)
-    k_gemm_tc(const __grid_constant__ CUtensorMap tw, const __grid_constant__ CUtensorMap ta, int N, int K,
+    k_gemm_tc(const __grid_constant__ CUtensorMap tw, const __grid_constant__ CUtensorMap ta,
+              const __grid_constant__ CUtensorMap ta128, const __grid_constant__ CUtensorMap tw3,
+              const __grid_constant__ CUtensorMap ta3, int N, int K,
               int M_cap, const int* __restrict__ rows_dev, const int* __restrict__ stop_dev, void* __restrict__ out,
               int64_t ldo, const __nv_bfloat16* __restrict__ bias, const int* __restrict__ sched_tab, int trace) {
   if (threadIdx.x == 0) trace_mark(trace, 0);
@@ -397,26 +400,25 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (pair) {
           // each CTA of the pair stages its 128 activation rows and its 128 weight rows; the
           // leader's full barrier counts both CTAs' bytes
-          auto boxes = [&](int p, int& nb, int& wb) {
-            nb = max(0, min(4, (rows - (m0 + 128 * p) + 31) >> 5));
+          // a stage = two 64-deep k-blocks: one 3-D box [2][128 rows][128 B] per operand
+          auto boxes = [&](int p, int& ab, int& wb) {
+            ab = rows - (m0 + 128 * p) > 0 ? 1 : 0;  // rows past the live count are stale / zero-filled
             wb = N - (n0 + 128 * p) > 0 ? 1 : 0;
           };
-          int nb_me, wb_me, nb0, wb0, nb1, wb1;
-          boxes(prank, nb_me, wb_me);
-          boxes(0, nb0, wb0);
-          boxes(1, nb1, wb1);
-          const uint32_t tx = (uint32_t)((wb0 + wb1) * kWBytes + (nb0 + nb1) * 32 * kBK * 2);
-          for (int kb = kb0; kb < kb1; ++kb, ++g) {
+          int a_me, w_me, a0, w0, a1, w1;
+          boxes(prank, a_me, w_me);
+          boxes(0, a0, w0);
+          boxes(1, a1, w1);
+          const uint32_t tx = (uint32_t)((w0 + w1 + a0 + a1) * 2 * kWBytes);
+          for (int kb = kb0; kb < kb1; kb += 2, ++g) {
             const int s = g % nst;
             mbar_wait(&empty[s], ((g / nst) & 1) ^ 1);
             uint8_t* st = ring + s * sc.stage_bytes;
             if (prank == 0) mbar_expect_tx(&full[s], tx);
             if constexpr (kPair) {
               const uint32_t fb = full_lead + s * 8;
-              if (wb_me) tma_load_2d_pair(&tw, fb, st, kb * kBK, n0 + 128 * prank, pol_w);
-              for (int j = 0; j < nb_me; ++j)
-                tma_load_2d_pair(&ta, fb, st + sc.w_bytes + j * 32 * kBK * 2, kb * kBK, m0 + 128 * prank + 32 * j,
-                                 pol_a);
+              if (w_me) tma_load_3d_pair(&tw3, fb, st, 0, n0 + 128 * prank, kb, pol_w);
+              if (a_me) tma_load_3d_pair(&ta3, fb, st + 2 * kWBytes, 0, m0 + 128 * prank, kb, pol_a);
             }
           }
           continue;
@@ -436,8 +438,12 @@ __global__ void __launch_bounds__(kThreads, 1)
           if constexpr (!kPair) {
             for (int j = 0; j < wbox; ++j)
               tma_load_2d(&tw, &full[s], st + j * kWBytes, kb * kBK, n0 + 128 * j, pol_w);
-            for (int j = 0; j < nbox; ++j)
-              tma_load_2d(&ta, &full[s], st + sc.w_bytes + j * 32 * kBK * 2, kb * kBK, m0 + 32 * j, pol_a);
+            if (nbox == 4 && sc.an == 128 && !(trace & 16)) {  // a full 128-row activation tile: one box
+              tma_load_2d(&ta128, &full[s], st + sc.w_bytes, kb * kBK, m0, pol_a);
+            } else {
+              for (int j = 0; j < nbox; ++j)
+                tma_load_2d(&ta, &full[s], st + sc.w_bytes + j * 32 * kBK * 2, kb * kBK, m0 + 32 * j, pol_a);
+            }
           }
           if (g == 0) trace_mark(trace, 2);
         }
@@ -459,16 +465,19 @@ __global__ void __launch_bounds__(kThreads, 1)
         mbar_wait(&tmem_empty[acc], ((t >> 1) & 1) ^ 1);
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
         const uint32_t d = tmem + (uint32_t)(acc * kMaxBN);
-        for (int kb = kb0; kb < kb1; ++kb, ++g) {
+        for (int kb = kb0; kb < kb1; kb += 2, ++g) {
           const int s = g % nst;
           mbar_wait(&full[s], (g / nst) & 1);
           asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-          const uint32_t sw = ring_s + s * sc.stage_bytes, sa = sw + sc.w_bytes;
-          const uint64_t da = umma_desc(sa), db = umma_desc(sw);
+          const uint32_t sw = ring_s + s * sc.stage_bytes, sa = sw + 2 * kWBytes;
           if (!(trace & 2)) {
 #pragma unroll
-            for (int k = 0; k < kBK / 16; ++k)
-              umma_bf16_pair(d, da + 2 * k, db + 2 * k, idesc, (kb != kb0 || k != 0) ? 1u : 0u);
+            for (int h = 0; h < 2; ++h) {
+              const uint64_t da = umma_desc(sa + h * kWBytes), db = umma_desc(sw + h * kWBytes);
+#pragma unroll
+              for (int k = 0; k < kBK / 16; ++k)
+                umma_bf16_pair(d, da + 2 * k, db + 2 * k, idesc, (kb != kb0 || h != 0 || k != 0) ? 1u : 0u);
+            }
           }
           umma_commit_pair(&empty[s], mask);
         }
@@ -862,6 +871,19 @@ void make_map(CUtensorMap* m, const void* ptr, int64_t rows, int64_t cols, int64
   AB_REQUIRE(r == CUDA_SUCCESS, AB_ERR_CUDA, "cuTensorMapEncodeTiled failed (" + std::to_string((int)r) + ")");
 }
 
+// 3-D view [K/64][rows][64] of a row-major [rows, K] bf16 matrix, box {64, 128, 2}: two
+// consecutive 64-deep k-blocks of 128 rows in one TMA operation (128-byte swizzle per row).
+void make_map3(CUtensorMap* m, const void* ptr, int64_t rows, int64_t K, int64_t ld) {
+  cuuint64_t dims[3] = {(cuuint64_t)kBK, (cuuint64_t)rows, (cuuint64_t)(K / kBK)};
+  cuuint64_t strides[2] = {(cuuint64_t)(ld * 2), (cuuint64_t)(kBK * 2)};
+  cuuint32_t box[3] = {(cuuint32_t)kBK, 128u, 2u};
+  cuuint32_t estr[3] = {1, 1, 1};
+  CUresult r = encode_fn()(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(ptr), dims, strides, box, estr,
+                           CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                           CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  AB_REQUIRE(r == CUDA_SUCCESS, AB_ERR_CUDA, "cuTensorMapEncodeTiled (3-D) failed (" + std::to_string((int)r) + ")");
+}
+
 template <int EPI>
 void set_attr() {
   static bool done = false;
@@ -934,10 +956,10 @@ void launch_t(const GemmPlan& p, cudaStream_t s) {
   cfg.attrs = at;
   cfg.numAttrs = 1;
   if (p.cluster == 2)
-    AB_CUDA(cudaLaunchKernelEx(&cfg, k_gemm_tc<EPI, true>, p.tw, p.ta, p.N, p.K, p.M_cap, p.rows_dev, p.stop_dev,
+    AB_CUDA(cudaLaunchKernelEx(&cfg, k_gemm_tc<EPI, true>, p.tw, p.ta, p.ta128, p.tw3, p.ta3, p.N, p.K, p.M_cap, p.rows_dev, p.stop_dev,
                                p.out, p.ldo, p.bias, p.sched, g_trace_on));
   else
-    AB_CUDA(cudaLaunchKernelEx(&cfg, k_gemm_tc<EPI, false>, p.tw, p.ta, p.N, p.K, p.M_cap, p.rows_dev, p.stop_dev,
+    AB_CUDA(cudaLaunchKernelEx(&cfg, k_gemm_tc<EPI, false>, p.tw, p.ta, p.ta128, p.tw3, p.ta3, p.N, p.K, p.M_cap, p.rows_dev, p.stop_dev,
                                p.out, p.ldo, p.bias, p.sched, g_trace_on));
 }
 
@@ -964,6 +986,9 @@ void gemm_plan(GemmPlan& p, const __nv_bfloat16* W, int N, int K, const __nv_bfl
   p.stop_dev = stop_dev;
   make_map(&p.tw, W, N, K, K, kBM);
   make_map(&p.ta, A, M_cap, K, lda, 32);  // activation tiles are loaded as 32-row boxes
+  make_map(&p.ta128, A, M_cap, K, lda, 128);  // ... or one 128-row box when the tile is full
+  make_map3(&p.tw3, W, N, K, K);              // CTA-pair stages: [2 k-blocks][128 rows][64]
+  make_map3(&p.ta3, A, M_cap, K, lda);
   gemm_set_schedule(p, 0);
 }
 

@@ -23,6 +23,8 @@ enum GemmEpi : int {
 struct GemmPlan {
   CUtensorMap tw;        // weights [N, K] bf16, box {64, 128}, 128B swizzle
   CUtensorMap ta;        // activations [M_cap, K] bf16, box {64, 32}, 128B swizzle
+  CUtensorMap ta128;     // the same, box {64, 128}
+  CUtensorMap tw3, ta3;  // 3-D views [K/64][rows][64], box {64, 128, 2} (CTA-pair stages)
   int N = 0, K = 0, M_cap = 0, BN = 0, epi = 0;  // BN: largest activation tile the kernel may pick
   void* out = nullptr;
   int64_t ldo = 0;

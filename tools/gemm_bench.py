@@ -97,6 +97,7 @@ def main():
     ap.add_argument("--bn", type=int, nargs="+", default=[0], help="activation tile width; 0 = automatic (as the decode path)")
     ap.add_argument("--split", type=int, default=1)
     ap.add_argument("--sweep", action="store_true")
+    ap.add_argument("--pair", action="store_true", help="time the CTA-pair plans (cluster of 2)")
     ap.add_argument("--mode", type=int, default=0, help="2: operand fill only, 4: MMA only (debug timing)")
     args = ap.parse_args()
     if args.mode:
@@ -107,7 +108,7 @@ def main():
     for name, (N, K, epi) in SHAPES.items():
         for M in args.m:
             for bn in args.bn:
-                r = run(N, K, M, epi, bn, args.reps, bool(args.split))
+                r = run(N, K, M, epi | (256 if args.pair else 0), bn, args.reps, bool(args.split) and not args.pair)
                 r.update({"shape": name, "M": M, "BN": bn})
                 res.append(r)
                 print(json.dumps(r), flush=True)
