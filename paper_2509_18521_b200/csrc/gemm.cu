@@ -71,12 +71,12 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   } while (!ok);
 }
 
-__device__ __forceinline__ void tma_load_2d(const CUtensorMap* map, uint64_t* bar, void* dst, int x, int y,
+__device__ __forceinline__ void tma_load_3d(const CUtensorMap* map, uint64_t* bar, void* dst, int x, int y, int z,
                                             uint64_t policy) {
   asm volatile(
-      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1, {%3, "
-      "%4}], [%2], %5;" ::"r"(smem_u32(dst)),
-      "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(x), "r"(y), "l"(policy)
+      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1, {%3, "
+      "%4, %5}], [%2], %6;" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(x), "r"(y), "r"(z), "l"(policy)
       : "memory");
 }
 
@@ -203,8 +203,9 @@ __host__ __device__ inline Sched sched_from(int code, int rows, int N, int K) {
   s.m_tiles = (rows + s.an - 1) / s.an;
   s.tiles = s.n_tiles * s.m_tiles;
   s.nk = K / kBK;
-  s.w_bytes = (s.pair ? 128 : s.wn) * kBK * 2;  // pair: per k-block slab (a stage holds two)
-  s.stage_bytes = s.pair ? 4 * kWBytes : s.w_bytes + s.an * kBK * 2;
+  // a stage holds two 64-deep k-blocks: [W kb0][W kb1][A kb0][A kb1], each slab rows x 128 B
+  s.w_bytes = (s.pair ? 128 : s.wn) * kBK * 2;  // one weight slab
+  s.stage_bytes = 2 * (s.w_bytes + (s.pair ? 128 : s.an) * kBK * 2);
   return s;
 }
 
@@ -221,8 +222,8 @@ int choose_sched(int rows, int N, int K, int max_bn, int cs, int ncl, int force,
     int lg = 0;
     while ((1 << lg) < t) ++lg;
     const int wn = pair ? 128 : swap ? kBM : t, an = pair ? 128 : swap ? t : kBM;
-    // pair stages carry two 64-deep k-blocks (one 32 KB 3-D TMA box per operand)
-    const int stages = std::min(kMaxStages, kRingBytes / ((wn * kBK * 2 + an * kBK * 2) * (pair ? 2 : 1)));
+    // stages carry two 64-deep k-blocks (one 3-D TMA box per operand, 8-64 KB per operation)
+    const int stages = std::min(kMaxStages, kRingBytes / ((wn * kBK * 2 + an * kBK * 2) * 2));
     return swap | (lg << 1) | (sp << 5) | (stages << 10) | (pair << 14);
   };
   if (force > 0 && (force & 0x40000000)) {  // a fixed code (tools/gemm_bench.py --sweep)
@@ -268,11 +269,12 @@ int choose_sched(int rows, int N, int K, int max_bn, int cs, int ncl, int force,
       const int live = std::min(an, rows);
       const int64_t epi_c = swap ? (int64_t)live * (epi == kEpiSwiGLU ? 96 : 48) : (int64_t)wn * 6 + 600;
       for (int sp = 1; sp <= cs; sp <<= 1) {
-        if (sp > 1 && ((int64_t)tiles * sp > (int64_t)ncl * cs || nk < 2 * sp)) continue;
+        if (sp > 1 && ((int64_t)tiles * sp > (int64_t)ncl * cs || nk < 4 * sp)) continue;
         const int64_t waves = sp > 1 ? 1 : (tiles + grid - 1) / grid;
         const int64_t main = (int64_t)((nk + sp - 1) / sp) * per_kb;
-        // DSMEM gather ~20 B/clk: each rank pulls (sp-1)/sp of its 1/sp lane share from the others
-        const int64_t split_cost = sp > 1 ? 1000 + (int64_t)(swap ? live : wn) * 26 * (sp - 1) / sp : 0;
+        // DSMEM gather, measured ~9 B/clk per SM (tools/gemm_trace.py): each rank pulls (sp-1)/sp of
+        // its 1/sp lane share (128 lanes x ncols fp32) from the others, plus two cluster barriers
+        const int64_t split_cost = sp > 1 ? 1500 + (int64_t)(swap ? live : wn) * 57 * (sp - 1) / sp : 0;
         const int64_t e = sp > 1 ? epi_c / sp : epi_c;
         const int64_t cost = waves * ((main > e ? main : e) + 700) + split_cost + e;
         if (cost < best_cost) {
@@ -303,9 +305,9 @@ __device__ __forceinline__ void trace_mark(int on, int k) {
 // runs the swap / no-swap / cluster split-K schedules.
 template <int EPI, bool kPair>
 __global__ void __launch_bounds__(kThreads, 1)
-    k_gemm_tc(const __grid_constant__ CUtensorMap tw, const __grid_constant__ CUtensorMap ta,
-              const __grid_constant__ CUtensorMap ta128, const __grid_constant__ CUtensorMap tw3,
-              const __grid_constant__ CUtensorMap ta3, int N, int K,
+    k_gemm_tc(const __grid_constant__ CUtensorMap tw3, const __grid_constant__ CUtensorMap tw3_256,
+              const __grid_constant__ CUtensorMap ta3_32, const __grid_constant__ CUtensorMap ta3_64,
+              const __grid_constant__ CUtensorMap ta3, const __grid_constant__ CUtensorMap ta3_256, int N, int K,
               int M_cap, const int* __restrict__ rows_dev, const int* __restrict__ stop_dev, void* __restrict__ out,
               int64_t ldo, const __nv_bfloat16* __restrict__ bias, const int* __restrict__ sched_tab, int trace) {
   if (threadIdx.x == 0) trace_mark(trace, 0);
@@ -332,6 +334,10 @@ __global__ void __launch_bounds__(kThreads, 1)
   if ((split || pair) ? ((int)blockIdx.x / cs) * per_cl >= sc.tiles : u_first >= sc.tiles)
     return;  // uniform per cluster
 
+  // the 3-D TMA views this schedule loads from
+  const CUtensorMap* mw = sc.wn == 256 && !sc.pair ? &tw3_256 : &tw3;
+  const CUtensorMap* ma = sc.pair || sc.an == 128 ? &ta3 : sc.an == 32 ? &ta3_32 : sc.an == 64 ? &ta3_64 : &ta3_256;
+
   extern __shared__ uint8_t smem_raw[];
   uint8_t* ring = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   float* xchg = reinterpret_cast<float*>(ring + kRingBytes);
@@ -353,8 +359,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_init(&tmem_empty[a], pair ? 8 : 4);  // pair: both CTAs' epilogue warps release the leader
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tw)) : "memory");
-    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&ta)) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(mw)) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(ma)) : "memory");
   }
   if (warp == 1) {
     if constexpr (kPair) {
@@ -379,8 +385,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int nt = u / sc.m_tiles;
     n0 = nt * sc.wn;
     m0 = (u - nt * sc.m_tiles) * sc.an;
-    kb0 = (int)(((int64_t)sc.nk * rank) / sc.splits);
-    kb1 = (int)(((int64_t)sc.nk * (rank + 1)) / sc.splits);
+    kb0 = 2 * (int)(((int64_t)(sc.nk / 2) * rank) / sc.splits);  // stages are k-block pairs
+    kb1 = 2 * (int)(((int64_t)(sc.nk / 2) * (rank + 1)) / sc.splits);
   };
 
   if (warp == 0) {
@@ -423,9 +429,10 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
           continue;
         }
-        const int nbox = (min(sc.an, rows - m0) + 31) >> 5;  // skip activation boxes past the live rows
-        const int wbox = (min(sc.wn, N - n0) + 127) >> 7;    // skip weight boxes past N
-        for (int kb = kb0; kb < kb1; ++kb, ++g) {
+        // one 3-D box per operand per stage: weights [2][wn][64], activations [2][an][64]
+        // (rows past N / M_cap are zero-filled, the full box is counted)
+        const uint32_t tx = (uint32_t)sc.stage_bytes;
+        for (int kb = kb0; kb < kb1; kb += 2, ++g) {
           const int s = g % nst;
           const uint32_t ph = (g / nst) & 1;
           mbar_wait(&empty[s], ph ^ 1);
@@ -434,16 +441,10 @@ __global__ void __launch_bounds__(kThreads, 1)
             mbar_arrive(&full[s]);
             continue;
           }
-          mbar_expect_tx(&full[s], wbox * kWBytes + nbox * 32 * kBK * 2);
+          mbar_expect_tx(&full[s], tx);
           if constexpr (!kPair) {
-            for (int j = 0; j < wbox; ++j)
-              tma_load_2d(&tw, &full[s], st + j * kWBytes, kb * kBK, n0 + 128 * j, pol_w);
-            if (nbox == 4 && sc.an == 128 && !(trace & 16)) {  // a full 128-row activation tile: one box
-              tma_load_2d(&ta128, &full[s], st + sc.w_bytes, kb * kBK, m0, pol_a);
-            } else {
-              for (int j = 0; j < nbox; ++j)
-                tma_load_2d(&ta, &full[s], st + sc.w_bytes + j * 32 * kBK * 2, kb * kBK, m0 + 32 * j, pol_a);
-            }
+            tma_load_3d(mw, &full[s], st, 0, n0, kb, pol_w);
+            tma_load_3d(ma, &full[s], st + 2 * sc.w_bytes, 0, m0, kb, pol_a);
           }
           if (g == 0) trace_mark(trace, 2);
         }
@@ -499,17 +500,22 @@ __global__ void __launch_bounds__(kThreads, 1)
         mbar_wait(&tmem_empty[acc], ((t >> 1) & 1) ^ 1);
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
         const uint32_t d = tmem + (uint32_t)(acc * kMaxBN);
-        for (int kb = kb0; kb < kb1; ++kb, ++g) {
+        const uint32_t a_slab = (uint32_t)(sc.an * kBK * 2);
+        for (int kb = kb0; kb < kb1; kb += 2, ++g) {
           const int s = g % nst;
           mbar_wait(&full[s], (g / nst) & 1);
           asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
           if (g == 0) trace_mark(trace, 3);
-          const uint32_t sw = ring_s + s * sc.stage_bytes, sa = sw + sc.w_bytes;
-          const uint64_t da = umma_desc(sc.swap ? sw : sa), db = umma_desc(sc.swap ? sa : sw);
+          const uint32_t sw0 = ring_s + s * sc.stage_bytes, sa0 = sw0 + 2 * sc.w_bytes;
           if (!(trace & 2)) {  // debug bit 2: fill-only timing (no MMAs)
 #pragma unroll
-            for (int k = 0; k < kBK / 16; ++k)  // +32 bytes along K inside the swizzle atom
-              umma_bf16(d, da + 2 * k, db + 2 * k, idesc, (kb != kb0 || k != 0) ? 1u : 0u);
+            for (int h = 0; h < 2; ++h) {
+              const uint32_t sw = sw0 + h * sc.w_bytes, sa = sa0 + h * a_slab;
+              const uint64_t da = umma_desc(sc.swap ? sw : sa), db = umma_desc(sc.swap ? sa : sw);
+#pragma unroll
+              for (int k = 0; k < kBK / 16; ++k)  // +32 bytes along K inside the swizzle atom
+                umma_bf16(d, da + 2 * k, db + 2 * k, idesc, (kb != kb0 || h != 0 || k != 0) ? 1u : 0u);
+            }
           }
           umma_commit(&empty[s]);
         }
@@ -860,23 +866,12 @@ EncodeFn encode_fn() {
   return fn;
 }
 
-void make_map(CUtensorMap* m, const void* ptr, int64_t rows, int64_t cols, int64_t ld, int box_rows) {
-  cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
-  cuuint64_t strides[1] = {(cuuint64_t)(ld * 2)};
-  cuuint32_t box[2] = {(cuuint32_t)kBK, (cuuint32_t)box_rows};
-  cuuint32_t estr[2] = {1, 1};
-  CUresult r = encode_fn()(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(ptr), dims, strides, box, estr,
-                           CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
-                           CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-  AB_REQUIRE(r == CUDA_SUCCESS, AB_ERR_CUDA, "cuTensorMapEncodeTiled failed (" + std::to_string((int)r) + ")");
-}
-
 // 3-D view [K/64][rows][64] of a row-major [rows, K] bf16 matrix, box {64, 128, 2}: two
 // consecutive 64-deep k-blocks of 128 rows in one TMA operation (128-byte swizzle per row).
-void make_map3(CUtensorMap* m, const void* ptr, int64_t rows, int64_t K, int64_t ld) {
+void make_map3(CUtensorMap* m, const void* ptr, int64_t rows, int64_t K, int64_t ld, int box_rows = 128) {
   cuuint64_t dims[3] = {(cuuint64_t)kBK, (cuuint64_t)rows, (cuuint64_t)(K / kBK)};
   cuuint64_t strides[2] = {(cuuint64_t)(ld * 2), (cuuint64_t)(kBK * 2)};
-  cuuint32_t box[3] = {(cuuint32_t)kBK, 128u, 2u};
+  cuuint32_t box[3] = {(cuuint32_t)kBK, (cuuint32_t)box_rows, 2u};
   cuuint32_t estr[3] = {1, 1, 1};
   CUresult r = encode_fn()(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(ptr), dims, strides, box, estr,
                            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
@@ -956,10 +951,10 @@ void launch_t(const GemmPlan& p, cudaStream_t s) {
   cfg.attrs = at;
   cfg.numAttrs = 1;
   if (p.cluster == 2)
-    AB_CUDA(cudaLaunchKernelEx(&cfg, k_gemm_tc<EPI, true>, p.tw, p.ta, p.ta128, p.tw3, p.ta3, p.N, p.K, p.M_cap, p.rows_dev, p.stop_dev,
+    AB_CUDA(cudaLaunchKernelEx(&cfg, k_gemm_tc<EPI, true>, p.tw3, p.tw3_256, p.ta3_32, p.ta3_64, p.ta3, p.ta3_256, p.N, p.K, p.M_cap, p.rows_dev, p.stop_dev,
                                p.out, p.ldo, p.bias, p.sched, g_trace_on));
   else
-    AB_CUDA(cudaLaunchKernelEx(&cfg, k_gemm_tc<EPI, false>, p.tw, p.ta, p.ta128, p.tw3, p.ta3, p.N, p.K, p.M_cap, p.rows_dev, p.stop_dev,
+    AB_CUDA(cudaLaunchKernelEx(&cfg, k_gemm_tc<EPI, false>, p.tw3, p.tw3_256, p.ta3_32, p.ta3_64, p.ta3, p.ta3_256, p.N, p.K, p.M_cap, p.rows_dev, p.stop_dev,
                                p.out, p.ldo, p.bias, p.sched, g_trace_on));
 }
 
@@ -968,7 +963,7 @@ void launch_t(const GemmPlan& p, cudaStream_t s) {
 void gemm_plan(GemmPlan& p, const __nv_bfloat16* W, int N, int K, const __nv_bfloat16* A, int M_cap, int64_t lda,
                int BN, int epi, void* out, int64_t ldo, const __nv_bfloat16* bias, const int* rows_dev,
                const int* stop_dev, int cluster) {
-  AB_REQUIRE(K % kBK == 0, AB_ERR_CONFIG, "GEMM K must be a multiple of 64");
+  AB_REQUIRE(K % (2 * kBK) == 0, AB_ERR_CONFIG, "GEMM K must be a multiple of 128");
   AB_REQUIRE(cluster == 1 || cluster == 2 || cluster == 4 || cluster == 8, AB_ERR_CONFIG,
              "GEMM split-K cluster must be 1, 2, 4 or 8");
   AB_REQUIRE(N % kBM == 0, AB_ERR_CONFIG, "GEMM N must be a multiple of 128");
@@ -984,11 +979,13 @@ void gemm_plan(GemmPlan& p, const __nv_bfloat16* W, int N, int K, const __nv_bfl
   p.bias = bias;
   p.rows_dev = rows_dev;
   p.stop_dev = stop_dev;
-  make_map(&p.tw, W, N, K, K, kBM);
-  make_map(&p.ta, A, M_cap, K, lda, 32);  // activation tiles are loaded as 32-row boxes
-  make_map(&p.ta128, A, M_cap, K, lda, 128);  // ... or one 128-row box when the tile is full
-  make_map3(&p.tw3, W, N, K, K);              // CTA-pair stages: [2 k-blocks][128 rows][64]
-  make_map3(&p.ta3, A, M_cap, K, lda);
+  // 3-D views [K/64][rows][64]: one TMA operation loads two 64-deep k-blocks of a tile operand
+  make_map3(&p.tw3, W, N, K, K, 128);
+  make_map3(&p.tw3_256, W, N, K, K, 256);
+  make_map3(&p.ta3_32, A, M_cap, K, lda, 32);
+  make_map3(&p.ta3_64, A, M_cap, K, lda, 64);
+  make_map3(&p.ta3, A, M_cap, K, lda, 128);
+  make_map3(&p.ta3_256, A, M_cap, K, lda, 256);
   gemm_set_schedule(p, 0);
 }
 

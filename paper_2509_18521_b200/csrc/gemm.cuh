@@ -21,10 +21,9 @@ enum GemmEpi : int {
 // side (BN) walks the activation rows, so small decode batches still issue
 // full 128-wide MMAs.
 struct GemmPlan {
-  CUtensorMap tw;        // weights [N, K] bf16, box {64, 128}, 128B swizzle
-  CUtensorMap ta;        // activations [M_cap, K] bf16, box {64, 32}, 128B swizzle
-  CUtensorMap ta128;     // the same, box {64, 128}
-  CUtensorMap tw3, ta3;  // 3-D views [K/64][rows][64], box {64, 128, 2} (CTA-pair stages)
+  // 3-D TMA views [K/64][rows][64] (128-byte swizzle): one operation = two 64-deep k-blocks
+  CUtensorMap tw3, tw3_256;                 // weights [N, K]: 128- / 256-row boxes
+  CUtensorMap ta3_32, ta3_64, ta3, ta3_256;  // activations [M_cap, K]: 32- / 64- / 128- / 256-row boxes
   int N = 0, K = 0, M_cap = 0, BN = 0, epi = 0;  // BN: largest activation tile the kernel may pick
   void* out = nullptr;
   int64_t ldo = 0;
