@@ -33,7 +33,7 @@ namespace {
 
 constexpr int kBM = 128;
 constexpr int kBK = 64;  // one 128-byte swizzle atom of bf16
-constexpr int kThreads = 192;
+constexpr int kThreads = 224;  // 7 warps: W producer, MMA, 4 epilogue, A producer
 constexpr int kMaxBN = 256;
 constexpr int kWBytes = kBM * kBK * 2;           // 16 KB weight tile per stage
 constexpr int kRingBytes = 192 * 1024;           // TMA ring, carved into stages per launch
@@ -389,7 +389,13 @@ __global__ void __launch_bounds__(kThreads, 1)
     kb1 = 2 * (int)(((int64_t)(sc.nk / 2) * (rank + 1)) / sc.splits);
   };
 
-  if (warp == 0) {
+  if (warp == 0 || warp == 6) {
+    // two producer threads in different warps: warp 0 issues the weight box (and arms the stage's
+    // full barrier with the whole stage's bytes), warp 6 the activation box.  A single thread's
+    // TMA issue rate (~1 operation per 240 ns, tools/probes/tma_rate.cu) would otherwise bound the
+    // fill; a complete_tx that lands before the arming expect_tx is fine (the phase also needs
+    // the arming arrival).
+    const bool wprod = warp == 0;
     if (lane == 0) {
       // weights stream through once per launch unless several row tiles share them
       uint64_t pol_w, pol_a;
@@ -420,11 +426,14 @@ __global__ void __launch_bounds__(kThreads, 1)
             const int s = g % nst;
             mbar_wait(&empty[s], ((g / nst) & 1) ^ 1);
             uint8_t* st = ring + s * sc.stage_bytes;
-            if (prank == 0) mbar_expect_tx(&full[s], tx);
+            if (wprod && prank == 0) mbar_expect_tx(&full[s], tx);
             if constexpr (kPair) {
               const uint32_t fb = full_lead + s * 8;
-              if (w_me) tma_load_3d_pair(&tw3, fb, st, 0, n0 + 128 * prank, kb, pol_w);
-              if (a_me) tma_load_3d_pair(&ta3, fb, st + 2 * kWBytes, 0, m0 + 128 * prank, kb, pol_a);
+              if (wprod) {
+                if (w_me) tma_load_3d_pair(&tw3, fb, st, 0, n0 + 128 * prank, kb, pol_w);
+              } else {
+                if (a_me) tma_load_3d_pair(&ta3, fb, st + 2 * kWBytes, 0, m0 + 128 * prank, kb, pol_a);
+              }
             }
           }
           continue;
@@ -438,15 +447,18 @@ __global__ void __launch_bounds__(kThreads, 1)
           mbar_wait(&empty[s], ph ^ 1);
           uint8_t* st = ring + s * sc.stage_bytes;
           if (trace & 4) {  // debug: MMA-only timing (no operand loads)
-            mbar_arrive(&full[s]);
+            if (wprod) mbar_arrive(&full[s]);
             continue;
           }
-          mbar_expect_tx(&full[s], tx);
           if constexpr (!kPair) {
-            tma_load_3d(mw, &full[s], st, 0, n0, kb, pol_w);
-            tma_load_3d(ma, &full[s], st + 2 * sc.w_bytes, 0, m0, kb, pol_a);
+            if (wprod) {
+              mbar_expect_tx(&full[s], tx);
+              tma_load_3d(mw, &full[s], st, 0, n0, kb, pol_w);
+            } else {
+              tma_load_3d(ma, &full[s], st + 2 * sc.w_bytes, 0, m0, kb, pol_a);
+            }
           }
-          if (g == 0) trace_mark(trace, 2);
+          if (g == 0 && wprod) trace_mark(trace, 2);
         }
       }
     }
@@ -524,7 +536,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       trace_mark(trace, 4);
     }
     }
-  } else {
+  } else if (warp < 6) {
     // epilogue warps 2..5 -> TMEM lane quadrants 2,3,0,1
     const int quad = warp & 3;
     const int lrow = quad * 32 + lane;  // TMEM lane
@@ -817,7 +829,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       cluster_sync_all();
     }
   }
-  if (split && warp < 2) {
+  if (split && (warp < 2 || warp == 6)) {
     // producer and MMA warps join the epilogue's two cluster barriers (one tile per cluster)
     __syncwarp();
     cluster_sync_all();
