@@ -20,6 +20,7 @@
 #include <cuda_bf16.h>
 
 #include <algorithm>
+#include <cmath>
 #include <map>
 #include <mutex>
 #include <tuple>
@@ -243,7 +244,6 @@ int choose_sched(int rows, int N, int K, int max_bn, int cs, int ncl, int force,
     }
     return pack(swap, t, sp);
   }
-  int64_t best_cost = INT64_MAX;
   int best = 0;
   if (cs == 2) {  // a pair plan: every row count runs the CTA-pair schedule
     if (N % 128 || (epi == kEpiSwiGLU && N % 256) || nk % 2) return 0;
@@ -252,6 +252,12 @@ int choose_sched(int rows, int N, int K, int max_bn, int cs, int ncl, int force,
     return pack(0, 256, 1, 1);
   }
   // force > 0: swap-AB with exactly an = force; force < 0: no swap with wn = -force
+  // Times in microseconds, calibrated against tools/gemm_sched_sweep.py on B200 (all schedules of
+  // the QKV / O / down shapes at 64-1024 rows): a stage (two 64-deep k-blocks) streams at ~100 GB/s
+  // per CTA or is MMA-bound; the swap-AB epilogue costs per live activation row, the no-swap one
+  // per weight row (its fp32 residual read-modify-write is the slow one); cluster split-K pays a
+  // fixed ~4 us (two cluster barriers + DSMEM gather) plus a per-column share.
+  double best_us = 1e30;
   for (int mode = 0; mode < 2; ++mode) {
     const int swap = mode == 0 ? 1 : 0;
     if (force > 0 && !swap) continue;
@@ -263,22 +269,20 @@ int choose_sched(int rows, int N, int K, int max_bn, int cs, int ncl, int force,
       if (!swap && epi == kEpiSwiGLU && t != 256) continue;
       const int wn = swap ? kBM : t, an = swap ? t : kBM;
       const int tiles = ((N + wn - 1) / wn) * ((rows + an - 1) / an);
-      const int64_t mma = (int64_t)wn * an / 64;  // 128 x 256 x 64 -> 512 clk
-      const int64_t fill = (int64_t)(wn + an) * 128 / 64;
-      const int64_t per_kb = mma > fill ? mma : fill;
+      const double t_stage = std::max((wn + an) * 256.0 / 100e3, wn * an / 32.0 / 1965.0);
       const int live = std::min(an, rows);
-      const int64_t epi_c = swap ? (int64_t)live * (epi == kEpiSwiGLU ? 96 : 48) : (int64_t)wn * 6 + 600;
+      const double epi_cols = swap ? live : wn;
+      const double epi_rate = swap ? (epi == kEpiAddF32 ? 0.05 : epi == kEpiSwiGLU ? 0.06 : 0.03)
+                                   : (epi == kEpiAddF32 ? 0.13 : epi == kEpiSwiGLU ? 0.03 : 0.02);
       for (int sp = 1; sp <= cs; sp <<= 1) {
         if (sp > 1 && ((int64_t)tiles * sp > (int64_t)ncl * cs || nk < 4 * sp)) continue;
-        const int64_t waves = sp > 1 ? 1 : (tiles + grid - 1) / grid;
-        const int64_t main = (int64_t)((nk + sp - 1) / sp) * per_kb;
-        // DSMEM gather, measured ~9 B/clk per SM (tools/gemm_trace.py): each rank pulls (sp-1)/sp of
-        // its 1/sp lane share (128 lanes x ncols fp32) from the others, plus two cluster barriers
-        const int64_t split_cost = sp > 1 ? 1500 + (int64_t)(swap ? live : wn) * 57 * (sp - 1) / sp : 0;
-        const int64_t e = sp > 1 ? epi_c / sp : epi_c;
-        const int64_t cost = waves * ((main > e ? main : e) + 700) + split_cost + e;
-        if (cost < best_cost) {
-          best_cost = cost;
+        const double waves = std::ceil((double)tiles * sp / grid);
+        const double main_us = std::ceil(nk / 2.0 / sp) * t_stage;
+        const double e = epi_rate * epi_cols / sp;
+        const double split_us = sp > 1 ? 4.0 + (swap ? 0.08 * live : 0.04 * wn) : 0.0;
+        const double us = waves * std::max(main_us, e) + e + split_us;
+        if (us < best_us) {
+          best_us = us;
           best = pack(swap, t, sp);
         }
       }
@@ -1152,4 +1156,10 @@ extern "C" int ab_debug_gemm_clusters(int cs, int* out) {
     ab::set_last_error(e.what());
     return e.code;
   }
+}
+
+// Debug / tests (no GPU needed): the packed schedule the cost model picks for `rows` live rows
+// (cs = cluster size, ncl = co-resident clusters, force as GemmPlan::force).
+extern "C" int ab_debug_gemm_sched(int N, int K, int rows, int max_bn, int cs, int ncl, int force, int epi) {
+  return ab::choose_sched(rows, N, K, max_bn, cs, ncl, force, epi);
 }
