@@ -1,0 +1,73 @@
+"""K1 (fused sampler) row rule: CPU oracle self-checks, and the CUDA kernel against it (gpu)."""
+
+import ctypes as C
+
+import numpy as np
+import pytest
+
+from oracle import sampler_ref
+
+
+def _brute_nucleus(z, T, top_p):
+    """Smallest prefix of the probability-sorted vocabulary reaching top_p (ties kept), in the
+    oracle's fixed-point units: the definition nucleus_threshold implements."""
+    z = np.asarray(z, np.float32)
+    inv_t = np.float32(1.0) / np.float32(T)
+    k2 = np.float32(inv_t * np.float32(1.4426950408889634))
+    p = np.exp2(((z - z.max()) * k2).astype(np.float32)).astype(np.float64)
+    q = np.floor(p * 2.0 ** 40).astype(np.uint64)
+    tot = int(q.sum(dtype=np.uint64))
+    target = max(1, int(np.ceil(top_p * float(tot))))
+    kept = set()
+    for v in sorted(set(z.tolist()), reverse=True):
+        idx = np.nonzero(z == np.float32(v))[0]
+        kept.update(idx.tolist())
+        if int(q[list(kept)].sum(dtype=np.uint64)) >= target:
+            return kept
+    return kept
+
+
+@pytest.mark.parametrize("top_p", [0.3, 0.9, 0.99])
+def test_oracle_nucleus_matches_brute_force(top_p):
+    rng = np.random.default_rng(1)
+    for _ in range(5):
+        z = (rng.standard_normal(300) * 3).astype(np.float32)
+        z[:5] = z[5]  # ties
+        k = sampler_ref.nucleus_threshold(z, 0.8, top_p)
+        kept = set(np.nonzero(sampler_ref.logit_keys(z) >= np.uint32(k))[0].tolist())
+        assert kept == _brute_nucleus(z, 0.8, top_p)
+
+
+def test_oracle_reduces_to_reference_rule_at_t1_p1():
+    """T = 1, top_p = 1: index-order inverse CDF of softmax(z) (policy.py:93-94)."""
+    rng = np.random.default_rng(2)
+    z = rng.standard_normal(50).astype(np.float32)
+    p = np.exp(z.astype(np.float64) - z.max())
+    cdf = np.cumsum(p / p.sum())
+    for u in rng.random(200):
+        tok, _ = sampler_ref.sample_row(z, 1.0, False, 1.0, float(u))
+        assert tok == min(int(np.searchsorted(cdf, u, side="right")), 49)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("V", [1000, 151936])
+@pytest.mark.parametrize("T,top_p,greedy", [(0.8, 1.0, False), (0.8, 0.9, False), (1.0, 0.5, False),
+                                            (0.6, 0.95, False), (0.8, 0.9, True)])
+def test_sampler_kernel_matches_oracle(V, T, top_p, greedy):
+    torch = pytest.importorskip("torch")
+    from paper_2509_18521_b200 import _capi
+
+    rows = 48
+    g = torch.Generator().manual_seed(V + int(top_p * 100))
+    z = (torch.randn(rows, V, generator=g) * 2.5).float()
+    u = torch.rand(rows, generator=g, dtype=torch.float64)
+    zd, ud = z.cuda(), u.cuda()
+    tok = torch.empty(rows, dtype=torch.int32, device="cuda")
+    lp = torch.empty(rows, dtype=torch.float64, device="cuda")
+    _capi.call("ab_debug_sample_rows", C.c_void_p(zd.data_ptr()), rows, V, C.c_float(T), int(greedy),
+               C.c_float(top_p), C.c_void_p(ud.data_ptr()), C.c_void_p(tok.data_ptr()), C.c_void_p(lp.data_ptr()))
+    tok, lp = tok.cpu().numpy(), lp.cpu().numpy()
+    for r in range(rows):
+        t_ref, lp_ref = sampler_ref.sample_row(z[r].numpy(), T, greedy, top_p, float(u[r]))
+        assert tok[r] == t_ref, (r, tok[r], t_ref)
+        assert abs(lp[r] - lp_ref) < 1e-5, (r, lp[r], lp_ref)
