@@ -182,6 +182,12 @@ int ab_engine_abort(ab_engine* e, int32_t* handles, int32_t* gen, int cap, int* 
 int ab_engine_active(ab_engine* e, int32_t* handles, int32_t* gen, int cap, int* n_active);
 int ab_engine_read_payload(ab_engine* e, const int32_t* handles, const int32_t* starts, const int32_t* counts, int n,
                            int32_t* tokens, double* logprobs);
+
+// GSPO / sequence-level ratios: per-sample sum of the recorded behaviour log-probabilities over
+// all generated tokens (device reduction of the partial-rollout payload) and the token count.
+// Reference: the build's addition for SURVEY.md §8a row a17 (GSPO length-normalised log-prob);
+// the reference computes sequence log-probs on the host (src/april_sim/policy.py:133-137).
+int ab_engine_sequence_logprobs(ab_engine* e, const int32_t* handles, int n, double* sums, int32_t* lens);
 int ab_engine_release(ab_engine* e, const int32_t* handles, int n);
 int ab_engine_stats(ab_engine* e, ab_stats* out);
 int ab_engine_profile(ab_engine* e, int enable, int sample_every);
@@ -192,7 +198,8 @@ int ab_engine_set_iteration(ab_engine* e, int64_t iteration_index);
 
 /* K6: group-normalised advantages over contiguous groups of G rewards.
  * mode 0 = mean baseline, 1 = mean/std (GRPO), 2 = mean/std with a
- * zero-std flag (DAPO); pointers are device or host (cudaMemcpyDefault). */
+ * zero-std flag (DAPO), 3 = mean/std for GSPO (whose sequence ratio uses
+ * ab_engine_sequence_logprobs); pointers are device or host. */
 int ab_group_advantages(const double* rewards, int n_groups, int group_size, int mode, double eps, double* adv,
                         int32_t* zero_std_flags, int device);
 
@@ -200,6 +207,16 @@ int ab_group_advantages(const double* rewards, int n_groups, int group_size, int
 int ab_debug_gemm(const void* W, const void* A, void* out, const void* bias, int N, int K, int M, int BN, int epi);
 int ab_debug_gemm_time(const void* W, const void* A, void* out, const void* bias, int N, int K, int M, int BN, int epi,
                        int reps, float* ms_out);
+/* packed GEMM schedule the cost model picks (host only, no GPU needed) */
+int ab_debug_gemm_sched(int N, int K, int rows, int max_bn, int cluster, int n_clusters, int force, int epi);
+/* co-resident persistent GEMM clusters of `cluster` CTAs */
+int ab_debug_gemm_clusters(int cluster, int* out);
+/* per-CTA %globaltimer timeline of the next GEMM launches (tools/gemm_trace.py) */
+int ab_debug_gemm_trace(int on, unsigned long long* out);
+int ab_debug_trace_mark(int slot);
+/* K1's per-row routine on device logits [rows, V] and draws u [rows] (tests/test_sampler.py) */
+int ab_debug_sample_rows(const float* logits, int rows, int V, float temperature, int greedy, float top_p,
+                         const double* u, int* tok, double* logp);
 
 #ifdef __cplusplus
 }

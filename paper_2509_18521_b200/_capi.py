@@ -107,6 +107,7 @@ _SIGS = {
     "ab_engine_abort": [P, I32P, I32P, C.c_int, C.POINTER(C.c_int), C.POINTER(C.c_int)],
     "ab_engine_active": [P, I32P, I32P, C.c_int, C.POINTER(C.c_int)],
     "ab_engine_read_payload": [P, I32P, I32P, I32P, C.c_int, I32P, F64P],
+    "ab_engine_sequence_logprobs": [P, I32P, C.c_int, F64P, I32P],
     "ab_engine_release": [P, I32P, C.c_int],
     "ab_engine_stats": [P, C.POINTER(Stats)],
     "ab_engine_profile": [P, C.c_int, C.c_int],
@@ -117,6 +118,11 @@ _SIGS = {
     "ab_debug_gemm": [P, P, P, P, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int],
     "ab_debug_gemm_time": [P, P, P, P, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int,
                            C.POINTER(C.c_float)],
+    "ab_debug_gemm_sched": [C.c_int] * 8,
+    "ab_debug_gemm_clusters": [C.c_int, C.POINTER(C.c_int)],
+    "ab_debug_gemm_trace": [C.c_int, P],
+    "ab_debug_trace_mark": [C.c_int],
+    "ab_debug_sample_rows": [P, C.c_int, C.c_int, C.c_float, C.c_int, C.c_float, P, P, P],
 }
 EXPORTS = sorted(_SIGS) + ["ab_last_error", "ab_version"]
 

@@ -7,6 +7,9 @@
 //   mode 2  DAPO                 as mode 1, plus a per-group zero-std flag
 //                                (dynamic-sampling filter; not in the reference,
 //                                parity-unpinned)
+//   mode 3  GSPO                 as mode 1 (the sequence-level ratio uses the
+//                                length-normalised behaviour log-prob from
+//                                ab_engine_sequence_logprobs; parity-unpinned)
 // numpy's mean/std are pairwise sums (np_pairwise_sum), so results are
 // bit-identical to the reference for any G.
 #include <vector>
@@ -64,7 +67,7 @@ extern "C" int ab_group_advantages(const double* rewards, int n_groups, int grou
   try {
     AB_REQUIRE(n_groups >= 0 && group_size >= 1, AB_ERR_CONFIG, "advantages need at least one reward");
     AB_REQUIRE(group_size <= ab::kMaxGroupForAdv, AB_ERR_CONFIG, "group too large");
-    AB_REQUIRE(mode >= 0 && mode <= 2, AB_ERR_CONFIG, "unknown advantage mode");
+    AB_REQUIRE(mode >= 0 && mode <= 3, AB_ERR_CONFIG, "unknown advantage mode");
     if (n_groups == 0) return AB_OK;
     AB_CUDA(cudaSetDevice(device));
     const size_t n = (size_t)n_groups * group_size;

@@ -832,6 +832,46 @@ static void read_payload(Engine& e, const int32_t* handles, const int32_t* start
   cudaFree(dl);
 }
 
+// Per-sample sum of the recorded behaviour log-probabilities over all generated tokens (one
+// warp per handle, lane-strided partial sums combined by a fixed xor tree: deterministic).
+// GSPO's length-normalised sequence log-ratio uses sum / length.
+__global__ void k_seq_logprob(EngineDev e, const int32_t* __restrict__ handles, int n, double* __restrict__ sums,
+                              int32_t* __restrict__ lens) {
+  const int i = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5), lane = threadIdx.x & 31;
+  if (i >= n) return;
+  const int h = handles[i];
+  const int len = e.h_gen[h];
+  const double* lp = e.h_logp + (size_t)h * e.L;
+  double acc = 0.0;
+  for (int j = lane; j < len; j += 32) acc += lp[j];
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+  if (lane == 0) {
+    sums[i] = acc;
+    lens[i] = len;
+  }
+}
+
+static void seq_logprob(Engine& e, const int32_t* handles, int n, double* sums, int32_t* lens) {
+  AB_REQUIRE(e.d.record, AB_ERR_CONTRACT, "engine does not record token payloads");
+  if (n <= 0) return;
+  for (int i = 0; i < n; ++i) AB_REQUIRE(handles[i] >= 0 && handles[i] < e.d.H, AB_ERR_CONTRACT, "handle out of range");
+  int32_t *dh, *dn;
+  double* ds;
+  AB_CUDA(cudaMalloc(&dh, sizeof(int32_t) * n));
+  AB_CUDA(cudaMalloc(&dn, sizeof(int32_t) * n));
+  AB_CUDA(cudaMalloc(&ds, sizeof(double) * n));
+  AB_CUDA(cudaMemcpyAsync(dh, handles, sizeof(int32_t) * n, cudaMemcpyHostToDevice, e.stream));
+  k_seq_logprob<<<ceil_div(n, 8), 256, 0, e.stream>>>(e.d, dh, n, ds, dn);
+  AB_CUDA(cudaGetLastError());
+  AB_CUDA(cudaMemcpyAsync(sums, ds, sizeof(double) * n, cudaMemcpyDeviceToHost, e.stream));
+  AB_CUDA(cudaMemcpyAsync(lens, dn, sizeof(int32_t) * n, cudaMemcpyDeviceToHost, e.stream));
+  AB_CUDA(cudaStreamSynchronize(e.stream));
+  cudaFree(dh);
+  cudaFree(dn);
+  cudaFree(ds);
+}
+
 static void set_groups(Engine& e, const int32_t* pairs, int n) {
   if (n <= 0) return;
   AB_REQUIRE((size_t)2 * n <= e.stage_i32_cap, AB_ERR_CONTRACT, "too many groups");
@@ -922,6 +962,10 @@ int ab_engine_active(ab_engine* e, int32_t* handles, int32_t* gen, int cap, int*
 int ab_engine_read_payload(ab_engine* e, const int32_t* handles, const int32_t* starts, const int32_t* counts, int n,
                            int32_t* tokens, double* logprobs) {
   return ab::guard([&] { ab::read_payload(*e->impl, handles, starts, counts, n, tokens, logprobs); });
+}
+
+int ab_engine_sequence_logprobs(ab_engine* e, const int32_t* handles, int n, double* sums, int32_t* lens) {
+  return ab::guard([&] { ab::seq_logprob(*e->impl, handles, n, sums, lens); });
 }
 
 int ab_engine_release(ab_engine* e, const int32_t* handles, int n) {

@@ -453,6 +453,28 @@ class Engine:
         self._release(drained)  # zero-token samples hold no device state worth keeping
         return out
 
+    def sequence_logprobs(self, samples):
+        """(sum of behaviour log-probs over all generated tokens, token count) per sample, reduced
+        on the device from the resident partial-rollout payload (GSPO's length-normalised sequence
+        log-ratio uses sum / count).  Samples must still hold their device handle (active, queued
+        or paused in the continuation buffer)."""
+        n = len(samples)
+        if n == 0 or self._h is None:
+            return np.zeros(0), np.zeros(0, dtype=np.int32)
+        self._flush()
+        hs = np.empty(n, dtype=np.int32)
+        for k, s in enumerate(samples):
+            h = self._handle.get(id(s))
+            if h is None:
+                raise ContractViolation("sample has no device payload (already delivered or never admitted)")
+            hs[k] = h
+        sums = np.empty(n, dtype=np.float64)
+        lens = np.empty(n, dtype=np.int32)
+        capi.call("ab_engine_sequence_logprobs", self._h, hs.ctypes.data_as(capi.I32P), n,
+                  sums.ctypes.data_as(capi.F64P), lens.ctypes.data_as(capi.I32P))
+        self._d2h += n * 12
+        return sums, lens
+
     def io_bytes(self) -> tuple[int, int]:
         """(host->device, device->host) bytes moved through the C-ABI so far."""
         return self._h2d, self._d2h

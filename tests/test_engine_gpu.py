@@ -261,3 +261,6 @@ def test_group_advantages_kernel_matches_numpy():
             assert np.array_equal(a, np.concatenate(ref)), (g, mode)
     a, flags = pb.batch_advantages(np.array([0.5] * 8 + [0.0, 1.0] * 4), 8, "dapo", return_flags=True)
     assert flags.tolist() == [1, 0]
+    # GSPO normalises like GRPO (its sequence ratio comes from Engine.sequence_logprobs)
+    r = rng.random(8 * 5)
+    assert np.array_equal(pb.batch_advantages(r, 8, "gspo"), pb.batch_advantages(r, 8, "mean_std_baseline"))

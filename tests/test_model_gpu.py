@@ -163,3 +163,28 @@ def test_kv_pages_are_recycled():
                 eng.submit(s)
         _drain(eng)
     assert eng.stats().kv_pages_free == free0
+
+
+def test_sequence_logprobs_reduce_the_resident_payload():
+    """GSPO's length-normalised sequence log-prob, reduced on the device while the samples are
+    still resident, equals the host sum of the behaviour log-probs delivered later."""
+    spec = pb.PRESETS["tiny"]
+    prompts = _prompts(spec, 1, 16)
+    eng = _engine(spec, prompts, greedy=False, temperature=0.9)
+    eng.begin_step(0)
+    samples = []
+    for j in range(4):
+        s = RolloutSample(0, j)
+        s.target_length = 30 + j
+        eng.submit(s)
+        samples.append(s)
+    for _ in range(12):
+        eng.decode_iteration()
+    sums, lens = eng.sequence_logprobs(samples)
+    assert lens.tolist() == [12] * 4
+    _drain(eng)
+    for s, sm, n in zip(samples, sums, lens):
+        full = s.behavior_logprob_trace()
+        assert len(full) == s.target_length
+        assert abs(sm - float(np.sum(full[:n]))) < 1e-9 * max(1.0, abs(sm))
+    eng.close()
