@@ -107,32 +107,43 @@ def build_engine(pb, w, device, seed, record=True):
     return spec, eng
 
 
-def make_scheduler(pb, w, eng, mode, seed):
-    cfg = pb.SchedulerConfig(rollout_batch_size=w["n"], samples_per_prompt=w["g"],
-                             over_sampling_batch_size=w["n_prime"] if mode == "april" else w["n"], mode=mode)
+def make_scheduler(pb, w, eng, mode, seed, world=1):
+    # weak scaling: N, N' grow with the number of data-parallel engines (fixed work per GPU)
+    n, n_prime = w["n"] * world, w["n_prime"] * world
+    cfg = pb.SchedulerConfig(rollout_batch_size=n, samples_per_prompt=w["g"],
+                             over_sampling_batch_size=n_prime if mode == "april" else n, mode=mode)
     dist = pb.LengthDistribution.lognormal(w["mu"], w["sigma"], w["l_max"])
     return pb.Scheduler(cfg, eng, pb.InstanceSource(group_size=w["g"]), pb.LengthSampler(dist, w["rho"], seed))
 
 
-def learner_glue(pb, w, out, target_token=0):
+def learner_glue(pb, w, out, target_token=0, comm=None):
     """Synthetic GRPO glue (simulate.py:47-65): target-token-fraction rewards on the
-    delivered token ids, then the K6 advantage kernel over contiguous groups."""
+    delivered token ids, then the K6 advantage kernel over contiguous groups.  Data-parallel:
+    each rank scores the responses it generated and the finished-response results are
+    gathered (NCCL) so every rank sees the whole batch in delivery order."""
     samples = out.batch_samples()
-    rewards = []
+    mine = {}
     for s in samples:
         toks = s.token_ids()
-        rewards.append(sum(1 for t in toks if t % 4 == target_token) / len(toks) if toks else 0.0)
+        if comm is None or len(toks) == s.total_tokens:  # this rank holds the payload
+            mine[s.sample_id] = sum(1 for t in toks if t % 4 == target_token) / len(toks) if toks else 0.0
+    if comm is not None:
+        merged = {}
+        for part in comm.allgather(mine):
+            merged.update(part)
+        mine = merged
+    rewards = [mine[s.sample_id] for s in samples]
     return pb.batch_advantages(rewards, w["g"], w["adv"])
 
 
-def run_steps(pb, w, sched, eng, k0, n, timed_e2e=False):
+def run_steps(pb, w, sched, eng, k0, n, timed_e2e=False, comm=None):
     recs = []
     for k in range(k0, k0 + n):
         h2d0 = eng.io_bytes()
         t0 = time.perf_counter()
         out = sched.run_step(k)
         if timed_e2e:
-            learner_glue(pb, w, out)
+            learner_glue(pb, w, out, comm=comm)
         t1 = time.perf_counter()
         h2d1 = eng.io_bytes()
         recs.append(dict(step=k, tokens=out.tokens_generated, wall=out.rollout_wall_time, host=t1 - t0,
@@ -219,6 +230,9 @@ def main():
     ap.add_argument("--profile-every", type=int, default=8)
     ap.add_argument("--ref-step-s", type=float, default=12.0)
     ap.add_argument("--seed", type=int, default=0)
+    ap.add_argument("--force-dp", action="store_true", help="run the data-parallel engine even at N = 1 (tests)")
+    ap.add_argument("--replicas", action="store_true",
+                    help="N > 1: independent engine replicas instead of the lockstep data-parallel engine")
     args = ap.parse_args()
     if args.impl == "reference":
         return reference_arm(args)
@@ -227,20 +241,32 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     dist = None
-    if world > 1:
+    if world > 1 or args.force_dp:
         import torch
         import torch.distributed as dist
 
         torch.cuda.set_device(local)
-        dist.init_process_group("nccl")
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        os.environ.setdefault("MASTER_PORT", "29531")
+        dist.init_process_group("nccl", rank=rank, world_size=world)
     import paper_2509_18521_b200 as pb
 
     w = WORKLOADS[args.workload]
-    seed = args.seed + rank  # replicas: independent prompt streams per rank
+    dp = (world > 1 and not args.replicas) or args.force_dp
+    # data-parallel: one replicated scheduler (same seed everywhere) over lockstep engines;
+    # replicas: independent prompt streams per rank
+    seed = args.seed if dp else args.seed + rank
     hbm_peak, tf_peak, peak_kind = _peaks()
 
     spec, eng = build_engine(pb, w, local, seed, record=True)
-    sched = make_scheduler(pb, w, eng, "april", seed)
+    comm = None
+    front = eng  # what the scheduler drives
+    if dp:
+        from paper_2509_18521_b200.dist import DataParallelEngine, GpuLocal, TorchComm
+
+        comm = TorchComm(device=f"cuda:{local}")
+        front = DataParallelEngine(GpuLocal(eng), comm, w["slots"])
+    sched = make_scheduler(pb, w, front, "april", seed, world if dp else 1)
     run_steps(pb, w, sched, eng, 0, args.warmup)
     if dist:
         dist.barrier()
@@ -262,7 +288,7 @@ def main():
     eng.profile(False)
     tokens = sum(r["tokens"] for r in rec)
     # e2e: same steps, payload gathered to host + rewards + advantages, host wall clock
-    rec_e2e = run_steps(pb, w, sched, eng, args.warmup + args.steps, args.steps, timed_e2e=True)
+    rec_e2e = run_steps(pb, w, sched, eng, args.warmup + args.steps, args.steps, timed_e2e=True, comm=comm)
     e2e_tps = sum(r["tokens"] for r in rec_e2e) / sum(r["host"] for r in rec_e2e)
     stats = eng.stats()
     eng.close()
@@ -271,14 +297,18 @@ def main():
     sync = None
     if not args.no_sync:
         _, eng_s = build_engine(pb, w, local, seed, record=True)
-        sch_s = make_scheduler(pb, w, eng_s, "baseline", seed)
+        front_s = eng_s
+        if dp:
+            front_s = DataParallelEngine(GpuLocal(eng_s), comm, w["slots"])
+        sch_s = make_scheduler(pb, w, front_s, "baseline", seed, world if dp else 1)
         rs = run_steps(pb, w, sch_s, eng_s, 0, args.sync_steps)
         sync = {"tokens_per_s": sum(r["tokens"] for r in rs) / sum(r["wall"] for r in rs),
                 "ms_per_step": 1e3 * statistics.mean(r["wall"] for r in rs), "steps": len(rs),
                 "iterations_per_step": statistics.mean(r["iters"] for r in rs)}
         eng_s.close()
 
-    total_tokens = tokens * world
+    # DP: every rank's scheduler already counts the whole job's tokens; replicas: per rank
+    total_tokens = tokens if dp else tokens * world
     value = total_tokens / t_dev if t_dev > 0 else 0.0
     att = kstats.get("attention")
     roof = None
@@ -305,14 +335,16 @@ def main():
                    "samples_per_prompt": w["g"], "over_provision_groups": w["n_prime"], "max_len": w["l_max"],
                    "length_dist": f"lognormal({w['mu']}, {w['sigma']}), rho {w['rho']}",
                    "prompt_len": w["prompt"], "slots": w["slots"], "temperature": w["temperature"],
-                   "parallelism": f"dp{world} replicas", "l2": "inputs larger than L2 (weights + KV >> 126 MB)"},
+                   "parallelism": (f"dp{world} lockstep engines (NCCL per-iteration count allreduce, response gather)"
+                                   if dp else f"dp{world} replicas"),
+                   "l2": "inputs larger than L2 (weights + KV >> 126 MB)"},
         "april": {"tokens_per_s": value, "ms_per_step": ms_step, "steps": len(rec),
                   "iterations_per_step": statistics.mean(r["iters"] for r in rec),
                   "carried_in_tokens_per_step": statistics.mean(r["carried"] for r in rec)},
         "sync": sync,
-        "april_over_sync": (value / world / sync["tokens_per_s"]) if sync else None,
+        "april_over_sync": ((value if dp else value / world) / sync["tokens_per_s"]) if sync else None,
         "roofline": roof, "kernels": kern,
-        "e2e": {"value": e2e_tps * world, "unit": "tokens/s",
+        "e2e": {"value": e2e_tps * (1 if dp else world), "unit": "tokens/s",
                 "h2d_bytes_per_step": int(statistics.mean(r["h2d"] for r in rec_e2e)),
                 "d2h_bytes_per_step": int(statistics.mean(r["d2h"] for r in rec_e2e))},
         "clocks": clk.summary(), "gpu_launches": int(launches),
