@@ -169,7 +169,10 @@ __global__ void __launch_bounds__(kThreads, 2)
         const int packed = m.att_items[rs];
         const int row = packed & 0xffff, sp = packed >> 16;
         const int n = m.row_pos[row] + 1;
-        const int c0 = sp * chunk, c1 = min(n, c0 + chunk);
+        // the row's nsplit = ceil(n / chunk) splits are balanced (64-token multiples)
+        const int nsplit_row = (n + chunk - 1) / chunk;
+        const int per = (((n + nsplit_row - 1) / nsplit_row) + kTok - 1) / kTok * kTok;
+        const int c0 = sp * per, c1 = min(n, c0 + per);
         const int ntiles = (c1 - c0 + kTok - 1) / kTok;
         const int32_t* bt = m.bt + (size_t)m.row_btrow[row] * m.MP;
         const int qslot = k % kQSlots;

@@ -65,6 +65,7 @@ __device__ __forceinline__ int pop_page(Ctl* c) {
 // allocate a KV page when the row crosses a page boundary, and build the
 // attention work list (exclusive prefix of KV splits per row).
 constexpr int kPrepThreads = 1024;
+constexpr unsigned long long kItemsPerCta = 3;  // attention work items per persistent CTA (dynamic cursor)
 
 // Per-iteration decode prologue: gather the live rows, allocate KV pages for the
 // token about to be written, and build the attention work list.  The KV split
@@ -107,7 +108,7 @@ __global__ void __launch_bounds__(kPrepThreads) k_prep_decode(EngineDev e, Model
   if (threadIdx.x == 0) {
     unsigned long long tot = 0;
     for (int k = 0; k < kPrepThreads / 32; ++k) tot += s_u[k];
-    const unsigned long long per = (tot * (unsigned long long)m.hk + 4ull * att_ctas - 1) / (4ull * att_ctas);
+    const unsigned long long per = (tot * (unsigned long long)m.hk + kItemsPerCta * att_ctas - 1) / (kItemsPerCta * att_ctas);
     int ch = (int)min(per, (unsigned long long)(1 << 30));
     ch = (ch + 63) & ~63;
     s_chunk = max(ch, min_chunk);
