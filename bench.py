@@ -38,7 +38,7 @@ METRIC = "rollout tokens/s & RL-step rollout time, APRIL vs sync, long-tail leng
 
 WORKLOADS = {
     "C2": dict(model="qwen2.5-1.5b", n=64, g=8, n_prime=128, slots=1024, l_max=4096, mu=6.6, sigma=1.0, rho=0.7,
-               prompt=256, temperature=0.8, adv="mean_std_baseline", page=64),
+               prompt=256, temperature=0.8, adv="mean_std_baseline", page=64, nondet_gemm=True),
     # small smoke workload (tiny decoder) for quick checks
     "C1": dict(model="tiny", n=8, g=4, n_prime=16, slots=64, l_max=1024, mu=5.5, sigma=1.0, rho=0.7, prompt=32,
                temperature=0.8, adv="mean_std_baseline", page=16),
@@ -103,7 +103,7 @@ def build_engine(pb, w, device, seed, record=True):
         pb.EngineConfig(max_slots=w["slots"], l_max=w["l_max"]), global_seed=seed, model=spec,
         sampling=pb.SamplingConfig(temperature=w["temperature"]), prompt_len=w["prompt"], page_size=w["page"],
         device=device, record_payload=record, max_handles=max(4096, 4 * w["n_prime"] * w["g"]),
-        max_groups=4 * w["n_prime"] + 64)
+        max_groups=4 * w["n_prime"] + 64, nondeterministic_gemm=w.get("nondet_gemm", False))
     return spec, eng
 
 
@@ -335,6 +335,8 @@ def main():
                    "samples_per_prompt": w["g"], "over_provision_groups": w["n_prime"], "max_len": w["l_max"],
                    "length_dist": f"lognormal({w['mu']}, {w['sigma']}), rho {w['rho']}",
                    "prompt_len": w["prompt"], "slots": w["slots"], "temperature": w["temperature"],
+                   "gemm": ("fp32-residual split-K partials reduce-added by TMA (split summation order not fixed)"
+                            if w.get("nondet_gemm") else "deterministic schedules"),
                    "parallelism": (f"dp{world} lockstep engines (NCCL per-iteration count allreduce, response gather)"
                                    if dp else f"dp{world} replicas"),
                    "l2": "inputs larger than L2 (weights + KV >> 126 MB)"},

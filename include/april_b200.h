@@ -91,7 +91,9 @@ typedef struct ab_engine_config {
   int32_t record_payload; /* keep token ids + behaviour logprobs on device    */
   uint64_t weight_seed;   /* transformer: N(0, weight_std) init seed          */
   float weight_std;
-  int32_t reserved[7];
+  int32_t nondeterministic_gemm; /* 1: fp32 residual GEMMs may split K with TMA reduce-add
+                                    (faster; split summation order not fixed run to run) */
+  int32_t reserved[6];
 } ab_engine_config;
 
 typedef struct ab_sample_desc {

@@ -44,7 +44,7 @@ class EngineConfigC(C.Structure):
                 ("max_prompt", C.c_int32), ("temperature", C.c_float), ("top_p", C.c_float),
                 ("greedy", C.c_int32), ("n_eos", C.c_int32), ("eos_ids", C.c_int32 * 8),
                 ("record_payload", C.c_int32), ("weight_seed", C.c_uint64), ("weight_std", C.c_float),
-                ("reserved", C.c_int32 * 7)]
+                ("nondeterministic_gemm", C.c_int32), ("reserved", C.c_int32 * 6)]
 
 
 class SampleDesc(C.Structure):

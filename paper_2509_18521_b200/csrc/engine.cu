@@ -643,7 +643,7 @@ static void submit(Engine& e, const ab_sample_desc* descs, int n) {
 }
 
 static void launch_iteration(Engine& e, int64_t run_iter, bool timed = false) {
-  e.launches += 2 + (e.model ? 5 + 9 * (int64_t)e.mcfg.n_layers : 1);
+  e.launches += 2 + (e.model ? 5 + 12 * (int64_t)e.mcfg.n_layers : 1);  // incl. the partitioned GEMM pairs
   {
     ScopedTimer t(e, timed, "admit", run_iter);
     k_admit<<<1, 256, 0, e.stream>>>(e.d);

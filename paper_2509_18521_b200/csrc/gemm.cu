@@ -38,7 +38,7 @@ constexpr int kThreads = 224;  // 7 warps: W producer, MMA, 4 epilogue, A produc
 constexpr int kMaxBN = 256;
 constexpr int kWBytes = kBM * kBK * 2;           // 16 KB weight tile per stage
 constexpr int kRingBytes = 192 * 1024;           // TMA ring, carved into stages per launch
-constexpr int kXchgBytes = 64 * 32 * 4;          // SwiGLU gate/up exchange
+constexpr int kXchgBytes = 16384;                // SwiGLU gate/up exchange, fp32 residual staging
 constexpr int kMaxStages = 12;
 constexpr int kTmemCols = 2 * kMaxBN;            // double-buffered accumulator
 constexpr int kSmem = 1024 + kRingBytes + kXchgBytes + 512;
@@ -116,6 +116,17 @@ __device__ __forceinline__ void tma_load_3d_pair(const CUtensorMap* map, uint32_
       "l"(reinterpret_cast<uint64_t>(map)), "r"(bar_cluster), "r"(x), "r"(y), "r"(z), "l"(policy)
       : "memory");
 }
+// fp32 tile in shared memory reduce-added into global memory by TMA (bulk-group completion)
+__device__ __forceinline__ void tma_reduce_add_2d(const CUtensorMap* map, const void* src, int x, int y) {
+  asm volatile("cp.reduce.async.bulk.tensor.2d.global.shared::cta.add.bulk_group [%0, {%2, %3}], [%1];" ::"l"(
+                   reinterpret_cast<uint64_t>(map)),
+               "r"(smem_u32(src)), "r"(x), "r"(y)
+               : "memory");
+  asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+}
+__device__ __forceinline__ void bulk_wait_read_all() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
+__device__ __forceinline__ void fence_proxy_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+
 __device__ __forceinline__ void mbar_arrive_cluster(uint32_t bar_cluster) {
   asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(bar_cluster) : "memory");
 }
@@ -187,7 +198,7 @@ __device__ __forceinline__ float4 ld_dsmem_f4(uint32_t addr) {
 //             `splits` consecutive ranks of a cluster reduces one tile, CS/splits tiles per
 //             cluster, one round).
 struct Sched {
-  int swap, pair, wn, an, splits, m_tiles, n_tiles, tiles, nk, stages, stage_bytes, w_bytes;
+  int swap, pair, red, wn, an, splits, m_tiles, n_tiles, tiles, units, nk, stages, stage_bytes, w_bytes;
 };
 
 __host__ __device__ inline Sched sched_from(int code, int rows, int N, int K) {
@@ -197,12 +208,14 @@ __host__ __device__ inline Sched sched_from(int code, int rows, int N, int K) {
   s.splits = (code >> 5) & 31;
   s.stages = (code >> 10) & 15;
   s.pair = (code >> 14) & 1;
+  s.red = (code >> 15) & 1;  // split-K partials reduce-added into the fp32 output by TMA (no cluster)
   // pair: one 256 x 256 tile per CTA pair; each CTA stages 128 activation + 128 weight rows
   s.wn = s.pair ? 256 : s.swap ? kBM : t;
   s.an = s.pair ? 256 : s.swap ? t : kBM;
   s.n_tiles = (N + s.wn - 1) / s.wn;
   s.m_tiles = (rows + s.an - 1) / s.an;
   s.tiles = s.n_tiles * s.m_tiles;
+  s.units = s.red ? s.tiles * s.splits : s.tiles;
   s.nk = K / kBK;
   // a stage holds two 64-deep k-blocks: [W kb0][W kb1][A kb0][A kb1], each slab rows x 128 B
   s.w_bytes = (s.pair ? 128 : s.wn) * kBK * 2;  // one weight slab
@@ -216,23 +229,31 @@ __host__ __device__ inline Sched sched_from(int code, int rows, int N, int K) {
 // overlaps the main loop of tile t+1); cluster split-K adds the partial park +
 // DSMEM reduction.  `cs` = cluster size of the launch, `ncl` = co-resident
 // clusters.  Returns the packed code (0 = no valid schedule).
-int choose_sched(int rows, int N, int K, int max_bn, int cs, int ncl, int force, int epi) {
+int choose_sched(int rows, int N, int K, int max_bn, int cs, int ncl, int force, int epi, bool pair_plan = false,
+                 double* est_us = nullptr, bool allow_red = false) {
   const int nk = K / kBK;
+  if (est_us) *est_us = 1e30;
   const int grid = cs * ncl;
-  auto pack = [&](int swap, int t, int sp, int pair = 0) {
+  auto pack = [&](int swap, int t, int sp, int pair = 0, int red = 0) {
     int lg = 0;
     while ((1 << lg) < t) ++lg;
     const int wn = pair ? 128 : swap ? kBM : t, an = pair ? 128 : swap ? t : kBM;
     // stages carry two 64-deep k-blocks (one 3-D TMA box per operand, 8-64 KB per operation)
     const int stages = std::min(kMaxStages, kRingBytes / ((wn * kBK * 2 + an * kBK * 2) * 2));
-    return swap | (lg << 1) | (sp << 5) | (stages << 10) | (pair << 14);
+    return swap | (lg << 1) | (sp << 5) | (stages << 10) | (pair << 14) | (red << 15);
   };
   if (force > 0 && (force & 0x40000000)) {  // a fixed code (tools/gemm_bench.py --sweep)
+    if (force & 0x8000) {  // reduce-added split-K (fp32 residual GEMMs, cluster of 1)
+      const int code = force & 0x3ff;
+      const int swap = code & 1, t = 1 << ((code >> 1) & 15), sp = (code >> 5) & 31;
+      if (cs != 1 || epi != kEpiAddF32 || sp < 1 || nk < 2 * sp || (!swap && N % 128)) return 0;
+      return pack(swap, t, sp, 0, 1);
+    }
     if (force & 0x4000) {  // CTA pair: a cluster of 2, no split
-      if (cs != 2 || (epi == kEpiSwiGLU && N % 256) || N % 128 || nk % 2) return 0;
+      if (!pair_plan || (epi == kEpiSwiGLU && N % 256) || N % 128 || nk % 2) return 0;
       return pack(0, 256, 1, 1);
     }
-    if (cs == 2) return 0;
+    if (pair_plan) return 0;
     const int code = force & 0x3ff;
     const int swap = code & 1, t = 1 << ((code >> 1) & 15), sp = (code >> 5) & 31;
     if (sp < 1 || sp > cs || (sp & (sp - 1))) return 0;
@@ -245,8 +266,8 @@ int choose_sched(int rows, int N, int K, int max_bn, int cs, int ncl, int force,
     return pack(swap, t, sp);
   }
   int best = 0;
-  if (cs == 2) {  // a pair plan: every row count runs the CTA-pair schedule
-    if (N % 128 || (epi == kEpiSwiGLU && N % 256) || nk % 2) return 0;
+  if (pair_plan) {  // a pair plan: every row count runs the CTA-pair schedule
+    if (cs != 2 || N % 128 || (epi == kEpiSwiGLU && N % 256) || nk % 2) return 0;
     // CTA pair (cta_group::2, 256 x 256 tile): per CTA and K block the same 128 x 256 x 64 MMA
     // as a 1-CTA 128 x 256 tile, but only 32 KB of operands instead of 48 KB
     return pack(0, 256, 1, 1);
@@ -272,8 +293,8 @@ int choose_sched(int rows, int N, int K, int max_bn, int cs, int ncl, int force,
       const double t_stage = std::max((wn + an) * 256.0 / 100e3, wn * an / 32.0 / 1965.0);
       const int live = std::min(an, rows);
       const double epi_cols = swap ? live : wn;
-      const double epi_rate = swap ? (epi == kEpiAddF32 ? 0.05 : epi == kEpiSwiGLU ? 0.06 : 0.03)
-                                   : (epi == kEpiAddF32 ? 0.13 : epi == kEpiSwiGLU ? 0.03 : 0.02);
+      // (the fp32 residual epilogue stages the tile in shared memory and reduce-adds it by TMA)
+      const double epi_rate = swap ? (epi == kEpiSwiGLU ? 0.06 : 0.03) : (epi == kEpiSwiGLU ? 0.03 : 0.02);
       for (int sp = 1; sp <= cs; sp <<= 1) {
         if (sp > 1 && ((int64_t)tiles * sp > (int64_t)ncl * cs || nk < 4 * sp)) continue;
         const double waves = std::ceil((double)tiles * sp / grid);
@@ -284,6 +305,23 @@ int choose_sched(int rows, int N, int K, int max_bn, int cs, int ncl, int force,
         if (us < best_us) {
           best_us = us;
           best = pack(swap, t, sp);
+          if (est_us) *est_us = us;
+        }
+      }
+      // reduce-added split-K: no cluster, any number of splits, partials summed by TMA in L2
+      // (summation order across splits is not fixed: only offered to non-deterministic plans)
+      if (allow_red && cs == 1 && epi == kEpiAddF32) {
+        for (int sp = 2; sp <= 8; sp <<= 1) {
+          if (nk < 4 * sp) continue;
+          const double waves = std::ceil((double)tiles * sp / grid);
+          const double main_us = std::ceil(nk / 2.0 / sp) * t_stage;
+          const double e = epi_rate * epi_cols;
+          const double us = waves * std::max(main_us, e) + e + 0.5;
+          if (us < best_us) {
+            best_us = us;
+            best = pack(swap, t, sp, 0, 1);
+            if (est_us) *est_us = us;
+          }
         }
       }
     }
@@ -311,7 +349,8 @@ template <int EPI, bool kPair>
 __global__ void __launch_bounds__(kThreads, 1)
     k_gemm_tc(const __grid_constant__ CUtensorMap tw3, const __grid_constant__ CUtensorMap tw3_256,
               const __grid_constant__ CUtensorMap ta3_32, const __grid_constant__ CUtensorMap ta3_64,
-              const __grid_constant__ CUtensorMap ta3, const __grid_constant__ CUtensorMap ta3_256, int N, int K,
+              const __grid_constant__ CUtensorMap ta3, const __grid_constant__ CUtensorMap ta3_256,
+              const __grid_constant__ CUtensorMap tx_ns, const __grid_constant__ CUtensorMap tx_sw, int N, int K,
               int M_cap, const int* __restrict__ rows_dev, const int* __restrict__ stop_dev, void* __restrict__ out,
               int64_t ldo, const __nv_bfloat16* __restrict__ bias, const int* __restrict__ sched_tab, int trace) {
   if (threadIdx.x == 0) trace_mark(trace, 0);
@@ -322,7 +361,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (code == 0) return;
   const Sched sc = sched_from(code, rows, N, K);
   const int cs = (int)cluster_nctarank();
-  const bool split = sc.splits > 1;
+  const bool split = sc.splits > 1 && !sc.red;  // cluster split-K
   constexpr bool pair = kPair;  // CTA pair (cta_group::2): even cluster rank leads
   if (kPair != (sc.pair != 0)) return;  // the host never builds such a table
   const int crank = (split || pair) ? (int)cluster_ctarank() : 0;
@@ -335,7 +374,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int u_first = split ? ((int)blockIdx.x / cs) * per_cl + crank / sc.splits
                       : pair ? (int)blockIdx.x / 2 : (int)blockIdx.x;
   const int u_step = split ? ((int)gridDim.x / cs) * per_cl : pair ? (int)gridDim.x / 2 : (int)gridDim.x;
-  if ((split || pair) ? ((int)blockIdx.x / cs) * per_cl >= sc.tiles : u_first >= sc.tiles)
+  const int n_units = sc.units;  // tiles, or (tile, split) pairs for reduce-added split-K
+  if ((split || pair) ? ((int)blockIdx.x / cs) * per_cl >= sc.tiles : u_first >= n_units)
     return;  // uniform per cluster
 
   // the 3-D TMA views this schedule loads from
@@ -385,13 +425,24 @@ __global__ void __launch_bounds__(kThreads, 1)
   const uint32_t leader = (uint32_t)(crank & ~1);
   if (threadIdx.x == 0) trace_mark(trace, 1);
 
+  // A unit's k-block pairs are visited in a rotated order (start offset spread by row tile):
+  // the CTAs that share a weight tile then read different k slices of it at any moment instead
+  // of hammering the same L2 lines in lockstep.  The summation order of a unit is fixed by its
+  // coordinates, so results stay deterministic.
+  int rot = 0, npairs = 0;
   auto unit_coords = [&](int u, int& n0, int& m0, int& kb0, int& kb1) {
+    const int z = sc.red ? u % sc.splits : rank;  // K slice
+    if (sc.red) u /= sc.splits;
     const int nt = u / sc.m_tiles;
+    const int mt = u - nt * sc.m_tiles;
     n0 = nt * sc.wn;
-    m0 = (u - nt * sc.m_tiles) * sc.an;
-    kb0 = 2 * (int)(((int64_t)(sc.nk / 2) * rank) / sc.splits);  // stages are k-block pairs
-    kb1 = 2 * (int)(((int64_t)(sc.nk / 2) * (rank + 1)) / sc.splits);
+    m0 = mt * sc.an;
+    kb0 = 2 * (int)(((int64_t)(sc.nk / 2) * z) / sc.splits);  // stages are k-block pairs
+    kb1 = 2 * (int)(((int64_t)(sc.nk / 2) * (z + 1)) / sc.splits);
+    npairs = (kb1 - kb0) / 2;
+    rot = npairs > 0 ? (int)(((int64_t)mt * npairs) / sc.m_tiles) : 0;
   };
+  auto kb_at = [&](int kb0, int i) { return kb0 + 2 * ((i + rot) % npairs); };
 
   if (warp == 0 || warp == 6) {
     // two producer threads in different warps: warp 0 issues the weight box (and arms the stage's
@@ -410,7 +461,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol_a));
       int g = 0;
       const uint32_t full_lead = pair ? map_rank(smem_u32(full), leader) : 0u;
-      for (int u = u_first; u < sc.tiles; u += u_step) {
+      for (int u = u_first; u < n_units; u += u_step) {
         int n0, m0, kb0, kb1;
         unit_coords(u, n0, m0, kb0, kb1);
         if (pair) {
@@ -426,7 +477,8 @@ __global__ void __launch_bounds__(kThreads, 1)
           boxes(0, a0, w0);
           boxes(1, a1, w1);
           const uint32_t tx = (uint32_t)((w0 + w1 + a0 + a1) * 2 * kWBytes);
-          for (int kb = kb0; kb < kb1; kb += 2, ++g) {
+          for (int i = 0; i < npairs; ++i, ++g) {
+            const int kb = kb_at(kb0, i);
             const int s = g % nst;
             mbar_wait(&empty[s], ((g / nst) & 1) ^ 1);
             uint8_t* st = ring + s * sc.stage_bytes;
@@ -445,7 +497,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         // one 3-D box per operand per stage: weights [2][wn][64], activations [2][an][64]
         // (rows past N / M_cap are zero-filled, the full box is counted)
         const uint32_t tx = (uint32_t)sc.stage_bytes;
-        for (int kb = kb0; kb < kb1; kb += 2, ++g) {
+        for (int i = 0; i < npairs; ++i, ++g) {
+          const int kb = kb_at(kb0, i);
           const int s = g % nst;
           const uint32_t ph = (g / nst) & 1;
           mbar_wait(&empty[s], ph ^ 1);
@@ -475,14 +528,14 @@ __global__ void __launch_bounds__(kThreads, 1)
       const uint16_t mask = (uint16_t)(3u << leader);
       const uint32_t ring_s = smem_u32(ring);
       int g = 0, t = 0;
-      for (int u = u_first; u < sc.tiles; u += u_step, ++t) {
+      for (int u = u_first; u < n_units; u += u_step, ++t) {
         int n0, m0, kb0, kb1;
         unit_coords(u, n0, m0, kb0, kb1);
         const int acc = t & 1;
         mbar_wait(&tmem_empty[acc], ((t >> 1) & 1) ^ 1);
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
         const uint32_t d = tmem + (uint32_t)(acc * kMaxBN);
-        for (int kb = kb0; kb < kb1; kb += 2, ++g) {
+        for (int i = 0; i < npairs; ++i, ++g) {
           const int s = g % nst;
           mbar_wait(&full[s], (g / nst) & 1);
           asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
@@ -493,7 +546,7 @@ __global__ void __launch_bounds__(kThreads, 1)
               const uint64_t da = umma_desc(sa + h * kWBytes), db = umma_desc(sw + h * kWBytes);
 #pragma unroll
               for (int k = 0; k < kBK / 16; ++k)
-                umma_bf16_pair(d, da + 2 * k, db + 2 * k, idesc, (kb != kb0 || h != 0 || k != 0) ? 1u : 0u);
+                umma_bf16_pair(d, da + 2 * k, db + 2 * k, idesc, (i != 0 || h != 0 || k != 0) ? 1u : 0u);
             }
           }
           umma_commit_pair(&empty[s], mask);
@@ -509,7 +562,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(un >> 3) << 17) | ((uint32_t)(um >> 4) << 24);
       const uint32_t ring_s = smem_u32(ring);
       int g = 0, t = 0;
-      for (int u = u_first; u < sc.tiles; u += u_step, ++t) {
+      for (int u = u_first; u < n_units; u += u_step, ++t) {
         int n0, m0, kb0, kb1;
         unit_coords(u, n0, m0, kb0, kb1);
         const int acc = t & 1;
@@ -517,7 +570,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
         const uint32_t d = tmem + (uint32_t)(acc * kMaxBN);
         const uint32_t a_slab = (uint32_t)(sc.an * kBK * 2);
-        for (int kb = kb0; kb < kb1; kb += 2, ++g) {
+        for (int i = 0; i < npairs; ++i, ++g) {
           const int s = g % nst;
           mbar_wait(&full[s], (g / nst) & 1);
           asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
@@ -530,7 +583,7 @@ __global__ void __launch_bounds__(kThreads, 1)
               const uint64_t da = umma_desc(sc.swap ? sw : sa), db = umma_desc(sc.swap ? sa : sw);
 #pragma unroll
               for (int k = 0; k < kBK / 16; ++k)  // +32 bytes along K inside the swizzle atom
-                umma_bf16(d, da + 2 * k, db + 2 * k, idesc, (kb != kb0 || h != 0 || k != 0) ? 1u : 0u);
+                umma_bf16(d, da + 2 * k, db + 2 * k, idesc, (i != 0 || h != 0 || k != 0) ? 1u : 0u);
             }
           }
           umma_commit(&empty[s]);
@@ -671,7 +724,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       cluster_sync_all();  // no rank leaves while others still read its parked partial
     };
     int t = 0;
-    for (int u = u_first; u < sc.tiles; u += u_step, ++t) {
+    for (int u = u_first; u < n_units; u += u_step, ++t) {
       int n0, m0, kb0, kb1;
       unit_coords(u, n0, m0, kb0, kb1);
       if (pair) m0 += 128 * prank;  // this CTA's TMEM holds rows [m0, m0 + 128) of the pair's tile
@@ -722,6 +775,24 @@ __global__ void __launch_bounds__(kThreads, 1)
               }
             }
           }
+        } else if constexpr (EPI == kEpiAddF32) {
+          // residual add: stage [128 rows][32 fp32] (128-byte swizzle) and reduce-add it into x by
+          // TMA; rows past the live count stage zeros (x + 0 leaves them unchanged)
+          float* stg = xchg;
+#pragma unroll 1
+          for (int c0 = 0; c0 < ncols; c0 += 32) {
+            float v[32];
+            fetch(c0, v);
+            if (threadIdx.x == 64) bulk_wait_read_all();  // the previous chunk has left the staging tile
+            asm volatile("bar.sync 1, 128;" ::: "memory");
+#pragma unroll
+            for (int q = 0; q < 8; ++q)
+              *reinterpret_cast<float4*>(stg + lrow * 32 + ((q ^ (lrow & 7)) << 2)) =
+                  mine ? make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]) : make_float4(0.f, 0.f, 0.f, 0.f);
+            fence_proxy_async_smem();
+            asm volatile("bar.sync 1, 128;" ::: "memory");
+            if (threadIdx.x == 64) tma_reduce_add_2d(&tx_ns, stg, n0 + c0, m0);
+          }
         } else {
 #pragma unroll 1
           for (int c0 = c_first; c0 < ncols; c0 += c_step) {
@@ -748,13 +819,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             } else {
               float4* dst = reinterpret_cast<float4*>(reinterpret_cast<float*>(out) + (int64_t)m * ldo + n);
               if constexpr (EPI == kEpiAddF32) {
-                float4 old[8];
-#pragma unroll
-                for (int q = 0; q < 8; ++q) old[q] = __ldcg(dst + q);
-#pragma unroll
-                for (int q = 0; q < 8; ++q)
-                  dst[q] = make_float4(old[q].x + v[4 * q], old[q].y + v[4 * q + 1], old[q].z + v[4 * q + 2],
-                                       old[q].w + v[4 * q + 3]);
+                // handled by the TMA reduce-add path below (never reached)
               } else {
 #pragma unroll
                 for (int q = 0; q < 8; ++q) dst[q] = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
@@ -793,16 +858,16 @@ __global__ void __launch_bounds__(kThreads, 1)
             float v[32];
             fetch(c0, v);
             if constexpr (EPI == kEpiAddF32) {
-              // residual add: all 32 loads in flight before any store (clamped rows: unconditional loads)
-              float* o = reinterpret_cast<float*>(out);
-              float old[32];
+              // residual add: stage [32 rows][128 fp32] and reduce-add it into x by TMA (rows past
+              // the live count stage zeros)
+              float* stg = xchg;
+              if (threadIdx.x == 64) bulk_wait_read_all();
+              asm volatile("bar.sync 1, 128;" ::: "memory");
 #pragma unroll
-              for (int c = 0; c < 32; ++c) old[c] = __ldcg(o + (int64_t)min(m0 + c0 + c, rows - 1) * ldo + n);
-#pragma unroll
-              for (int c = 0; c < 32; ++c) {
-                const int m = m0 + c0 + c;
-                if (m < rows) o[(int64_t)m * ldo + n] = old[c] + v[c];
-              }
+              for (int c = 0; c < 32; ++c) stg[c * 128 + lrow] = (m0 + c0 + c < rows) ? v[c] : 0.f;
+              fence_proxy_async_smem();
+              asm volatile("bar.sync 1, 128;" ::: "memory");
+              if (threadIdx.x == 64) tma_reduce_add_2d(&tx_sw, stg, n0, m0 + c0);
             } else {
 #pragma unroll
               for (int c = 0; c < 32; ++c) {
@@ -839,7 +904,10 @@ __global__ void __launch_bounds__(kThreads, 1)
     cluster_sync_all();
     cluster_sync_all();
   }
-  if (threadIdx.x == 64) trace_mark(trace, 6);
+  if (threadIdx.x == 64) {
+    if constexpr (EPI == kEpiAddF32) bulk_wait_read_all();
+    trace_mark(trace, 6);
+  }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
   if (pair) cluster_sync_all();  // both CTAs of the pair are done with the pair's TMEM
@@ -882,6 +950,20 @@ EncodeFn encode_fn() {
   return fn;
 }
 
+// fp32 row-major [rows, cols] (leading dimension ld elements), box {box_cols, box_rows}
+void make_map_f32(CUtensorMap* m, void* ptr, int64_t rows, int64_t cols, int64_t ld, int box_cols, int box_rows,
+                  bool swizzle128) {
+  cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
+  cuuint64_t strides[1] = {(cuuint64_t)(ld * 4)};
+  cuuint32_t box[2] = {(cuuint32_t)box_cols, (cuuint32_t)box_rows};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = encode_fn()(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, ptr, dims, strides, box, estr,
+                           CU_TENSOR_MAP_INTERLEAVE_NONE,
+                           swizzle128 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_NONE,
+                           CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  AB_REQUIRE(r == CUDA_SUCCESS, AB_ERR_CUDA, "cuTensorMapEncodeTiled (fp32) failed (" + std::to_string((int)r) + ")");
+}
+
 // 3-D view [K/64][rows][64] of a row-major [rows, K] bf16 matrix, box {64, 128, 2}: two
 // consecutive 64-deep k-blocks of 128 rows in one TMA operation (128-byte swizzle per row).
 void make_map3(CUtensorMap* m, const void* ptr, int64_t rows, int64_t K, int64_t ld, int box_rows = 128) {
@@ -909,11 +991,11 @@ void set_attr() {
 
 // co-resident clusters of `cs` persistent CTAs (one CTA per SM)
 template <int EPI>
-int max_clusters(int cs) {
+int max_clusters(int cs, bool pair) {
   static std::mutex mu;
   static std::map<int, int> memo;
   std::lock_guard<std::mutex> lock(mu);
-  auto it = memo.find(cs);
+  auto it = memo.find(cs * 2 + (pair ? 1 : 0));
   if (it != memo.end()) return it->second;
   set_attr<EPI>();
   int dev = 0, sms = 0;
@@ -932,22 +1014,22 @@ int max_clusters(int cs) {
     at[0].val.clusterDim.z = 1;
     cfg.attrs = at;
     cfg.numAttrs = 1;
-    if (cs == 2)
+    if (pair)
       AB_CUDA(cudaOccupancyMaxActiveClusters(&n, k_gemm_tc<EPI, true>, &cfg));
     else
       AB_CUDA(cudaOccupancyMaxActiveClusters(&n, k_gemm_tc<EPI, false>, &cfg));
     AB_REQUIRE(n >= 1, AB_ERR_CONFIG, "GEMM cluster size does not fit on this device");
   }
-  memo[cs] = n;
+  memo[cs * 2 + (pair ? 1 : 0)] = n;
   return n;
 }
 
-int max_clusters_epi(int epi, int cs) {
+int max_clusters_epi(int epi, int cs, bool pair = false) {
   switch (epi) {
-    case kEpiBF16: return max_clusters<kEpiBF16>(cs);
-    case kEpiF32: return max_clusters<kEpiF32>(cs);
-    case kEpiAddF32: return max_clusters<kEpiAddF32>(cs);
-    default: return max_clusters<kEpiSwiGLU>(cs);
+    case kEpiBF16: return max_clusters<kEpiBF16>(cs, pair);
+    case kEpiF32: return max_clusters<kEpiF32>(cs, pair);
+    case kEpiAddF32: return max_clusters<kEpiAddF32>(cs, pair);
+    default: return max_clusters<kEpiSwiGLU>(cs, pair);
   }
 }
 
@@ -966,11 +1048,11 @@ void launch_t(const GemmPlan& p, cudaStream_t s) {
   at[0].val.clusterDim.z = 1;
   cfg.attrs = at;
   cfg.numAttrs = 1;
-  if (p.cluster == 2)
-    AB_CUDA(cudaLaunchKernelEx(&cfg, k_gemm_tc<EPI, true>, p.tw3, p.tw3_256, p.ta3_32, p.ta3_64, p.ta3, p.ta3_256, p.N, p.K, p.M_cap, p.rows_dev, p.stop_dev,
+  if (p.pair)
+    AB_CUDA(cudaLaunchKernelEx(&cfg, k_gemm_tc<EPI, true>, p.tw3, p.tw3_256, p.ta3_32, p.ta3_64, p.ta3, p.ta3_256, p.tx_ns, p.tx_sw, p.N, p.K, p.M_cap, p.rows_dev, p.stop_dev,
                                p.out, p.ldo, p.bias, p.sched, g_trace_on));
   else
-    AB_CUDA(cudaLaunchKernelEx(&cfg, k_gemm_tc<EPI, false>, p.tw3, p.tw3_256, p.ta3_32, p.ta3_64, p.ta3, p.ta3_256, p.N, p.K, p.M_cap, p.rows_dev, p.stop_dev,
+    AB_CUDA(cudaLaunchKernelEx(&cfg, k_gemm_tc<EPI, false>, p.tw3, p.tw3_256, p.ta3_32, p.ta3_64, p.ta3, p.ta3_256, p.tx_ns, p.tx_sw, p.N, p.K, p.M_cap, p.rows_dev, p.stop_dev,
                                p.out, p.ldo, p.bias, p.sched, g_trace_on));
 }
 
@@ -978,13 +1060,15 @@ void launch_t(const GemmPlan& p, cudaStream_t s) {
 
 void gemm_plan(GemmPlan& p, const __nv_bfloat16* W, int N, int K, const __nv_bfloat16* A, int M_cap, int64_t lda,
                int BN, int epi, void* out, int64_t ldo, const __nv_bfloat16* bias, const int* rows_dev,
-               const int* stop_dev, int cluster) {
+               const int* stop_dev, int cluster, bool pair) {
   AB_REQUIRE(K % (2 * kBK) == 0, AB_ERR_CONFIG, "GEMM K must be a multiple of 128");
   AB_REQUIRE(cluster == 1 || cluster == 2 || cluster == 4 || cluster == 8, AB_ERR_CONFIG,
              "GEMM split-K cluster must be 1, 2, 4 or 8");
   AB_REQUIRE(N % kBM == 0, AB_ERR_CONFIG, "GEMM N must be a multiple of 128");
   AB_REQUIRE(BN == 32 || BN == 64 || BN == 128 || BN == 256, AB_ERR_CONFIG, "GEMM BN must be 32/64/128/256");
+  AB_REQUIRE(!pair || cluster == 2, AB_ERR_CONFIG, "a CTA-pair plan runs in clusters of 2");
   p.cluster = cluster;
+  p.pair = pair;
   p.N = N;
   p.K = K;
   p.M_cap = M_cap;
@@ -1002,13 +1086,20 @@ void gemm_plan(GemmPlan& p, const __nv_bfloat16* W, int N, int K, const __nv_bfl
   make_map3(&p.ta3_64, A, M_cap, K, lda, 64);
   make_map3(&p.ta3, A, M_cap, K, lda, 128);
   make_map3(&p.ta3_256, A, M_cap, K, lda, 256);
+  if (epi == kEpiAddF32) {  // the fp32 residual the epilogue reduce-adds into
+    make_map_f32(&p.tx_ns, out, M_cap, N, ldo, 32, 128, true);
+    make_map_f32(&p.tx_sw, out, M_cap, N, ldo, 128, 32, false);
+  } else {
+    p.tx_ns = p.tw3;  // unused
+    p.tx_sw = p.tw3;
+  }
   gemm_set_schedule(p, 0);
 }
 
 void gemm_set_schedule(GemmPlan& p, int force) {
   // launch geometry: clusters of p.cluster CTAs, never more than the largest possible tile count needs
   const int cs = p.cluster;
-  const int ncl_max = max_clusters_epi(p.epi, cs);
+  const int ncl_max = max_clusters_epi(p.epi, cs, p.pair);
   const int64_t max_tiles = (int64_t)ceil_div(p.N, kBM) * ceil_div(p.M_cap, 32);
   const int ncl = (int)std::min<int64_t>(ncl_max, cs > 1 ? max_tiles : ceil_div(max_tiles, 1));
   p.grid = ncl * cs;
@@ -1018,7 +1109,8 @@ void gemm_set_schedule(GemmPlan& p, int force) {
   static std::map<std::tuple<int, int, int, int, int, int, int, int>, int*> cache;
   int dev = 0;
   AB_CUDA(cudaGetDevice(&dev));
-  const auto key = std::make_tuple(p.N, p.K, p.M_cap, p.BN, cs, force, p.epi, ncl * 16 + dev);
+  const auto key = std::make_tuple(p.N, p.K, p.M_cap, p.BN, cs * 4 + (p.pair ? 1 : 0) + (p.nondet ? 2 : 0), force,
+                                   p.epi, ncl * 16 + dev);
   std::lock_guard<std::mutex> lock(mu);
   auto it = cache.find(key);
   if (it != cache.end()) {
@@ -1026,12 +1118,35 @@ void gemm_set_schedule(GemmPlan& p, int force) {
     return;
   }
   std::vector<int> tab(p.M_cap + 1, 0);
-  for (int r = 1; r <= p.M_cap; ++r) tab[r] = choose_sched(r, p.N, p.K, p.BN, cs, ncl, force, p.epi);
+  for (int r = 1; r <= p.M_cap; ++r)
+    tab[r] = choose_sched(r, p.N, p.K, p.BN, cs, ncl, force, p.epi, p.pair, nullptr, p.nondet);
   int* d = nullptr;
   AB_CUDA(cudaMalloc(&d, sizeof(int) * tab.size()));
   AB_CUDA(cudaMemcpy(d, tab.data(), sizeof(int) * tab.size(), cudaMemcpyHostToDevice));
   cache[key] = d;
   p.sched = d;
+}
+
+void gemm_partition(GemmPlan& a, GemmPlan& b) {
+  AB_REQUIRE(a.N == b.N && a.K == b.K && a.M_cap == b.M_cap && a.epi == b.epi && !a.pair && !b.pair, AB_ERR_CONFIG,
+             "partitioned GEMM plans must compute the same product");
+  std::vector<int> ta(a.M_cap + 1, 0), tb(a.M_cap + 1, 0);
+  for (int r = 1; r <= a.M_cap; ++r) {
+    double ea = 0, eb = 0;
+    const int ca = choose_sched(r, a.N, a.K, a.BN, a.cluster, a.grid / a.cluster, 0, a.epi, false, &ea, a.nondet);
+    const int cb = choose_sched(r, b.N, b.K, b.BN, b.cluster, b.grid / b.cluster, 0, b.epi, false, &eb, b.nondet);
+    if (cb != 0 && (ca == 0 || eb < ea))
+      tb[r] = cb;
+    else
+      ta[r] = ca;
+  }
+  for (auto* pt : {&a, &b}) {
+    int* d = nullptr;
+    const std::vector<int>& tab = pt == &a ? ta : tb;
+    AB_CUDA(cudaMalloc(&d, sizeof(int) * tab.size()));
+    AB_CUDA(cudaMemcpy(d, tab.data(), sizeof(int) * tab.size(), cudaMemcpyHostToDevice));
+    pt->sched = d;
+  }
 }
 
 void make_tmap_bf16(CUtensorMap* m, const void* ptr, int64_t rows, int64_t cols, int64_t ld, int box_cols,
@@ -1066,13 +1181,19 @@ extern "C" int ab_debug_gemm_time(const void* W, const void* A, void* out, const
     // epi bit 4: cluster split-K allowed (cluster of 8); bit 5: automatic schedule (BN = max activation
     // tile); bit 6: forced no-swap schedule with BN weight rows; bit 7: BN is a fixed schedule code;
     // else forced swap-AB with BN activation rows
-    const int max_splits = (epi & 256) ? 2 : (epi & 16) ? 8 : 1;  // bit 8: a CTA-pair plan (cluster of 2)
+    // bit 8: a CTA-pair plan (cluster of 2); bit 9: a plain cluster-of-2 plan (split-K <= 2);
+    // bit 10: a cluster-of-1 plan that may split K with TMA reduce-add (non-deterministic)
+    const int max_splits = (epi & (256 | 512)) ? 2 : (epi & 16) ? 8 : 1;
+    const bool pair_plan = (epi & 256) != 0;
+    const bool nondet = (epi & 1024) != 0;
     const int force = (epi & 128) ? (0x40000000 | BN) : (epi & 32) ? 0 : (epi & 64) ? -BN : BN;
     epi &= 15;
     if (!flush) AB_CUDA(cudaMalloc(&flush, size_t(256) << 20));
     ab::GemmPlan p;
     ab::gemm_plan(p, (const __nv_bfloat16*)W, N, K, (const __nv_bfloat16*)A, M, K, (force > 0 && (force & 0x40000000)) ? 256 : BN, epi, out,
-                  epi == ab::kEpiSwiGLU ? N / 2 : N, (const __nv_bfloat16*)bias, nullptr, nullptr, max_splits);
+                  epi == ab::kEpiSwiGLU ? N / 2 : N, (const __nv_bfloat16*)bias, nullptr, nullptr, max_splits,
+                  pair_plan);
+    p.nondet = nondet;
     ab::gemm_set_schedule(p, force);
     ab::gemm_launch(p, 0);  // warm: kernel attributes, TMA descriptors
     std::vector<float> t(reps);
@@ -1106,12 +1227,18 @@ extern "C" int ab_debug_gemm(const void* W, const void* A, void* out, const void
     // epi bit 4: cluster split-K allowed (cluster of 8); bit 5: automatic schedule (BN = max activation
     // tile); bit 6: forced no-swap schedule with BN weight rows; bit 7: BN is a fixed schedule code;
     // else forced swap-AB with BN activation rows
-    const int max_splits = (epi & 256) ? 2 : (epi & 16) ? 8 : 1;  // bit 8: a CTA-pair plan (cluster of 2)
+    // bit 8: a CTA-pair plan (cluster of 2); bit 9: a plain cluster-of-2 plan (split-K <= 2);
+    // bit 10: a cluster-of-1 plan that may split K with TMA reduce-add (non-deterministic)
+    const int max_splits = (epi & (256 | 512)) ? 2 : (epi & 16) ? 8 : 1;
+    const bool pair_plan = (epi & 256) != 0;
+    const bool nondet = (epi & 1024) != 0;
     const int force = (epi & 128) ? (0x40000000 | BN) : (epi & 32) ? 0 : (epi & 64) ? -BN : BN;
     epi &= 15;
     ab::GemmPlan p;
     ab::gemm_plan(p, (const __nv_bfloat16*)W, N, K, (const __nv_bfloat16*)A, M, K, (force > 0 && (force & 0x40000000)) ? 256 : BN, epi, out,
-                  epi == ab::kEpiSwiGLU ? N / 2 : N, (const __nv_bfloat16*)bias, nullptr, nullptr, max_splits);
+                  epi == ab::kEpiSwiGLU ? N / 2 : N, (const __nv_bfloat16*)bias, nullptr, nullptr, max_splits,
+                  pair_plan);
+    p.nondet = nondet;
     ab::gemm_set_schedule(p, force);
     ab::gemm_launch(p, 0);
     AB_CUDA(cudaGetLastError());
@@ -1161,5 +1288,6 @@ extern "C" int ab_debug_gemm_clusters(int cs, int* out) {
 // Debug / tests (no GPU needed): the packed schedule the cost model picks for `rows` live rows
 // (cs = cluster size, ncl = co-resident clusters, force as GemmPlan::force).
 extern "C" int ab_debug_gemm_sched(int N, int K, int rows, int max_bn, int cs, int ncl, int force, int epi) {
-  return ab::choose_sched(rows, N, K, max_bn, cs, ncl, force, epi);
+  // epi bit 8: a CTA-pair plan
+  return ab::choose_sched(rows, N, K, max_bn, cs, ncl, force, epi & 15, (epi & 256) != 0);
 }

@@ -24,6 +24,7 @@ struct GemmPlan {
   // 3-D TMA views [K/64][rows][64] (128-byte swizzle): one operation = two 64-deep k-blocks
   CUtensorMap tw3, tw3_256;                 // weights [N, K]: 128- / 256-row boxes
   CUtensorMap ta3_32, ta3_64, ta3, ta3_256;  // activations [M_cap, K]: 32- / 64- / 128- / 256-row boxes
+  CUtensorMap tx_ns, tx_sw;                  // fp32 residual output: {32 x 128} swizzled / {128 x 32} boxes
   int N = 0, K = 0, M_cap = 0, BN = 0, epi = 0;  // BN: largest activation tile the kernel may pick
   void* out = nullptr;
   int64_t ldo = 0;
@@ -33,6 +34,8 @@ struct GemmPlan {
   // deterministic split-K inside a thread-block cluster of `cluster` CTAs (1 = none):
   // the schedule table picks split = cluster (one tile per cluster) or none per row count
   int cluster = 1;
+  bool pair = false;    // CTA-pair plan (cta_group::2, cluster of 2)
+  bool nondet = false;  // fp32 residual plans may split K with TMA reduce-add (order not fixed)
   int grid = 0;  // persistent CTAs (a multiple of cluster)
   // tests: > 0 forces swap-AB with exactly `force` activation rows per tile, < 0 forces the
   // no-swap schedule with -force weight rows per tile, 0 = on-device choice
@@ -42,7 +45,11 @@ struct GemmPlan {
 
 void gemm_plan(GemmPlan& p, const __nv_bfloat16* W, int N, int K, const __nv_bfloat16* A, int M_cap, int64_t lda,
                int BN, int epi, void* out, int64_t ldo, const __nv_bfloat16* bias, const int* rows_dev,
-               const int* stop_dev, int cluster = 1);
+               const int* stop_dev, int cluster = 1, bool pair = false);
+// Split the row range between two plans of the same product (e.g. a cluster-8 split-K plan and a
+// cluster-2 plan): each row count runs on the plan the cost model expects to be faster, the other
+// launch exits at once.  Both plans are launched every time.
+void gemm_partition(GemmPlan& a, GemmPlan& b);
 void gemm_launch(const GemmPlan& p, cudaStream_t s);
 // Rebuild the plan's schedule table (force: see GemmPlan::force).
 void gemm_set_schedule(GemmPlan& p, int force);

@@ -36,6 +36,9 @@ struct Model {
   int max_splits = 1, chunk = 256;
   struct Plans {
     GemmPlan qkv, o, gu, down;
+    // decode only: the same QKV / O / down products on clusters of 2 (148 CTAs, split-K <= 2);
+    // gemm_partition gives each row count to the faster of the pair of plans
+    GemmPlan qkv2, o2, down2;
   };
   std::vector<Plans> dec, pf;
   GemmPlan lm_dec;
@@ -234,8 +237,24 @@ Model* model_create(Engine& e) {
               8);
     gemm_plan(d.o, w.wo, m.d, m.qd, M->attn, M->S, m.qd, bn_dec, kEpiAddF32, M->x, m.d, nullptr, b, stop, 8);
     gemm_plan(d.gu, w.wgu, 2 * m.f, m.d, M->xn, M->S, m.d, bn_dec, kEpiSwiGLU, M->hbuf, m.f, nullptr, b, stop,
-              2);
+              2, true);
     gemm_plan(d.down, w.wd, m.d, m.f, M->hbuf, M->S, m.f, bn_dec, kEpiAddF32, M->x, m.d, nullptr, b, stop, 8);
+    gemm_plan(d.qkv2, w.wqkv, m.qkv_dim, m.d, M->xn, M->S, m.d, bn_dec, kEpiBF16, M->qkv, m.qkv_dim, w.bqkv, b,
+              stop, 2);
+    // fp32 residual GEMMs: the second plan is either a cluster-of-2 plan (deterministic) or, when
+    // the engine allows it, a cluster-of-1 plan whose split-K partials are reduce-added by TMA
+    const bool nd = ec.nondeterministic_gemm != 0;
+    gemm_plan(d.o2, w.wo, m.d, m.qd, M->attn, M->S, m.qd, bn_dec, kEpiAddF32, M->x, m.d, nullptr, b, stop, nd ? 1 : 2);
+    gemm_plan(d.down2, w.wd, m.d, m.f, M->hbuf, M->S, m.f, bn_dec, kEpiAddF32, M->x, m.d, nullptr, b, stop,
+              nd ? 1 : 2);
+    if (nd) {
+      d.o2.nondet = d.down2.nondet = true;
+      gemm_set_schedule(d.o2, 0);
+      gemm_set_schedule(d.down2, 0);
+    }
+    gemm_partition(d.qkv, d.qkv2);
+    gemm_partition(d.o, d.o2);
+    gemm_partition(d.down, d.down2);
     gemm_plan(p.qkv, w.wqkv, m.qkv_dim, m.d, M->xn, M->M_pf, m.d, 256, kEpiBF16, M->qkv, m.qkv_dim, w.bqkv,
               M->pf_rows, nullptr);
     gemm_plan(p.o, w.wo, m.d, m.qd, M->attn, M->M_pf, m.qd, 256, kEpiAddF32, M->x, m.d, nullptr, M->pf_rows,
@@ -247,7 +266,7 @@ Model* model_create(Engine& e) {
     M->dec.push_back(d);
     M->pf.push_back(p);
   }
-  gemm_plan(M->lm_dec, M->lm_head, m.V, m.d, M->xn, M->S, m.d, bn_dec, kEpiF32, M->logits, m.V, nullptr, b, stop, 2);
+  gemm_plan(M->lm_dec, M->lm_head, m.V, m.d, M->xn, M->S, m.d, bn_dec, kEpiF32, M->logits, m.V, nullptr, b, stop, 2, true);
   M->inv_temp = ec.greedy ? 1.f / std::max(ec.temperature, 1e-6f) : 1.f / ec.temperature;
   if (ec.temperature <= 0.f) M->inv_temp = 1.f;
   AB_CUDA(cudaStreamSynchronize(s));
@@ -419,6 +438,7 @@ void model_iteration(Engine& e, int64_t run_iter, bool timed) {
     {
       ScopedTimer t(e, timed, "gemm_qkv", run_iter);
       gemm_launch(p.qkv, s);
+      gemm_launch(p.qkv2, s);
     }
     {
       ScopedTimer t(e, timed, "rope_kv", run_iter);
@@ -432,6 +452,7 @@ void model_iteration(Engine& e, int64_t run_iter, bool timed) {
     {
       ScopedTimer t(e, timed, "gemm_o", run_iter);
       gemm_launch(p.o, s);
+      gemm_launch(p.o2, s);
     }
     {
       ScopedTimer t(e, timed, "rmsnorm", run_iter);
@@ -444,6 +465,7 @@ void model_iteration(Engine& e, int64_t run_iter, bool timed) {
     {
       ScopedTimer t(e, timed, "gemm_down", run_iter);
       gemm_launch(p.down, s);
+      gemm_launch(p.down2, s);
     }
   }
   {

@@ -95,7 +95,7 @@ class Engine:
                  sampling: SamplingConfig | None = None, max_handles: int | None = None,
                  max_groups: int | None = None, device: int = 0, record_payload: bool | None = None,
                  prompt_len: int = 256, page_size: int = 16, kv_pages: int = 0, weight_seed: int = 0,
-                 weight_std: float = 0.02, prompt_source=None):
+                 weight_std: float = 0.02, prompt_source=None, nondeterministic_gemm: bool = False):
         self.config = config
         self.global_seed = global_seed
         self.model = model
@@ -109,6 +109,9 @@ class Engine:
         self.page_size = page_size
         self.kv_pages = kv_pages
         self.weight_seed, self.weight_std = weight_seed, weight_std
+        # fp32 residual GEMMs may split K with TMA reduce-add (faster at mid-size batches; the split
+        # summation order is then not fixed run to run)
+        self.nondeterministic_gemm = bool(nondeterministic_gemm)
         self.prompt_source = prompt_source or (
             lambda iid: synthetic_prompt(global_seed, iid, prompt_len, model.vocab)) if model else None
         if record_payload is None:
@@ -149,6 +152,7 @@ class Engine:
             c.eos_ids[i] = t
         c.record_payload = int(self._record)
         c.weight_seed, c.weight_std = self.weight_seed, self.weight_std
+        c.nondeterministic_gemm = int(self.nondeterministic_gemm)
         m = None
         if self.model is not None:
             sp = self.model

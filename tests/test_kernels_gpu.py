@@ -130,3 +130,22 @@ def test_tcgen05_gemm_cta_pair(shape, epi):
     torch.cuda.synchronize()
     tol = 2e-2 if epi in (0, 3) else 2e-3
     torch.testing.assert_close(out.float(), ref, rtol=tol, atol=tol * max(1.0, ref.abs().max().item() * 0.01))
+
+
+@pytest.mark.parametrize("shape", [(1536, 1536, 384), (1536, 8960, 256), (384, 640, 1000), (1536, 8960, 37)])
+@pytest.mark.parametrize("code", [1 | (6 << 1) | (2 << 5), 0 | (7 << 1) | (4 << 5), 1 | (5 << 1) | (8 << 5)])
+def test_tcgen05_gemm_reduce_add_split(shape, code):
+    """fp32 residual GEMM with split-K partials reduce-added by TMA (no cluster); fixed schedules."""
+    N, K, M = shape
+    if _capi.lib().ab_debug_gemm_sched(N, K, M, 256, 1, 148, 0x40000000 | 0x8000 | code, 2) == 0:
+        pytest.skip("schedule not valid for this shape (too few k-blocks per split)")
+    g = torch.Generator(device="cuda").manual_seed(N + K + M + code)
+    W = (torch.randn(N, K, device="cuda", generator=g) * 0.05).to(torch.bfloat16)
+    A = torch.randn(M, K, device="cuda", generator=g).to(torch.bfloat16)
+    base = torch.randn(M, N, device="cuda", generator=g)
+    out = base.clone()
+    # bit 10: cluster-of-1 plan allowing reduce-add split-K, bit 7: fixed code, 0x8000: reduce-add split
+    _capi.call("ab_debug_gemm", _ptr(W), _ptr(A), _ptr(out), None, N, K, M, 0x8000 | code, 2 + 1024 + 128)
+    torch.cuda.synchronize()
+    ref = base + A.float() @ W.float().t()
+    torch.testing.assert_close(out, ref, rtol=2e-3, atol=2e-3 * max(1.0, ref.abs().max().item() * 0.01))

@@ -22,12 +22,13 @@ MARGIN_EPS = 0.05   # logit units
 LOGP_TOL = 0.05     # nats
 
 
-def _engine(spec, prompts, S=8, l_max=64, page=16, greedy=True, temperature=1.0, P=None):
+def _engine(spec, prompts, S=8, l_max=64, page=16, greedy=True, temperature=1.0, P=None, nondet=False):
     P = P or len(next(iter(prompts.values())))
     return pb.LengthDrivenEngine(
         pb.EngineConfig(max_slots=S, l_max=l_max), global_seed=3, model=spec,
         sampling=pb.SamplingConfig(temperature=temperature, greedy=greedy), prompt_len=P, page_size=page,
-        kv_pages=1024, max_handles=64, max_groups=16, prompt_source=lambda iid: prompts[iid])
+        kv_pages=1024, max_handles=64, max_groups=16, prompt_source=lambda iid: prompts[iid],
+        nondeterministic_gemm=nondet)
 
 
 def _prompts(spec, n, P):
@@ -50,13 +51,14 @@ def _check_greedy(dec, prompt, toks, logps):
     return flips
 
 
+@pytest.mark.parametrize("nondet", [False, True])
 @pytest.mark.parametrize("preset,layers", [("tiny", None), ("qwen2.5-1.5b", 2), ("qwen3-4b", 1)])
-def test_greedy_tokens_match_oracle(preset, layers):
+def test_greedy_tokens_match_oracle(preset, layers, nondet):
     spec = pb.PRESETS[preset]
     if layers:
         spec = spec.truncated(layers)
     prompts = _prompts(spec, 2, 24)
-    eng = _engine(spec, prompts, page=16 if preset == "tiny" else 64)
+    eng = _engine(spec, prompts, page=16 if preset == "tiny" else 64, nondet=nondet)
     eng.begin_step(0)
     samples = []
     for iid, lens in ((0, [5, 17, 30, 40]), (1, [9, 33])):

@@ -29,6 +29,7 @@ def main():
     ap.add_argument("--iters", type=int, default=16)
     ap.add_argument("--page", type=int, default=64)
     ap.add_argument("--kv-pages", type=int, default=0)
+    ap.add_argument("--det", action="store_true", help="deterministic GEMM plans only (no reduce-add split-K)")
     ap.add_argument("--ncu", action="store_true",
                     help="bracket only the profiled iterations with cudaProfilerStart/Stop "
                          "(run under ncu --profile-from-start off)")
@@ -40,7 +41,7 @@ def main():
     eng = pb.LengthDrivenEngine(pb.EngineConfig(max_slots=args.batch, l_max=l_max), model=spec,
                                 sampling=pb.SamplingConfig(temperature=0.8), prompt_len=args.prompt,
                                 page_size=args.page, kv_pages=args.kv_pages, max_handles=max(4096, 2 * args.batch),
-                                max_groups=args.batch)
+                                max_groups=args.batch, nondeterministic_gemm=not args.det)
     eng.begin_step(0)
     for i in range(args.batch):
         s = RolloutSample(i // 8, i % 8)

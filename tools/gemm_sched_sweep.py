@@ -30,10 +30,14 @@ def main():
     ap.add_argument("--m", type=int, nargs="+", default=[64, 128, 192, 256, 384, 512, 768, 1024])
     ap.add_argument("--shapes", nargs="+", default=["qkv", "o", "down"])
     ap.add_argument("--reps", type=int, default=7)
+    ap.add_argument("--cluster", type=int, default=8, choices=[1, 2, 8],
+                    help="plan cluster size (2: plain, not pair; 1: TMA reduce-add split-K for fp32 residual GEMMs)")
     args = ap.parse_args()
     lib = _capi.lib()
     ncl = C.c_int()
-    _capi.call("ab_debug_gemm_clusters", 8, C.byref(ncl))
+    _capi.call("ab_debug_gemm_clusters", args.cluster, C.byref(ncl))
+    cs = args.cluster
+    flag = {8: 16, 2: 512, 1: 1024}[cs]
     for name in args.shapes:
         N, K, epi = SHAPES[name]
         W = (torch.randn(N, K, device="cuda") * 0.02).to(torch.bfloat16)
@@ -42,18 +46,22 @@ def main():
             out = torch.zeros(M, N if epi != 3 else N // 2, device="cuda",
                               dtype=torch.float32 if epi in (1, 2) else torch.bfloat16)
             bias = torch.zeros(N, device="cuda", dtype=torch.bfloat16) if epi == 0 else None
-            auto = lib.ab_debug_gemm_sched(N, K, M, 256, 8, ncl.value, 0, epi)
+            auto = lib.ab_debug_gemm_sched(N, K, M, 256, cs, ncl.value, 0, epi)
             res = []
             for swap in (1, 0):
                 for t in ((32, 64, 128, 256) if swap else (128, 256)):
-                    for sp in (1, 2, 4, 8):
+                    for sp in ((1, 2, 4, 8) if cs != 2 else (1, 2)):
                         code = swap | ((t.bit_length() - 1) << 1) | (sp << 5)
-                        if lib.ab_debug_gemm_sched(N, K, M, 256, 8, ncl.value, 0x40000000 | code, epi) == 0:
+                        if cs == 1 and sp > 1:
+                            if epi != 2:
+                                continue
+                            code |= 0x8000
+                        if lib.ab_debug_gemm_sched(N, K, M, 256, cs, ncl.value, 0x40000000 | code, epi) == 0:
                             continue
                         ms = C.c_float()
                         _capi.call("ab_debug_gemm_time", C.c_void_p(W.data_ptr()), C.c_void_p(A.data_ptr()),
                                    C.c_void_p(out.data_ptr()), C.c_void_p(bias.data_ptr()) if bias is not None else None,
-                                   N, K, M, code, epi + 16 + 128, args.reps, C.byref(ms))
+                                   N, K, M, code, epi + flag + 128, args.reps, C.byref(ms))
                         res.append((round(ms.value * 1e3, 1), code))
             res.sort()
             a = [r for r in res if r[1] == (auto & 0x3ff)]
