@@ -219,19 +219,23 @@ __global__ void __launch_bounds__(256) k_rmsnorm_v(const float* __restrict__ x, 
   if (r >= rows) return;
   constexpr int D = NV * 128;
   const float4* xr = reinterpret_cast<const float4*>(x + (size_t)r * D);
+  const uint2* wv = reinterpret_cast<const uint2*>(w);
   float4 v[NV];
+  uint2 wr[NV];  // the norm weights are loaded together with x: one memory round trip
 #pragma unroll
-  for (int i = 0; i < NV; ++i) v[i] = xr[i * 32 + lane];
+  for (int i = 0; i < NV; ++i) {
+    v[i] = xr[i * 32 + lane];
+    wr[i] = __ldg(wv + i * 32 + lane);
+  }
   float ss = 0.f;
 #pragma unroll
   for (int i = 0; i < NV; ++i) ss += v[i].x * v[i].x + v[i].y * v[i].y + v[i].z * v[i].z + v[i].w * v[i].w;
   ss = warp_sum(ss);
   const float rs = rsqrtf(ss / (float)D + eps);
-  const uint2* wv = reinterpret_cast<const uint2*>(w);
   uint2* o = reinterpret_cast<uint2*>(out + (size_t)r * D);
 #pragma unroll
   for (int i = 0; i < NV; ++i) {
-    const uint2 ww = __ldg(wv + i * 32 + lane);
+    const uint2 ww = wr[i];
     const __nv_bfloat162 w01 = *reinterpret_cast<const __nv_bfloat162*>(&ww.x);
     const __nv_bfloat162 w23 = *reinterpret_cast<const __nv_bfloat162*>(&ww.y);
     const __nv_bfloat162 o01 = __floats2bfloat162_rn(v[i].x * rs * __low2float(w01), v[i].y * rs * __high2float(w01));
