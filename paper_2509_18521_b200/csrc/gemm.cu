@@ -354,15 +354,45 @@ __global__ void __launch_bounds__(kThreads, 1)
               int M_cap, const int* __restrict__ rows_dev, const int* __restrict__ stop_dev, void* __restrict__ out,
               int64_t ldo, const __nv_bfloat16* __restrict__ bias, const int* __restrict__ sched_tab, int trace) {
   if (threadIdx.x == 0) trace_mark(trace, 0);
-  if (stop_dev && *stop_dev) return;
-  const int rows = rows_dev ? min(*rows_dev, M_cap) : M_cap;
-  if (rows <= 0) return;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* ring = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  float* xchg = reinterpret_cast<float*>(ring + kRingBytes);
+  uint64_t* full = reinterpret_cast<uint64_t*>(ring + kRingBytes + kXchgBytes);
+  uint64_t* empty = full + kMaxStages;
+  uint64_t* tmem_full = empty + kMaxStages;  // [2]
+  uint64_t* tmem_empty = tmem_full + 2;      // [2]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tmem_empty + 2);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  constexpr bool pair = kPair;  // CTA pair (cta_group::2): even cluster rank leads
+
+  // Setup that does not depend on the live row count (descriptor prefetch, every barrier of the
+  // ring) runs while the stop flag / row count / schedule loads are in flight.
+  if (warp == 0 && lane == 0) {
+    for (const CUtensorMap* mp : {&tw3, &tw3_256, &ta3_32, &ta3_64, &ta3, &ta3_256})
+      asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(mp)) : "memory");
+    if constexpr (EPI == kEpiAddF32) {
+      asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tx_ns)) : "memory");
+      asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tx_sw)) : "memory");
+    }
+    for (int s = 0; s < kMaxStages; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(&tmem_full[a], 1);
+      mbar_init(&tmem_empty[a], pair ? 8 : 4);  // pair: both CTAs' epilogue warps release the leader
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  const int stop = stop_dev ? *stop_dev : 0;
+  const int rows_raw = rows_dev ? *rows_dev : M_cap;
+  const int rows = min(rows_raw, M_cap);
+  if (stop || rows <= 0) return;
   const int code = sched_tab[rows];
   if (code == 0) return;
   const Sched sc = sched_from(code, rows, N, K);
   const int cs = (int)cluster_nctarank();
   const bool split = sc.splits > 1 && !sc.red;  // cluster split-K
-  constexpr bool pair = kPair;  // CTA pair (cta_group::2): even cluster rank leads
   if (kPair != (sc.pair != 0)) return;  // the host never builds such a table
   const int crank = (split || pair) ? (int)cluster_ctarank() : 0;
   const int prank = pair ? (crank & 1) : 0;
@@ -381,31 +411,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   // the 3-D TMA views this schedule loads from
   const CUtensorMap* mw = sc.wn == 256 && !sc.pair ? &tw3_256 : &tw3;
   const CUtensorMap* ma = sc.pair || sc.an == 128 ? &ta3 : sc.an == 32 ? &ta3_32 : sc.an == 64 ? &ta3_64 : &ta3_256;
-
-  extern __shared__ uint8_t smem_raw[];
-  uint8_t* ring = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  float* xchg = reinterpret_cast<float*>(ring + kRingBytes);
-  uint64_t* full = reinterpret_cast<uint64_t*>(ring + kRingBytes + kXchgBytes);
-  uint64_t* empty = full + kMaxStages;
-  uint64_t* tmem_full = empty + kMaxStages;  // [2]
-  uint64_t* tmem_empty = tmem_full + 2;      // [2]
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tmem_empty + 2);
-
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int nst = sc.stages;
-  if (warp == 0 && lane == 0) {
-    for (int s = 0; s < nst; ++s) {
-      mbar_init(&full[s], 1);
-      mbar_init(&empty[s], 1);
-    }
-    for (int a = 0; a < 2; ++a) {
-      mbar_init(&tmem_full[a], 1);
-      mbar_init(&tmem_empty[a], pair ? 8 : 4);  // pair: both CTAs' epilogue warps release the leader
-    }
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(mw)) : "memory");
-    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(ma)) : "memory");
-  }
   if (warp == 1) {
     if constexpr (kPair) {
       asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
@@ -437,10 +443,12 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int mt = u - nt * sc.m_tiles;
     n0 = nt * sc.wn;
     m0 = mt * sc.an;
-    kb0 = 2 * (int)(((int64_t)(sc.nk / 2) * z) / sc.splits);  // stages are k-block pairs
-    kb1 = 2 * (int)(((int64_t)(sc.nk / 2) * (z + 1)) / sc.splits);
-    npairs = (kb1 - kb0) / 2;
-    rot = npairs > 0 ? (int)(((int64_t)mt * npairs) / sc.m_tiles) : 0;
+    // (32-bit arithmetic: 64-bit divisions cost ~1 us on the producer's critical path)
+    const int np_all = sc.nk >> 1;
+    kb0 = 2 * ((np_all * z) / sc.splits);  // stages are k-block pairs
+    kb1 = 2 * ((np_all * (z + 1)) / sc.splits);
+    npairs = (kb1 - kb0) >> 1;
+    rot = npairs > 0 ? (mt * npairs) / sc.m_tiles : 0;
   };
   auto kb_at = [&](int kb0, int i) { return kb0 + 2 * ((i + rot) % npairs); };
 
@@ -452,6 +460,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     // the arming arrival).
     const bool wprod = warp == 0;
     if (lane == 0) {
+      if (wprod) trace_mark(trace, 9);
       // weights stream through once per launch unless several row tiles share them
       uint64_t pol_w, pol_a;
       if (sc.m_tiles > 1)
@@ -459,6 +468,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       else
         asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol_w));
       asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol_a));
+      if (wprod) trace_mark(trace, 10);
       int g = 0;
       const uint32_t full_lead = pair ? map_rank(smem_u32(full), leader) : 0u;
       for (int u = u_first; u < n_units; u += u_step) {
@@ -503,6 +513,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           const uint32_t ph = (g / nst) & 1;
           mbar_wait(&empty[s], ph ^ 1);
           uint8_t* st = ring + s * sc.stage_bytes;
+          if (g == 0 && wprod) trace_mark(trace, 13);
           if (trace & 4) {  // debug: MMA-only timing (no operand loads)
             if (wprod) mbar_arrive(&full[s]);
             continue;
