@@ -125,6 +125,8 @@ __global__ void __launch_bounds__(kThreads, 2)
                   const bf16* __restrict__ q, bf16* __restrict__ out, float* __restrict__ part_o,
                   float* __restrict__ part_ml, int max_splits) {
   using Cfg = AttCfg<HD>;
+  pdl_wait();
+  // (no early launch_dependents: the successor pre-launches when this grid drains)
   const Ctl* c = e.ctl;
   if (c->stop) return;
   const int b = c->b;
@@ -426,8 +428,8 @@ int grid_t() {
 template <int HD>
 void launch_t(const CUtensorMap& map, const EngineDev& e, const ModelDev& m, int layer, const bf16* q, bf16* out,
               float* part_o, float* part_ml, int max_splits, cudaStream_t s) {
-  k_decode_attn<HD><<<grid_t<HD>(), kThreads, AttCfg<HD>::kSmem, s>>>(map, e, m, layer, q, out, part_o, part_ml,
-                                                                      max_splits);
+  launch_pdl(k_decode_attn<HD>, dim3(grid_t<HD>()), dim3(kThreads), AttCfg<HD>::kSmem, s, map, e, m, layer, q, out,
+             part_o, part_ml, max_splits);
 }
 
 }  // namespace

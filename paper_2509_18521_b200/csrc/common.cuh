@@ -127,6 +127,28 @@ __host__ __device__ inline double np_pairwise_sum(const double* a, int n) {
 
 void set_last_error(const char* msg);  // engine.cu
 
+// Programmatic dependent launch: kernels of the decode iteration are launched with programmatic
+// stream serialization, so a kernel's CTAs are scheduled while its predecessor's last CTAs are
+// still running; each such kernel calls pdl_wait() before it touches anything the predecessor
+// writes, and pdl_launch() once it no longer needs to delay its own successor.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_launch() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
+template <typename... KArgs, typename... Args>
+inline void launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s, Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  AB_CUDA(cudaLaunchKernelEx(&cfg, kern, args...));
+}
+
 inline int ceil_div(int64_t a, int64_t b) { return (int)((a + b - 1) / b); }
 
 }  // namespace ab

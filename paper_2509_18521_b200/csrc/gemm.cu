@@ -384,6 +384,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
+  pdl_wait();  // everything below reads what the previous kernel of the stream wrote
+  // (no early launch_dependents: the successor pre-launches when this grid drains)
   const int stop = stop_dev ? *stop_dev : 0;
   const int rows_raw = rows_dev ? *rows_dev : M_cap;
   const int rows = min(rows_raw, M_cap);
@@ -1052,13 +1054,15 @@ void launch_t(const GemmPlan& p, cudaStream_t s) {
   cfg.blockDim = dim3(kThreads);
   cfg.dynamicSmemBytes = kSmem;
   cfg.stream = s;
-  cudaLaunchAttribute at[1];
+  cudaLaunchAttribute at[2];
   at[0].id = cudaLaunchAttributeClusterDimension;
   at[0].val.clusterDim.x = p.cluster;
   at[0].val.clusterDim.y = 1;
   at[0].val.clusterDim.z = 1;
+  at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;  // see pdl_wait in the kernel
+  at[1].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = at;
-  cfg.numAttrs = 1;
+  cfg.numAttrs = 2;
   if (p.pair)
     AB_CUDA(cudaLaunchKernelEx(&cfg, k_gemm_tc<EPI, true>, p.tw3, p.tw3_256, p.ta3_32, p.ta3_64, p.ta3, p.ta3_256, p.tx_ns, p.tx_sw, p.N, p.K, p.M_cap, p.rows_dev, p.stop_dev,
                                p.out, p.ldo, p.bias, p.sched, g_trace_on));

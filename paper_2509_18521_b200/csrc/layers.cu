@@ -182,6 +182,8 @@ __global__ void k_embed(ModelDev m, const bf16* __restrict__ emb, float* __restr
 // one warp per row: y = bf16(x * rsqrt(mean(x^2) + eps) * w)
 __global__ void k_rmsnorm(const float* __restrict__ x, const bf16* __restrict__ w, bf16* __restrict__ out, int d,
                           float eps, const int* rows_dev, int rows_cap, const int* stop) {
+  pdl_wait();
+  // (no early launch_dependents: the successor pre-launches when this grid drains)
   if (stopped(stop)) return;
   const int rows = rows_dev ? min(*rows_dev, rows_cap) : rows_cap;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -212,6 +214,8 @@ template <int NV>
 __global__ void __launch_bounds__(256) k_rmsnorm_v(const float* __restrict__ x, const bf16* __restrict__ w,
                                                    bf16* __restrict__ out, float eps, const int* rows_dev,
                                                    int rows_cap, const int* stop) {
+  pdl_wait();
+  // (no early launch_dependents: the successor pre-launches when this grid drains)
   if (stopped(stop)) return;
   const int rows = rows_dev ? min(*rows_dev, rows_cap) : rows_cap;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -277,6 +281,8 @@ template <int HD>
 __global__ void k_rope_kv(ModelDev m, int layer, const bf16* __restrict__ qkv, const bf16* __restrict__ qn,
                           const bf16* __restrict__ kn, bf16* __restrict__ qout, const int* rows_dev, int rows_cap,
                           const int* stop) {
+  pdl_wait();
+  // (no early launch_dependents: the successor pre-launches when this grid drains)
   if (stopped(stop)) return;
   const int rows = rows_dev ? min(*rows_dev, rows_cap) : rows_cap;
   const int r = blockIdx.x;
@@ -509,25 +515,27 @@ void launch_rmsnorm(const float* x, const bf16* w, bf16* out, int d, float eps, 
                     const int* stop, cudaStream_t s) {
   const dim3 g(ceil_div(rows_cap, 8)), t(256);
   switch (d % 128 ? 0 : d / 128) {
-    case 2: k_rmsnorm_v<2><<<g, t, 0, s>>>(x, w, out, eps, rows_dev, rows_cap, stop); break;
-    case 4: k_rmsnorm_v<4><<<g, t, 0, s>>>(x, w, out, eps, rows_dev, rows_cap, stop); break;
-    case 8: k_rmsnorm_v<8><<<g, t, 0, s>>>(x, w, out, eps, rows_dev, rows_cap, stop); break;
-    case 12: k_rmsnorm_v<12><<<g, t, 0, s>>>(x, w, out, eps, rows_dev, rows_cap, stop); break;
-    case 16: k_rmsnorm_v<16><<<g, t, 0, s>>>(x, w, out, eps, rows_dev, rows_cap, stop); break;
-    case 20: k_rmsnorm_v<20><<<g, t, 0, s>>>(x, w, out, eps, rows_dev, rows_cap, stop); break;
-    case 24: k_rmsnorm_v<24><<<g, t, 0, s>>>(x, w, out, eps, rows_dev, rows_cap, stop); break;
-    case 28: k_rmsnorm_v<28><<<g, t, 0, s>>>(x, w, out, eps, rows_dev, rows_cap, stop); break;
-    case 32: k_rmsnorm_v<32><<<g, t, 0, s>>>(x, w, out, eps, rows_dev, rows_cap, stop); break;
-    default: k_rmsnorm<<<g, t, 0, s>>>(x, w, out, d, eps, rows_dev, rows_cap, stop); break;
+    case 2: launch_pdl(k_rmsnorm_v<2>, g, t, 0, s, x, w, out, eps, rows_dev, rows_cap, stop); break;
+    case 4: launch_pdl(k_rmsnorm_v<4>, g, t, 0, s, x, w, out, eps, rows_dev, rows_cap, stop); break;
+    case 8: launch_pdl(k_rmsnorm_v<8>, g, t, 0, s, x, w, out, eps, rows_dev, rows_cap, stop); break;
+    case 12: launch_pdl(k_rmsnorm_v<12>, g, t, 0, s, x, w, out, eps, rows_dev, rows_cap, stop); break;
+    case 16: launch_pdl(k_rmsnorm_v<16>, g, t, 0, s, x, w, out, eps, rows_dev, rows_cap, stop); break;
+    case 20: launch_pdl(k_rmsnorm_v<20>, g, t, 0, s, x, w, out, eps, rows_dev, rows_cap, stop); break;
+    case 24: launch_pdl(k_rmsnorm_v<24>, g, t, 0, s, x, w, out, eps, rows_dev, rows_cap, stop); break;
+    case 28: launch_pdl(k_rmsnorm_v<28>, g, t, 0, s, x, w, out, eps, rows_dev, rows_cap, stop); break;
+    case 32: launch_pdl(k_rmsnorm_v<32>, g, t, 0, s, x, w, out, eps, rows_dev, rows_cap, stop); break;
+    default: launch_pdl(k_rmsnorm, g, t, 0, s, x, w, out, d, eps, rows_dev, rows_cap, stop); break;
   }
 }
 
 void launch_rope_kv(const ModelDev& m, int layer, const bf16* qkv, const bf16* q_norm, const bf16* k_norm, bf16* q_out,
                     const int* rows_dev, int rows_cap, const int* stop, cudaStream_t s) {
   if (m.hd == 128)
-    k_rope_kv<128><<<rows_cap, 256, 0, s>>>(m, layer, qkv, q_norm, k_norm, q_out, rows_dev, rows_cap, stop);
+    launch_pdl(k_rope_kv<128>, dim3(rows_cap), dim3(256), 0, s, m, layer, qkv, q_norm, k_norm, q_out, rows_dev, rows_cap,
+               stop);
   else
-    k_rope_kv<64><<<rows_cap, 256, 0, s>>>(m, layer, qkv, q_norm, k_norm, q_out, rows_dev, rows_cap, stop);
+    launch_pdl(k_rope_kv<64>, dim3(rows_cap), dim3(256), 0, s, m, layer, qkv, q_norm, k_norm, q_out, rows_dev, rows_cap,
+               stop);
 }
 
 void launch_prefill_attention(const ModelDev& m, int layer, const bf16* q, bf16* out, const int* seg_start,

@@ -247,6 +247,8 @@ __device__ void sample_row(const float* __restrict__ z, int V, float inv_temp, i
 
 __global__ void __launch_bounds__(kSampThreads) k_sample(EngineDev e, ModelDev m, const float* __restrict__ logits,
                                                          float inv_temp, int greedy, float top_p) {
+  pdl_wait();
+  // (no early launch_dependents: the successor pre-launches when this grid drains)
   Ctl* c = e.ctl;
   if (c->stop) return;
   const int i = blockIdx.x;
@@ -307,7 +309,7 @@ __global__ void __launch_bounds__(kSampThreads) k_sample_rows(const float* __res
 void launch_sampler(const EngineDev& e, const ModelDev& m, const float* logits, float inv_temp, int greedy,
                     float top_p, cudaStream_t s) {
   AB_REQUIRE(top_p > 0.f && top_p <= 1.f, AB_ERR_CONFIG, "top_p must lie in (0, 1]");
-  k_sample<<<e.S, kSampThreads, 0, s>>>(e, m, logits, inv_temp, greedy, top_p);
+  launch_pdl(k_sample, dim3(e.S), dim3(kSampThreads), 0, s, e, m, logits, inv_temp, greedy, top_p);
 }
 
 }  // namespace ab
