@@ -39,6 +39,10 @@ METRIC = "rollout tokens/s & RL-step rollout time, APRIL vs sync, long-tail leng
 WORKLOADS = {
     "C2": dict(model="qwen2.5-1.5b", n=64, g=8, n_prime=128, slots=1024, l_max=4096, mu=6.6, sigma=1.0, rho=0.7,
                prompt=256, temperature=0.8, adv="mean_std_baseline", page=64, nondet_gemm=True),
+    # BASELINE.json configs[2] per engine: Qwen3-4B shape, DAPO, partial-rollout recycling, S = 64 (the
+    # per-GPU slot count of the 8-GPU run); `--workload C3` (not the default line)
+    "C3": dict(model="qwen3-4b", n=32, g=8, n_prime=64, slots=64, l_max=16384, mu=7.5, sigma=1.0, rho=0.7,
+               prompt=256, temperature=0.8, adv="dapo", page=64, nondet_gemm=True),
     # small smoke workload (tiny decoder) for quick checks
     "C1": dict(model="tiny", n=8, g=4, n_prime=16, slots=64, l_max=1024, mu=5.5, sigma=1.0, rho=0.7, prompt=32,
                temperature=0.8, adv="mean_std_baseline", page=16),
@@ -97,13 +101,13 @@ class ClockSampler:
                 "reasons": reasons, "samples": len(self.rows)}
 
 
-def build_engine(pb, w, device, seed, record=True):
+def build_engine(pb, w, device, seed, record=True, kv_resume="retain"):
     spec = pb.PRESETS[w["model"]]
     eng = pb.LengthDrivenEngine(
         pb.EngineConfig(max_slots=w["slots"], l_max=w["l_max"]), global_seed=seed, model=spec,
         sampling=pb.SamplingConfig(temperature=w["temperature"]), prompt_len=w["prompt"], page_size=w["page"],
         device=device, record_payload=record, max_handles=max(4096, 4 * w["n_prime"] * w["g"]),
-        max_groups=4 * w["n_prime"] + 64, nondeterministic_gemm=w.get("nondet_gemm", False))
+        max_groups=4 * w["n_prime"] + 64, nondeterministic_gemm=w.get("nondet_gemm", False), kv_resume=kv_resume)
     return spec, eng
 
 
@@ -230,6 +234,9 @@ def main():
     ap.add_argument("--profile-every", type=int, default=8)
     ap.add_argument("--ref-step-s", type=float, default=12.0)
     ap.add_argument("--seed", type=int, default=0)
+    ap.add_argument("--kv-resume", default="reprefill", choices=["retain", "reprefill"],
+                    help="paused partials: re-prefill prompt + carried tokens at resume (the cost APRIL pays when "
+                         "weights change every step; inside the rollout wall time) or keep their KV resident")
     ap.add_argument("--force-dp", action="store_true", help="run the data-parallel engine even at N = 1 (tests)")
     ap.add_argument("--replicas", action="store_true",
                     help="N > 1: independent engine replicas instead of the lockstep data-parallel engine")
@@ -258,7 +265,7 @@ def main():
     seed = args.seed if dp else args.seed + rank
     hbm_peak, tf_peak, peak_kind = _peaks()
 
-    spec, eng = build_engine(pb, w, local, seed, record=True)
+    spec, eng = build_engine(pb, w, local, seed, record=True, kv_resume=args.kv_resume)
     comm = None
     front = eng  # what the scheduler drives
     if dp:
@@ -271,7 +278,8 @@ def main():
     if dist:
         dist.barrier()
     eng.profile(True, args.profile_every)
-    launches0 = eng.stats().kernel_launches
+    st0 = eng.stats()
+    launches0 = st0.kernel_launches
     with ClockSampler(local) as clk:
         t0 = time.perf_counter()
         rec = run_steps(pb, w, sched, eng, args.warmup, args.steps)
@@ -283,7 +291,12 @@ def main():
             dist.all_reduce(tt, op=dist.ReduceOp.MAX)
             t_dev = float(tt)
         t_host = time.perf_counter() - t0
-    launches = eng.stats().kernel_launches - launches0
+    st1 = eng.stats()
+    launches = st1.kernel_launches - launches0
+    reprefill = {"mode": args.kv_resume,
+                 "tokens_per_step": (st1.reprefill_tokens - st0.reprefill_tokens) / max(args.steps, 1),
+                 "prompt_prefill_tokens_per_step": (st1.prefill_tokens - st0.prefill_tokens) / max(args.steps, 1),
+                 "seconds_per_step": (st1.reprefill_seconds - st0.reprefill_seconds) / max(args.steps, 1)}
     kstats = {k["name"]: k for k in eng.kernel_stats()}
     eng.profile(False)
     tokens = sum(r["tokens"] for r in rec)
@@ -316,7 +329,7 @@ def main():
         ach = att["bytes"] / (att["ms"] * 1e-3) / 1e9
         roof = {"kernel": "paged GQA decode attention (k_decode_attn + combine)", "bound": "hbm",
                 "achieved": ach, "peak": hbm_peak, "unit": "GB/s", "frac": ach / hbm_peak,
-                "peak_kind": peak_kind, "traffic": _ncu_traffic(), "launches_timed": att["launches"],
+                "peak_kind": peak_kind, "traffic": _ncu_traffic(args.workload), "launches_timed": att["launches"],
                 "avg_launch_us": 1e3 * att["ms"] / att["launches"]}
     kern = {}
     tot_ms = sum(k["ms"] for k in kstats.values()) or 1.0
@@ -343,6 +356,7 @@ def main():
         "april": {"tokens_per_s": value, "ms_per_step": ms_step, "steps": len(rec),
                   "iterations_per_step": statistics.mean(r["iters"] for r in rec),
                   "carried_in_tokens_per_step": statistics.mean(r["carried"] for r in rec)},
+        "kv_resume": reprefill,
         "sync": sync,
         "april_over_sync": ((value if dp else value / world) / sync["tokens_per_s"]) if sync else None,
         "roofline": roof, "kernels": kern,
@@ -366,12 +380,14 @@ def main():
     return 0
 
 
-def _ncu_traffic():
-    """dram read+write bytes per launch of the attention kernel from the committed ncu capture."""
+def _ncu_traffic(workload):
+    """dram read+write bytes per launch of the attention kernel from the committed ncu capture
+    (taken at the C2 decode microbench point; other workloads have no capture -> null)."""
     p = os.path.join(ROOT, "profiles", "attention_dram_bytes.json")
     try:
         with open(p) as f:
-            return json.load(f).get("bytes_per_launch")
+            d = json.load(f)
+        return d.get("bytes_per_launch") if d.get("workload", "C2") == workload else None
     except Exception:
         return None
 

@@ -93,7 +93,12 @@ typedef struct ab_engine_config {
   float weight_std;
   int32_t nondeterministic_gemm; /* 1: fp32 residual GEMMs may split K with TMA reduce-add
                                     (faster; split summation order not fixed run to run) */
-  int32_t reserved[6];
+  int32_t kv_resume; /* 0: a paused sample keeps its KV across steps; 1: the abort drops it and the
+                        resubmit re-prefills prompt + carried tokens (prompt KV of resident groups is
+                        recomputed when the step version changes) -- SURVEY §8 f1 */
+  int32_t gemm_autotune; /* transformer: time the decode GEMM schedules on this GPU at engine creation
+                            and run each live row count on the fastest (0: cost-model tables) */
+  int32_t reserved[4];
 } ab_engine_config;
 
 typedef struct ab_sample_desc {
@@ -147,6 +152,8 @@ typedef struct ab_stats {
   int64_t kv_pages_total, kv_pages_free;
   int64_t prefill_tokens; /* prompt tokens prefilled (excluded from "generated") */
   int64_t kernel_launches; /* kernels this engine has launched */
+  int64_t reprefill_tokens; /* carried tokens re-prefilled at resume (kv_resume = 1) */
+  double reprefill_seconds; /* wall time spent re-prefilling (resumed partials + prompt recompute) */
 } ab_stats;
 
 typedef struct ab_kernel_stat {

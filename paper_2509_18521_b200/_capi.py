@@ -44,7 +44,8 @@ class EngineConfigC(C.Structure):
                 ("max_prompt", C.c_int32), ("temperature", C.c_float), ("top_p", C.c_float),
                 ("greedy", C.c_int32), ("n_eos", C.c_int32), ("eos_ids", C.c_int32 * 8),
                 ("record_payload", C.c_int32), ("weight_seed", C.c_uint64), ("weight_std", C.c_float),
-                ("nondeterministic_gemm", C.c_int32), ("reserved", C.c_int32 * 6)]
+                ("nondeterministic_gemm", C.c_int32), ("kv_resume", C.c_int32),
+                ("gemm_autotune", C.c_int32), ("reserved", C.c_int32 * 4)]
 
 
 class SampleDesc(C.Structure):
@@ -77,7 +78,8 @@ class RunResult(C.Structure):
 class Stats(C.Structure):
     _fields_ = [("iteration_index", C.c_int64), ("cumulative_tokens", C.c_int64), ("active", C.c_int32),
                 ("queued", C.c_int32), ("clock", C.c_double), ("kv_pages_total", C.c_int64),
-                ("kv_pages_free", C.c_int64), ("prefill_tokens", C.c_int64), ("kernel_launches", C.c_int64)]
+                ("kv_pages_free", C.c_int64), ("prefill_tokens", C.c_int64), ("kernel_launches", C.c_int64),
+                ("reprefill_tokens", C.c_int64), ("reprefill_seconds", C.c_double)]
 
 
 class KernelStat(C.Structure):

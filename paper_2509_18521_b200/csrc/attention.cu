@@ -432,7 +432,200 @@ void launch_t(const CUtensorMap& map, const EngineDev& e, const ModelDev& m, int
              part_o, part_ml, max_splits);
 }
 
+// ---------------------------------------------------------------------------
+// Causal prefill attention (prompt prefill and the re-prefill of resumed
+// partials, §8 f1): flash-attention-2 over the paged pool.  Block = up to 64
+// consecutive rows of one sequence (its block-table row and first position
+// come from the host-built block list), one q head per CTA; 4 warps own 16
+// rows each.  K / V tiles of 64 tokens are gathered page by page with
+// cp.async into the same 128-byte-swizzled layout the decode kernel reads
+// (double-buffered), S = Q K^T and O += P V run as mma.sync m16n8k16 with
+// exp2 online softmax; tokens past a row's position are masked.
+// ---------------------------------------------------------------------------
+
+template <int HD>
+struct PfCfg {
+  static constexpr int kTile = kTok * HD * 2;        // 64 rows x HD bf16
+  static constexpr int kSmem = 1024 + 5 * kTile;     // Q + 2 stages x (K, V)
+};
+
+__device__ __forceinline__ void cp_async16(uint32_t dst, const void* src, bool valid) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst), "l"(src), "r"(valid ? 16 : 0) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+
+template <int HD>
+__global__ void __launch_bounds__(128, 2)
+    k_prefill_flash(ModelDev m, int layer, const bf16* __restrict__ q, bf16* __restrict__ out,
+                    const int4* __restrict__ blocks) {
+  using Cfg = PfCfg<HD>;
+  constexpr int CH = HD / 8;  // 16-byte chunks per row
+  const int4 blk = blocks[blockIdx.x];  // {first row, rows, block-table row, first position}
+  const int row0 = blk.x, nrows = blk.y, pos0 = blk.w;
+  const int head = blockIdx.y, kvh = head / m.gq;
+  const int32_t* bt = m.bt + (size_t)blk.z * m.MP;
+  const int last_pos = pos0 + nrows - 1;
+  const int n_kt = last_pos / kTok + 1;
+
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  const uint32_t sQ = su32(base), sKV = sQ + Cfg::kTile;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int gr = lane >> 2, tq = lane & 3;
+
+  for (int i = tid; i < kTok * CH; i += 128) {
+    const int r = i / CH, ch = i % CH;
+    const bool v = r < nrows;
+    cp_async16(sQ + tile_off(r, ch), q + (size_t)(row0 + (v ? r : 0)) * m.qd + head * HD + ch * 8, v);
+  }
+  auto load_kv = [&](int kt, int stage) {
+    const uint32_t K = sKV + stage * 2 * Cfg::kTile, V = K + Cfg::kTile;
+    for (int i = tid; i < kTok * CH; i += 128) {
+      const int r = i / CH, ch = i % CH;
+      const int tok = kt * kTok + r;
+      const bool v = tok <= last_pos;
+      const int t = v ? tok : 0;
+      const int page = bt[t / m.P], slot = t % m.P;
+      cp_async16(K + tile_off(r, ch), m.kv + m.kv_off(layer, page, 0, kvh, slot) + ch * 8, v);
+      cp_async16(V + tile_off(r, ch), m.kv + m.kv_off(layer, page, 1, kvh, slot) + ch * 8, v);
+    }
+  };
+  load_kv(0, 0);
+  cp_async_commit();
+
+  const float scale = rsqrtf((float)HD) * kLog2e;
+  const int wq = warp * 16;
+  const int qp[2] = {pos0 + wq + gr, pos0 + wq + gr + 8};
+  const int warp_last = pos0 + wq + 15;
+  float o[HD / 8][4];
+#pragma unroll
+  for (int t = 0; t < HD / 8; ++t) o[t][0] = o[t][1] = o[t][2] = o[t][3] = 0.f;
+  float mrow[2] = {-FLT_MAX, -FLT_MAX}, lrow[2] = {0.f, 0.f};
+  uint32_t qa[HD / 16][4];
+
+  for (int kt = 0; kt < n_kt; ++kt) {
+    if (kt + 1 < n_kt) load_kv(kt + 1, (kt + 1) & 1);
+    cp_async_commit();
+    cp_async_wait<1>();
+    __syncthreads();
+    if (kt == 0) {
+#pragma unroll
+      for (int kk = 0; kk < HD / 16; ++kk) ldsm_x4(qa[kk], sQ + tile_off(wq + (lane & 15), kk * 2 + (lane >> 4)), false);
+    }
+    const int tb = kt * kTok;
+    if (tb <= warp_last && wq < nrows) {
+      const uint32_t K = sKV + (kt & 1) * 2 * Cfg::kTile, V = K + Cfg::kTile;
+      float s[8][4];
+#pragma unroll
+      for (int j = 0; j < 8; ++j) s[j][0] = s[j][1] = s[j][2] = s[j][3] = 0.f;
+#pragma unroll
+      for (int kk = 0; kk < HD / 16; ++kk) {
+        const int mi = lane >> 3;
+#pragma unroll
+        for (int kg = 0; kg < 4; ++kg) {
+          uint32_t bb[4];
+          ldsm_x4(bb, K + tile_off(kg * 16 + (mi >> 1) * 8 + (lane & 7), kk * 2 + (mi & 1)), false);
+          mma16816(s[2 * kg], qa[kk], bb[0], bb[1]);
+          mma16816(s[2 * kg + 1], qa[kk], bb[2], bb[3]);
+        }
+      }
+      float mx[2] = {-FLT_MAX, -FLT_MAX};
+#pragma unroll
+      for (int j = 0; j < 8; ++j)
+#pragma unroll
+        for (int q4 = 0; q4 < 4; ++q4) {
+          const int tok = tb + j * 8 + tq * 2 + (q4 & 1);
+          const float v = tok <= qp[q4 >> 1] ? s[j][q4] * scale : -FLT_MAX;
+          s[j][q4] = v;
+          mx[q4 >> 1] = fmaxf(mx[q4 >> 1], v);
+        }
+      float alpha[2];
+#pragma unroll
+      for (int r = 0; r < 2; ++r) {
+        mx[r] = fmaxf(mx[r], __shfl_xor_sync(0xffffffffu, mx[r], 1));
+        mx[r] = fmaxf(mx[r], __shfl_xor_sync(0xffffffffu, mx[r], 2));
+        const float mn = fmaxf(mrow[r], mx[r]);
+        alpha[r] = (mrow[r] == -FLT_MAX) ? 0.f : exp2f(mrow[r] - mn);
+        mrow[r] = mn;
+      }
+      float rsum[2] = {0.f, 0.f};
+#pragma unroll
+      for (int j = 0; j < 8; ++j)
+#pragma unroll
+        for (int q4 = 0; q4 < 4; ++q4) {
+          const int r = q4 >> 1;
+          const float p = (s[j][q4] == -FLT_MAX) ? 0.f : exp2f(s[j][q4] - mrow[r]);
+          s[j][q4] = p;
+          rsum[r] += p;
+        }
+#pragma unroll
+      for (int r = 0; r < 2; ++r) lrow[r] = lrow[r] * alpha[r] + rsum[r];
+#pragma unroll
+      for (int nt = 0; nt < HD / 8; ++nt) {
+        o[nt][0] *= alpha[0];
+        o[nt][1] *= alpha[0];
+        o[nt][2] *= alpha[1];
+        o[nt][3] *= alpha[1];
+      }
+#pragma unroll
+      for (int ks = 0; ks < 4; ++ks) {
+        const uint32_t pa[4] = {pack_bf16(s[2 * ks][0], s[2 * ks][1]), pack_bf16(s[2 * ks][2], s[2 * ks][3]),
+                                pack_bf16(s[2 * ks + 1][0], s[2 * ks + 1][1]),
+                                pack_bf16(s[2 * ks + 1][2], s[2 * ks + 1][3])};
+#pragma unroll
+        for (int nt2 = 0; nt2 < HD / 16; ++nt2) {
+          const int mi = lane >> 3;
+          uint32_t bb[4];
+          ldsm_x4(bb, V + tile_off(ks * 16 + (mi & 1) * 8 + (lane & 7), nt2 * 2 + (mi >> 1)), true);
+          mma16816(o[2 * nt2], pa, bb[0], bb[1]);
+          mma16816(o[2 * nt2 + 1], pa, bb[2], bb[3]);
+        }
+      }
+    }
+    __syncthreads();  // the stage is reloaded two tiles later
+  }
+#pragma unroll
+  for (int r = 0; r < 2; ++r) {
+    lrow[r] += __shfl_xor_sync(0xffffffffu, lrow[r], 1);
+    lrow[r] += __shfl_xor_sync(0xffffffffu, lrow[r], 2);
+  }
+#pragma unroll
+  for (int r = 0; r < 2; ++r) {
+    const int rr = wq + gr + 8 * r;
+    if (rr >= nrows) continue;
+    const float inv = 1.f / lrow[r];
+    bf16* dst = out + (size_t)(row0 + rr) * m.qd + head * HD + tq * 2;
+#pragma unroll
+    for (int nt = 0; nt < HD / 8; ++nt)
+      *reinterpret_cast<uint32_t*>(dst + nt * 8) = pack_bf16(o[nt][2 * r] * inv, o[nt][2 * r + 1] * inv);
+  }
+}
+
+template <int HD>
+void launch_pf(const ModelDev& m, int layer, const bf16* q, bf16* out, const int4* blocks, int n_blocks,
+               cudaStream_t s) {
+  static bool init = false;
+  if (!init) {
+    AB_CUDA(cudaFuncSetAttribute(k_prefill_flash<HD>, cudaFuncAttributeMaxDynamicSharedMemorySize, PfCfg<HD>::kSmem));
+    init = true;
+  }
+  k_prefill_flash<HD><<<dim3(n_blocks, m.hq), 128, PfCfg<HD>::kSmem, s>>>(m, layer, q, out, blocks);
+}
+
 }  // namespace
+
+void launch_prefill_flash(const ModelDev& m, int layer, const bf16* q, bf16* out, const int4* blocks, int n_blocks,
+                          cudaStream_t s) {
+  if (n_blocks <= 0) return;
+  if (m.hd == 128)
+    launch_pf<128>(m, layer, q, out, blocks, n_blocks, s);
+  else
+    launch_pf<64>(m, layer, q, out, blocks, n_blocks, s);
+}
 
 void make_kv_tmap(CUtensorMap* map, const ModelDev& m) {
   AB_REQUIRE(m.gq <= kMergeRows, AB_ERR_CONFIG, "decode attention supports GQA groups of at most 8");

@@ -501,7 +501,9 @@ static void validate(const ab_engine_config& c, const ab_model_config* m) {
     AB_REQUIRE(c.temperature > 0.f || c.greedy, AB_ERR_CONFIG, "temperature must be > 0");
     AB_REQUIRE(c.top_p > 0.f && c.top_p <= 1.f, AB_ERR_CONFIG, "top_p must lie in (0, 1]");
     AB_REQUIRE(c.n_eos >= 0 && c.n_eos <= 8, AB_ERR_CONFIG, "at most 8 EOS ids");
+    AB_REQUIRE(!c.kv_resume || c.record_payload, AB_ERR_CONFIG, "KV re-prefill needs the token payload on device");
   }
+  AB_REQUIRE(c.kv_resume == 0 || c.kv_resume == 1, AB_ERR_CONFIG, "kv_resume must be 0 or 1");
 }
 
 static Engine* create(const ab_engine_config* cfgp, const ab_model_config* m, int device) {
@@ -619,6 +621,7 @@ static void begin_step(Engine& e, int64_t version, const double* logits) {
                             e.stream));
     k_cf_prepare<<<1, 1, 0, e.stream>>>(e.d);
   }
+  if (e.model) model_begin_step(e, version);
   AB_CUDA(cudaStreamSynchronize(e.stream));
 }
 
@@ -643,7 +646,7 @@ static void submit(Engine& e, const ab_sample_desc* descs, int n) {
 }
 
 static void launch_iteration(Engine& e, int64_t run_iter, bool timed = false) {
-  e.launches += 2 + (e.model ? 5 + 12 * (int64_t)e.mcfg.n_layers : 1);  // incl. the partitioned GEMM pairs
+  e.launches += 2 + (e.model ? model_iter_launches(e.model) : 1);
   {
     ScopedTimer t(e, timed, "admit", run_iter);
     k_admit<<<1, 256, 0, e.stream>>>(e.d);
@@ -779,6 +782,15 @@ static void abort_active(Engine& e, int32_t* handles, int32_t* gen, int cap, int
   c.q_head = c.q_tail;
   AB_CUDA(cudaMemcpy(&e.d.ctl->b, &c.b, sizeof(int32_t), cudaMemcpyHostToDevice));
   AB_CUDA(cudaMemcpy(&e.d.ctl->q_head, &c.q_head, sizeof(int32_t), cudaMemcpyHostToDevice));
+  if (e.model && e.cfg.kv_resume && b + q) {
+    std::vector<int32_t> g2(b + q);
+    if (!gen) {
+      std::vector<int32_t> all(e.d.H);
+      AB_CUDA(cudaMemcpy(all.data(), e.d.h_gen, sizeof(int32_t) * e.d.H, cudaMemcpyDeviceToHost));
+      for (int i = 0; i < b + q; ++i) g2[i] = all[handles[i]];
+    }
+    model_evict(e, handles, gen ? gen : g2.data(), b + q);
+  }
   *n_active = b;
   *n_queued = q;
 }
@@ -1010,6 +1022,8 @@ int ab_engine_stats(ab_engine* e, ab_stats* out) {
     out->kv_pages_total = g.model ? ab::model_pages_total(g.model) : 0;
     out->kv_pages_free = c.kv_free_top;
     out->prefill_tokens = g.prefill_tokens;
+    out->reprefill_tokens = g.reprefill_tokens;
+    out->reprefill_seconds = g.reprefill_seconds;
     out->kernel_launches = g.launches;
   });
 }

@@ -89,6 +89,8 @@ struct Engine {
   int32_t* stage_i32_host = nullptr;
   size_t stage_i32_cap = 0;
   int64_t prefill_tokens = 0;
+  int64_t reprefill_tokens = 0;
+  double reprefill_seconds = 0;  // host wall time of KV re-prefill (resumed partials + prompt recompute)
   int64_t launches = 0;  // kernels launched (gpu_launches claim)
   bool use_graphs = true;
   int64_t direct_launches = 0;
@@ -130,6 +132,9 @@ void model_open_group(Engine& e, int group_slot, const int32_t* prompt, int prom
 void model_release_group(Engine& e, int group_slot);
 void model_submit(Engine& e, const ab_sample_desc* descs_dev, int n);  // after per-handle state is set
 void model_release(Engine& e, const int32_t* handles_dev, int n);
+void model_evict(Engine& e, const int32_t* handles_host, const int32_t* gen, int n);  // kv_resume: drop private KV
+void model_begin_step(Engine& e, int64_t version);
+int64_t model_iter_launches(Model* m);
 void model_iteration(Engine& e, int64_t run_iter, bool timed);         // pages + forward + sampler
 int64_t model_pages_total(Model* m);
 void model_kernel_cost(Model* m, const std::string& name, double b, double sum_ctx, double* bytes, double* flops);

@@ -246,7 +246,8 @@ int choose_sched(int rows, int N, int K, int max_bn, int cs, int ncl, int force,
     if (force & 0x8000) {  // reduce-added split-K (fp32 residual GEMMs, cluster of 1)
       const int code = force & 0x3ff;
       const int swap = code & 1, t = 1 << ((code >> 1) & 15), sp = (code >> 5) & 31;
-      if (cs != 1 || epi != kEpiAddF32 || sp < 1 || nk < 2 * sp || (!swap && N % 128)) return 0;
+      if (cs != 1 || epi != kEpiAddF32 || sp < 1 || nk < 2 * sp || (!swap && (N % 128 || t < 128))) return 0;
+      if (swap && (t < 32 || t > 256)) return 0;
       return pack(swap, t, sp, 0, 1);
     }
     if (force & 0x4000) {  // CTA pair: a cluster of 2, no split
@@ -257,11 +258,13 @@ int choose_sched(int rows, int N, int K, int max_bn, int cs, int ncl, int force,
     const int code = force & 0x3ff;
     const int swap = code & 1, t = 1 << ((code >> 1) & 15), sp = (code >> 5) & 31;
     if (sp < 1 || sp > cs || (sp & (sp - 1))) return 0;
-    if (!swap && N % 128) return 0;
+    if (!swap && (N % 128 || t < 128 || t > 256)) return 0;  // no-swap tiles: 128 or 256 weight rows
+    if (swap && (t < 32 || t > 256)) return 0;
     if (!swap && epi == kEpiSwiGLU && (t != 256 || N % 256)) return 0;
     if (sp > 1) {
       const int wn = swap ? kBM : t, an = swap ? t : kBM;
-      if ((int64_t)((N + wn - 1) / wn) * ((rows + an - 1) / an) * sp > (int64_t)ncl * cs || nk < sp) return 0;
+      // (every split needs at least one k-block pair)
+      if ((int64_t)((N + wn - 1) / wn) * ((rows + an - 1) / an) * sp > (int64_t)ncl * cs || nk < 2 * sp) return 0;
     }
     return pack(swap, t, sp);
   }
@@ -1115,8 +1118,10 @@ void gemm_set_schedule(GemmPlan& p, int force) {
   // launch geometry: clusters of p.cluster CTAs, never more than the largest possible tile count needs
   const int cs = p.cluster;
   const int ncl_max = max_clusters_epi(p.epi, cs, p.pair);
-  const int64_t max_tiles = (int64_t)ceil_div(p.N, kBM) * ceil_div(p.M_cap, 32);
-  const int ncl = (int)std::min<int64_t>(ncl_max, cs > 1 ? max_tiles : ceil_div(max_tiles, 1));
+  // (reduce-added split-K multiplies the work units by up to 8)
+  const int64_t max_tiles = (int64_t)ceil_div(p.N, kBM) * ceil_div(p.M_cap, 32) *
+                            (p.nondet && cs == 1 && p.epi == kEpiAddF32 ? 8 : 1);
+  const int ncl = (int)std::min<int64_t>(ncl_max, max_tiles);
   p.grid = ncl * cs;
   p.force = force;
   // one device table per distinct (shape, geometry): the kernel reads sched[rows]
@@ -1140,6 +1145,72 @@ void gemm_set_schedule(GemmPlan& p, int force) {
   AB_CUDA(cudaMemcpy(d, tab.data(), sizeof(int) * tab.size(), cudaMemcpyHostToDevice));
   cache[key] = d;
   p.sched = d;
+}
+
+std::vector<int> gemm_candidates(const GemmPlan& p, int rows) {
+  std::vector<int> out;
+  const int ncl = p.grid / p.cluster;
+  auto add = [&](int force) {
+    const int c = choose_sched(rows, p.N, p.K, p.BN, p.cluster, ncl, force, p.epi, p.pair);
+    if (c && std::find(out.begin(), out.end(), c) == out.end()) out.push_back(c);
+  };
+  if (p.pair) {
+    add(0x40000000 | 0x4000);
+    return out;
+  }
+  for (int swap = 1; swap >= 0; --swap)
+    for (int lg = swap ? 5 : 7; lg <= 8; ++lg) {
+      if (swap && (1 << lg) > std::max(p.BN, 32)) continue;
+      for (int sp = 1; sp <= 8; sp <<= 1) {
+        add(0x40000000 | swap | (lg << 1) | (sp << 5));
+        if (p.nondet && p.cluster == 1 && p.epi == kEpiAddF32 && sp > 1)
+          add(0x40000000 | 0x8000 | swap | (lg << 1) | (sp << 5));
+      }
+    }
+  return out;
+}
+
+void gemm_set_table(GemmPlan& p, const std::vector<int>& tab) {
+  AB_REQUIRE((int)tab.size() == p.M_cap + 1, AB_ERR_CONFIG, "schedule table size");
+  int* d = nullptr;
+  AB_CUDA(cudaMalloc(&d, sizeof(int) * tab.size()));
+  AB_CUDA(cudaMemcpy(d, tab.data(), sizeof(int) * tab.size(), cudaMemcpyHostToDevice));
+  p.sched = d;  // (tables live for the process, like the cached ones)
+  p.idle = std::all_of(tab.begin(), tab.end(), [](int c) { return c == 0; });
+}
+
+double gemm_time_code(const GemmPlan& p, int rows, int code, int reps, void* flush, size_t flush_bytes,
+                      cudaStream_t s) {
+  static int* scratch = nullptr;  // [0]: row count, [1..]: a table with one entry set
+  static int scratch_cap = 0;
+  if (p.M_cap + 2 > scratch_cap) {
+    if (scratch) cudaFree(scratch);
+    scratch_cap = p.M_cap + 2;
+    AB_CUDA(cudaMalloc(&scratch, sizeof(int) * scratch_cap));
+  }
+  std::vector<int> h(p.M_cap + 2, 0);
+  h[0] = rows;
+  h[1 + rows] = code;
+  AB_CUDA(cudaMemcpyAsync(scratch, h.data(), sizeof(int) * h.size(), cudaMemcpyHostToDevice, s));
+  GemmPlan t = p;
+  t.rows_dev = scratch;
+  t.stop_dev = nullptr;
+  t.sched = scratch + 1;
+  t.idle = false;
+  std::vector<cudaEvent_t> ev(2 * reps);
+  for (auto& x : ev) AB_CUDA(cudaEventCreate(&x));
+  for (int r = 0; r < reps; ++r) {
+    if (flush) AB_CUDA(cudaMemsetAsync(flush, r & 0xff, flush_bytes, s));
+    AB_CUDA(cudaEventRecord(ev[2 * r], s));
+    gemm_launch(t, s);
+    AB_CUDA(cudaEventRecord(ev[2 * r + 1], s));
+  }
+  AB_CUDA(cudaStreamSynchronize(s));
+  std::vector<float> ms(reps);
+  for (int r = 0; r < reps; ++r) AB_CUDA(cudaEventElapsedTime(&ms[r], ev[2 * r], ev[2 * r + 1]));
+  for (auto& x : ev) cudaEventDestroy(x);
+  std::sort(ms.begin(), ms.end());
+  return 1e3 * ms[reps / 2];
 }
 
 void gemm_partition(GemmPlan& a, GemmPlan& b) {
@@ -1177,6 +1248,7 @@ void make_tmap_bf16(CUtensorMap* m, const void* ptr, int64_t rows, int64_t cols,
 }
 
 void gemm_launch(const GemmPlan& p, cudaStream_t s) {
+  if (p.idle) return;
   switch (p.epi) {
     case kEpiBF16: launch_t<kEpiBF16>(p, s); break;
     case kEpiF32: launch_t<kEpiF32>(p, s); break;

@@ -5,6 +5,8 @@
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
+#include <vector>
+
 #include "common.cuh"
 
 namespace ab {
@@ -41,6 +43,7 @@ struct GemmPlan {
   // no-swap schedule with -force weight rows per tile, 0 = on-device choice
   int force = 0;
   const int* sched = nullptr;  // device table: packed schedule per live row count [0, M_cap]
+  bool idle = false;           // the table is all zeros: gemm_launch skips the launch
 };
 
 void gemm_plan(GemmPlan& p, const __nv_bfloat16* W, int N, int K, const __nv_bfloat16* A, int M_cap, int64_t lda,
@@ -51,6 +54,13 @@ void gemm_plan(GemmPlan& p, const __nv_bfloat16* W, int N, int K, const __nv_bfl
 // launch exits at once.  Both plans are launched every time.
 void gemm_partition(GemmPlan& a, GemmPlan& b);
 void gemm_launch(const GemmPlan& p, cudaStream_t s);
+// Autotuning (engine creation): the fixed schedule codes valid for the plan at `rows`; the
+// median device time (us) of `reps` launches of one code at `rows` (L2 flushed before each by
+// a memset of `flush`); install a per-row-count table built from measurements.
+std::vector<int> gemm_candidates(const GemmPlan& p, int rows);
+double gemm_time_code(const GemmPlan& p, int rows, int code, int reps, void* flush, size_t flush_bytes,
+                      cudaStream_t s);
+void gemm_set_table(GemmPlan& p, const std::vector<int>& tab);
 // Rebuild the plan's schedule table (force: see GemmPlan::force).
 void gemm_set_schedule(GemmPlan& p, int force);
 

@@ -293,7 +293,7 @@ __global__ void k_rope_kv(ModelDev m, int layer, const bf16* __restrict__ qkv, c
   const int page = m.bt[(size_t)m.row_btrow[r] * m.MP + pos / m.P], slot = pos % m.P;
   const float2* rp = m.rope + (size_t)pos * (HD / 2);
   const bf16* src = qkv + (size_t)r * m.qkv_dim;
-  for (int head = warp; head < m.hq + 2 * m.hk; head += nw) {
+  for (int head = warp + blockIdx.y * nw; head < m.hq + 2 * m.hk; head += nw * gridDim.y) {
     const bf16* hv = src + head * HD;
     float a[NP], b[NP];
     load_pairs<NP>(hv + lane * NP, a);
@@ -335,56 +335,90 @@ __global__ void k_rope_kv(ModelDev m, int layer, const bf16* __restrict__ qkv, c
   }
 }
 
-// ---------------------------------------------------------------------------
-// causal prefill attention over a prompt group's own tokens (paged K/V)
-// one warp per (row, q head)
-// ---------------------------------------------------------------------------
-
+// Decode variant: the QKV GEMM reduce-adds its fp32 accumulator into a zeroed workspace (so it can
+// split K); this kernel adds the bias, rounds to bf16 exactly where the bf16 GEMM epilogue would
+// have (bf16(acc + bias)), runs the same q/k-norm + RoPE + paged KV write, and zeroes the rows it
+// consumed for the next layer's GEMM.
 template <int HD>
-__global__ void k_prefill_attn(ModelDev m, int layer, const bf16* __restrict__ q, bf16* __restrict__ out,
-                               const int* __restrict__ seg_start, const int* __restrict__ seg_group, int n_seg,
-                               int rows) {
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int r = blockIdx.x * (blockDim.x >> 5) + warp;
+__global__ void k_rope_kv_f32(ModelDev m, int layer, float* __restrict__ qkv, const bf16* __restrict__ bias,
+                              const bf16* __restrict__ qn, const bf16* __restrict__ kn, bf16* __restrict__ qout,
+                              const int* rows_dev, int rows_cap, const int* stop) {
+  pdl_wait();
+  if (stopped(stop)) return;
+  const int rows = rows_dev ? min(*rows_dev, rows_cap) : rows_cap;
+  const int r = blockIdx.x;
   if (r >= rows) return;
-  const int head = blockIdx.y, kvh = head / m.gq;
-  int lo = 0, hi = n_seg - 1;
-  while (lo < hi) {  // last segment with start <= r
-    const int mid = (lo + hi + 1) >> 1;
-    if (seg_start[mid] <= r)
-      lo = mid;
-    else
-      hi = mid - 1;
+  constexpr int NP = HD / 64;  // rotation pairs per lane
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+  const int pos = m.row_pos[r];
+  const int page = m.bt[(size_t)m.row_btrow[r] * m.MP + pos / m.P], slot = pos % m.P;
+  const float2* rp = m.rope + (size_t)pos * (HD / 2);
+  float* src = qkv + (size_t)r * m.qkv_dim;
+  for (int head = warp + blockIdx.y * nw; head < m.hq + 2 * m.hk; head += nw * gridDim.y) {
+    float* hv = src + head * HD;
+    float a[NP], b[NP];
+    static_assert(NP == 1 || NP == 2, "rotation pairs per lane");
+    float ba[NP] = {}, bb[NP] = {};
+    if (bias) {
+      load_pairs<NP>(bias + head * HD + lane * NP, ba);
+      load_pairs<NP>(bias + head * HD + lane * NP + HD / 2, bb);
+    }
+    if constexpr (NP == 2) {
+      float2* pa = reinterpret_cast<float2*>(hv + lane * 2);
+      float2* pb = reinterpret_cast<float2*>(hv + lane * 2 + HD / 2);
+      const float2 va = __ldcg(pa), vb = __ldcg(pb);
+      a[0] = va.x;
+      a[1] = va.y;
+      b[0] = vb.x;
+      b[1] = vb.y;
+      __stcg(pa, make_float2(0.f, 0.f));
+      __stcg(pb, make_float2(0.f, 0.f));
+    } else {
+      a[0] = __ldcg(hv + lane);
+      b[0] = __ldcg(hv + lane + HD / 2);
+      __stcg(hv + lane, 0.f);
+      __stcg(hv + lane + HD / 2, 0.f);
+    }
+#pragma unroll
+    for (int j = 0; j < NP; ++j) {
+      a[j] = __bfloat162float(__float2bfloat16(a[j] + ba[j]));
+      b[j] = __bfloat162float(__float2bfloat16(b[j] + bb[j]));
+    }
+    if (head >= m.hq + m.hk) {  // V: straight into the page
+      const int kvh = head - m.hq - m.hk;
+      bf16* dst = m.kv + m.kv_off(layer, page, 1, kvh, slot);
+      store_pairs<NP>(dst + lane * NP, a);
+      store_pairs<NP>(dst + lane * NP + HD / 2, b);
+      continue;
+    }
+    const bool is_q = head < m.hq;
+    if (m.qk_norm) {
+      float ss = 0.f;
+#pragma unroll
+      for (int j = 0; j < NP; ++j) ss += a[j] * a[j] + b[j] * b[j];
+      ss = warp_sum(ss);
+      const float rs = rsqrtf(ss / (float)HD + m.eps);
+      const bf16* nw_ = is_q ? qn : kn;
+      float wa[NP], wb[NP];
+      load_pairs<NP>(nw_ + lane * NP, wa);
+      load_pairs<NP>(nw_ + lane * NP + HD / 2, wb);
+#pragma unroll
+      for (int j = 0; j < NP; ++j) {
+        a[j] = __bfloat162float(__float2bfloat16(a[j] * rs * wa[j]));
+        b[j] = __bfloat162float(__float2bfloat16(b[j] * rs * wb[j]));
+      }
+    }
+    float oa[NP], ob[NP];
+#pragma unroll
+    for (int j = 0; j < NP; ++j) {
+      const float2 cs = rp[lane * NP + j];
+      oa[j] = a[j] * cs.x - b[j] * cs.y;
+      ob[j] = b[j] * cs.x + a[j] * cs.y;
+    }
+    bf16* dst = is_q ? qout + (size_t)r * m.qd + head * HD : m.kv + m.kv_off(layer, page, 0, head - m.hq, slot);
+    store_pairs<NP>(dst + lane * NP, oa);
+    store_pairs<NP>(dst + lane * NP + HD / 2, ob);
   }
-  const int p = r - seg_start[lo];
-  const int32_t* bt = m.bt + (size_t)(m.H + seg_group[lo]) * m.MP;
-  constexpr int E = HD / 32;
-  float qv[E], acc[E];
-  const bf16* qr = q + (size_t)r * m.qd + head * HD;
-#pragma unroll
-  for (int j = 0; j < E; ++j) {
-    qv[j] = __bfloat162float(qr[lane * E + j]) * rsqrtf((float)HD) * kLog2e;
-    acc[j] = 0.f;
-  }
-  float mx = -FLT_MAX, l = 0.f;
-  for (int t = 0; t <= p; ++t) {
-    const int page = bt[t / m.P], slot = t % m.P;
-    const bf16* k = m.kv + m.kv_off(layer, page, 0, kvh, slot);
-    float s = 0.f;
-#pragma unroll
-    for (int j = 0; j < E; ++j) s += qv[j] * __bfloat162float(k[lane * E + j]);
-    s = warp_sum(s);
-    const float mn = fmaxf(mx, s);
-    const float a = exp2f(mx - mn), pw = exp2f(s - mn);
-    l = l * a + pw;
-    const bf16* v = m.kv + m.kv_off(layer, page, 1, kvh, slot);
-#pragma unroll
-    for (int j = 0; j < E; ++j) acc[j] = acc[j] * a + pw * __bfloat162float(v[lane * E + j]);
-    mx = mn;
-  }
-  bf16* o = out + (size_t)r * m.qd + head * HD;
-#pragma unroll
-  for (int j = 0; j < E; ++j) o[lane * E + j] = __float2bfloat16(acc[j] / l);
 }
 
 // ---------------------------------------------------------------------------
@@ -430,6 +464,61 @@ __global__ void k_fork_copy(ModelDev m, const int32_t* tail_src, const int32_t* 
   const uint4* s = reinterpret_cast<const uint4*>(m.kv + m.kv_off(layer, src, 0, 0, 0));
   uint4* d = reinterpret_cast<uint4*>(m.kv + m.kv_off(layer, dst, 0, 0, 0));
   for (size_t j = threadIdx.x; j < n; j += blockDim.x) d[j] = s[j];
+}
+
+// Re-prefill resume (§8 f1): a paused sample whose private KV was dropped at the abort
+// re-forks its group's prompt pages (full pages shared, the partial tail page copied) and
+// gets fresh pages for every position up to its context; the rows for positions
+// g_ctx .. g_ctx + gen - 1 are then recomputed by the prefill pass.  items[k] = {handle,
+// group slot, generated tokens, -}.
+__global__ void k_resume_fork(EngineDev e, ModelDev m, const int4* items, int n, int32_t* tail_src,
+                              int32_t* tail_dst) {
+  Ctl* c = e.ctl;
+  const int k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= n) return;
+  tail_src[k] = -1;
+  const int4 it = items[k];
+  const int h = it.x, g = it.y, gen = it.z;
+  const int ctx_g = m.g_ctx[g];
+  const int nfull = ctx_g / m.P;
+  const int ctx = ctx_g + gen;
+  const int need = (ctx + m.P - 1) / m.P;
+  const int32_t* gb = m.bt + (size_t)(m.H + g) * m.MP;
+  int32_t* hb = m.bt + (size_t)h * m.MP;
+  for (int j = 0; j < nfull; ++j) hb[j] = gb[j];
+  m.h_shared[h] = nfull;
+  for (int j = nfull; j < need; ++j) {
+    const int idx = pop_page(c);
+    if (idx < 0 || j >= m.MP) {
+      atomicCAS(&c->error, kErrNone, kErrOutOfKV);
+      m.h_ctx[h] = j * m.P;  // what is allocated, so a release frees exactly it
+      return;
+    }
+    hb[j] = m.free_pages[idx];
+  }
+  m.h_ctx[h] = ctx;
+  m.h_last_tok[h] = e.h_tokens[(size_t)h * e.L + gen - 1];
+  if (ctx_g % m.P) {
+    tail_src[k] = gb[nfull];
+    tail_dst[k] = hb[nfull];
+  }
+}
+
+// Prefill rows of resumed samples: pieces[k] = {handle, group slot, first generated index j0,
+// first row}; piece k covers rows [pieces[k].w, pieces[k+1].w).  Row for generated index j
+// sits at position g_ctx + j and feeds token j - 1 (j = 0: the prompt's last token).
+__global__ void k_extend_rows(EngineDev e, ModelDev m, const int4* pieces, int n_pieces) {
+  const int k = blockIdx.x;
+  if (k >= n_pieces) return;
+  const int4 p = pieces[k];
+  const int rend = pieces[k + 1].w;
+  const int ctx_g = m.g_ctx[p.y];
+  for (int r = p.w + threadIdx.x; r < rend; r += blockDim.x) {
+    const int j = p.z + (r - p.w);
+    m.row_tok[r] = j == 0 ? m.g_last_tok[p.y] : e.h_tokens[(size_t)p.x * e.L + j - 1];
+    m.row_pos[r] = ctx_g + j;
+    m.row_btrow[r] = p.x;
+  }
 }
 
 __global__ void k_release(EngineDev e, ModelDev m, const int32_t* handles, int n) {
@@ -528,24 +617,29 @@ void launch_rmsnorm(const float* x, const bf16* w, bf16* out, int d, float eps, 
   }
 }
 
+// q / k / v heads per row spread over blockIdx.y so that each warp owns one head (a latency-bound
+// kernel: a short dependent chain per warp, many warps)
+static int rope_hy(const ModelDev& m) { return ceil_div(m.hq + 2 * m.hk, 8); }
+
 void launch_rope_kv(const ModelDev& m, int layer, const bf16* qkv, const bf16* q_norm, const bf16* k_norm, bf16* q_out,
                     const int* rows_dev, int rows_cap, const int* stop, cudaStream_t s) {
   if (m.hd == 128)
-    launch_pdl(k_rope_kv<128>, dim3(rows_cap), dim3(256), 0, s, m, layer, qkv, q_norm, k_norm, q_out, rows_dev, rows_cap,
+    launch_pdl(k_rope_kv<128>, dim3(rows_cap, rope_hy(m)), dim3(256), 0, s, m, layer, qkv, q_norm, k_norm, q_out, rows_dev, rows_cap,
                stop);
   else
-    launch_pdl(k_rope_kv<64>, dim3(rows_cap), dim3(256), 0, s, m, layer, qkv, q_norm, k_norm, q_out, rows_dev, rows_cap,
+    launch_pdl(k_rope_kv<64>, dim3(rows_cap, rope_hy(m)), dim3(256), 0, s, m, layer, qkv, q_norm, k_norm, q_out, rows_dev, rows_cap,
                stop);
 }
 
-void launch_prefill_attention(const ModelDev& m, int layer, const bf16* q, bf16* out, const int* seg_start,
-                              const int* seg_group, int n_seg, int rows, int max_len, cudaStream_t s) {
-  (void)max_len;
-  dim3 grid(ceil_div(rows, 4), m.hq);
+void launch_rope_kv_f32(const ModelDev& m, int layer, float* qkv, const bf16* bias, const bf16* q_norm,
+                        const bf16* k_norm, bf16* q_out, const int* rows_dev, int rows_cap, const int* stop,
+                        cudaStream_t s) {
   if (m.hd == 128)
-    k_prefill_attn<128><<<grid, 128, 0, s>>>(m, layer, q, out, seg_start, seg_group, n_seg, rows);
+    launch_pdl(k_rope_kv_f32<128>, dim3(rows_cap, rope_hy(m)), dim3(256), 0, s, m, layer, qkv, bias, q_norm, k_norm, q_out,
+               rows_dev, rows_cap, stop);
   else
-    k_prefill_attn<64><<<grid, 128, 0, s>>>(m, layer, q, out, seg_start, seg_group, n_seg, rows);
+    launch_pdl(k_rope_kv_f32<64>, dim3(rows_cap, rope_hy(m)), dim3(256), 0, s, m, layer, qkv, bias, q_norm, k_norm, q_out,
+               rows_dev, rows_cap, stop);
 }
 
 void launch_fork_groups(const EngineDev& e, const ModelDev& m, const ab_sample_desc* descs, int n, cudaStream_t s) {
@@ -558,6 +652,22 @@ void launch_fork_groups(const EngineDev& e, const ModelDev& m, const ab_sample_d
   }
   k_fork_meta<<<ceil_div(n, 128), 128, 0, s>>>(e, m, descs, n, buf, buf + cap);
   k_fork_copy<<<dim3(n, m.L), 256, 0, s>>>(m, buf, buf + cap);
+}
+
+void launch_resume_fork(const EngineDev& e, const ModelDev& m, const int4* items, int n, cudaStream_t s) {
+  static int32_t* buf = nullptr;
+  static int cap = 0;
+  if (n > cap) {
+    if (buf) cudaFree(buf);
+    cap = n + 1024;
+    AB_CUDA(cudaMalloc(&buf, sizeof(int32_t) * 2 * cap));
+  }
+  k_resume_fork<<<ceil_div(n, 128), 128, 0, s>>>(e, m, items, n, buf, buf + cap);
+  k_fork_copy<<<dim3(n, m.L), 256, 0, s>>>(m, buf, buf + cap);
+}
+
+void launch_extend_rows(const EngineDev& e, const ModelDev& m, const int4* pieces, int n_pieces, cudaStream_t s) {
+  k_extend_rows<<<n_pieces, 256, 0, s>>>(e, m, pieces, n_pieces);
 }
 
 void launch_release_handles(const EngineDev& e, const ModelDev& m, const int32_t* handles, int n, cudaStream_t s) {

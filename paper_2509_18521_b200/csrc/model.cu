@@ -8,7 +8,11 @@
 #include <cuda_bf16.h>
 
 #include <algorithm>
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
+#include <map>
 #include <string>
 #include <vector>
 
@@ -33,25 +37,37 @@ struct Model {
   int S = 0, M_pf = 0, rows_cap = 0;
   float *x = nullptr, *logits = nullptr, *part_o = nullptr, *part_ml = nullptr;
   bf16 *xn = nullptr, *qkv = nullptr, *qrot = nullptr, *attn = nullptr, *hbuf = nullptr;
+  float* qkv32 = nullptr;
   int max_splits = 1, chunk = 256;
   struct Plans {
     GemmPlan qkv, o, gu, down;
     // decode only: the same QKV / O / down products on clusters of 2 (148 CTAs, split-K <= 2);
     // gemm_partition gives each row count to the faster of the pair of plans
     GemmPlan qkv2, o2, down2;
+    GemmPlan gu2;  // decode gate-up on a cluster-of-8 (non-pair) plan: small row counts (autotuned)
   };
   std::vector<Plans> dec, pf;
   GemmPlan lm_dec;
   int* pf_rows = nullptr;  // device row count for prefill GEMMs
   CUtensorMap kvmap;         // TMA view of the KV pool for the decode attention
-  int32_t *seg_start = nullptr, *seg_group = nullptr, *ga_g = nullptr, *ga_len = nullptr, *ga_last = nullptr;
+  int32_t *ga_g = nullptr, *ga_len = nullptr, *ga_last = nullptr;
   int32_t* host_stage = nullptr;
   size_t host_stage_cap = 0;
   struct PendingGroup {
     int g;
     std::vector<int32_t> prompt;
+    bool in_place;  // re-prefill of a resident group's prompt (pages already allocated)
   };
   std::vector<PendingGroup> pending;
+  // causal attention blocks of a prefill chunk ({first row, rows, block-table row, first position})
+  int4 *pf_blocks = nullptr, *pf_blocks_host = nullptr;
+  int pf_blocks_cap = 0;
+  // KV re-prefill mode (§8 f1): prompts of resident groups, their prefilled context, evicted handles
+  std::map<int, std::vector<int32_t>> prompts;
+  std::vector<int32_t> g_ctx_host;
+  std::vector<char> evicted;
+  int4 *rs_items = nullptr, *rs_pieces = nullptr;
+  int64_t last_version = -1;
   float inv_temp = 1.f;
 };
 
@@ -75,6 +91,85 @@ int pick_bn(int rows) {
 }
 
 }  // namespace
+
+// Decode GEMM autotuning: for every projection, each of its alternative plans (cluster-8 split-K,
+// cluster-1 reduce-add / cluster-2, CTA pair) and every valid fixed schedule is timed on this GPU
+// at a ladder of live row counts (L2 flushed before each launch); each row count then runs the
+// fastest (plan, schedule) and the other plan's table entry is 0.  Layers share shapes, so layer 0
+// is tuned and its tables are installed on every layer; results are cached per process.
+static void autotune_decode(Engine& e, Model* M) {
+  static std::map<std::string, std::vector<std::vector<int>>> cache;
+  const char* lv = getenv("AB_AUTOTUNE_LOG");
+  const bool log = lv != nullptr, log_all = lv && lv[0] == '2';
+  cudaStream_t s = e.stream;
+  const int S = M->S;
+  std::vector<int> ladder;
+  for (int r : {1, 2, 4, 8, 12, 16, 24, 32, 40, 48, 56, 64, 80, 96, 112, 128, 160, 192, 224, 256, 320, 384, 448, 512,
+                640, 768, 896, 1024, 1280, 1536, 1792, 2048})
+    if (r < S) ladder.push_back(r);
+  ladder.push_back(S);
+  void* flush = nullptr;
+  const size_t flush_bytes = (size_t)192 << 20;  // > L2 (126 MB)
+  auto key_of = [&](const std::vector<GemmPlan*>& g) {
+    std::string k;
+    for (auto* p : g)
+      k += std::to_string(p->N) + "," + std::to_string(p->K) + "," + std::to_string(p->epi) + "," +
+           std::to_string(p->M_cap) + "," + std::to_string(p->BN) + "," + std::to_string(p->cluster) + "," +
+           std::to_string(p->pair) + "," + std::to_string(p->nondet) + "," + std::to_string(p->grid) + ";";
+    return k;
+  };
+  auto tune = [&](std::vector<GemmPlan*> g) -> std::vector<std::vector<int>> {
+    const std::string key = key_of(g);
+    auto it = cache.find(key);
+    if (it != cache.end()) return it->second;
+    if (!flush) AB_CUDA(cudaMalloc(&flush, flush_bytes));
+    std::vector<std::vector<int>> tabs(g.size(), std::vector<int>(S + 1, 0));
+    int lo = 1;
+    for (int r : ladder) {
+      double best = 1e30;
+      int bp = -1, bc = 0;
+      for (size_t i = 0; i < g.size(); ++i)
+        for (int c : gemm_candidates(*g[i], r)) {
+          if (log_all) {
+            fprintf(stderr, "[autotune]   try N=%d K=%d rows=%d plan=%zu code=0x%x\n", g[i]->N, g[i]->K, r, i, c);
+            fflush(stderr);
+          }
+          const double us = gemm_time_code(*g[i], r, c, 3, flush, flush_bytes, s);
+          if (us < best) {
+            best = us;
+            bp = (int)i;
+            bc = c;
+          }
+        }
+      if (bp >= 0)
+        for (int x = lo; x <= r; ++x) tabs[bp][x] = bc;
+      if (log)
+        fprintf(stderr, "[autotune] N=%d K=%d epi=%d rows=%d plan=%d (cluster %d%s) code=0x%x %.1f us\n", g[0]->N,
+                g[0]->K, g[0]->epi, r, bp, bp >= 0 ? g[bp]->cluster : 0, bp >= 0 && g[bp]->pair ? " pair" : "", bc,
+                best);
+      lo = r + 1;
+    }
+    cache[key] = tabs;
+    return tabs;
+  };
+  const int L = (int)M->dec.size();
+  auto apply = [&](GemmPlan Model::Plans::*a, GemmPlan Model::Plans::*b) {
+    std::vector<GemmPlan*> g = {&(M->dec[0].*a), &(M->dec[0].*b)};
+    const auto tabs = tune(g);
+    for (int l = 0; l < L; ++l) {
+      gemm_set_table(M->dec[l].*a, tabs[0]);
+      gemm_set_table(M->dec[l].*b, tabs[1]);
+    }
+  };
+  apply(&Model::Plans::qkv, &Model::Plans::qkv2);
+  apply(&Model::Plans::o, &Model::Plans::o2);
+  apply(&Model::Plans::down, &Model::Plans::down2);
+  apply(&Model::Plans::gu, &Model::Plans::gu2);
+  if (flush) AB_CUDA(cudaFree(flush));
+  // the timing runs accumulated into the decode workspaces: the QKV accumulator must start at zero
+  AB_CUDA(cudaMemsetAsync(M->qkv32, 0, sizeof(float) * (size_t)S * M->md.qkv_dim, s));
+  AB_CUDA(cudaStreamSynchronize(s));
+}
 
 Model* model_create(Engine& e) {
   const ab_model_config& c = e.mcfg;
@@ -167,6 +262,7 @@ Model* model_create(Engine& e) {
   M->x = dalloc<float>(R * m.d);
   M->xn = dalloc<bf16>(R * std::max(m.d, m.f));
   M->qkv = dalloc<bf16>(R * m.qkv_dim);
+  M->qkv32 = dalloc<float>((size_t)M->S * m.qkv_dim);  // decode QKV accumulator (kept zeroed between uses)
   M->qrot = dalloc<bf16>(R * m.qd);
   M->attn = dalloc<bf16>(R * m.qd);
   M->hbuf = dalloc<bf16>(R * m.f);
@@ -194,11 +290,16 @@ Model* model_create(Engine& e) {
   m.rope = dalloc<float2>((size_t)m.max_pos * (m.hd / 2));
   launch_rope_table(m.rope, m.max_pos, m.hd, c.rope_theta, s);
   M->pf_rows = dalloc<int>(1);
-  M->seg_start = dalloc<int32_t>(M->M_pf + 1);
-  M->seg_group = dalloc<int32_t>(M->M_pf + 1);
   M->ga_g = dalloc<int32_t>(M->M_pf + 1);
   M->ga_len = dalloc<int32_t>(M->M_pf + 1);
   M->ga_last = dalloc<int32_t>(M->M_pf + 1);
+  M->pf_blocks_cap = M->M_pf / 64 + M->M_pf + 16;  // a chunk holds <= M_pf rows, each piece adds one block
+  M->pf_blocks = dalloc<int4>(M->pf_blocks_cap);
+  AB_CUDA(cudaMallocHost(&M->pf_blocks_host, sizeof(int4) * M->pf_blocks_cap));
+  M->rs_items = dalloc<int4>(m.H + 1);
+  M->rs_pieces = dalloc<int4>(M->M_pf + 2);
+  M->g_ctx_host.assign(m.G_cap, 0);
+  M->evicted.assign(m.H, 0);
   M->host_stage_cap = (size_t)8 * (M->M_pf + 16);
   AB_CUDA(cudaMallocHost(&M->host_stage, sizeof(int32_t) * M->host_stage_cap));
 
@@ -233,28 +334,33 @@ Model* model_create(Engine& e) {
   for (int l = 0; l < m.L; ++l) {
     const LayerW& w = M->layers[l];
     Model::Plans d, p;
-    gemm_plan(d.qkv, w.wqkv, m.qkv_dim, m.d, M->xn, M->S, m.d, bn_dec, kEpiBF16, M->qkv, m.qkv_dim, w.bqkv, b, stop,
-              8);
+    const bool nd = ec.nondeterministic_gemm != 0;
+    // decode QKV: fp32 accumulator reduce-added into a zeroed workspace (it may then split K like the
+    // residual GEMMs); bias, bf16 rounding and RoPE / KV write happen in k_rope_kv_f32
+    gemm_plan(d.qkv, w.wqkv, m.qkv_dim, m.d, M->xn, M->S, m.d, bn_dec, kEpiAddF32, M->qkv32, m.qkv_dim, nullptr, b,
+              stop, 8);
     gemm_plan(d.o, w.wo, m.d, m.qd, M->attn, M->S, m.qd, bn_dec, kEpiAddF32, M->x, m.d, nullptr, b, stop, 8);
     gemm_plan(d.gu, w.wgu, 2 * m.f, m.d, M->xn, M->S, m.d, bn_dec, kEpiSwiGLU, M->hbuf, m.f, nullptr, b, stop,
               2, true);
     gemm_plan(d.down, w.wd, m.d, m.f, M->hbuf, M->S, m.f, bn_dec, kEpiAddF32, M->x, m.d, nullptr, b, stop, 8);
-    gemm_plan(d.qkv2, w.wqkv, m.qkv_dim, m.d, M->xn, M->S, m.d, bn_dec, kEpiBF16, M->qkv, m.qkv_dim, w.bqkv, b,
-              stop, 2);
+    gemm_plan(d.qkv2, w.wqkv, m.qkv_dim, m.d, M->xn, M->S, m.d, bn_dec, kEpiAddF32, M->qkv32, m.qkv_dim, nullptr, b,
+              stop, nd ? 1 : 2);
     // fp32 residual GEMMs: the second plan is either a cluster-of-2 plan (deterministic) or, when
     // the engine allows it, a cluster-of-1 plan whose split-K partials are reduce-added by TMA
-    const bool nd = ec.nondeterministic_gemm != 0;
     gemm_plan(d.o2, w.wo, m.d, m.qd, M->attn, M->S, m.qd, bn_dec, kEpiAddF32, M->x, m.d, nullptr, b, stop, nd ? 1 : 2);
     gemm_plan(d.down2, w.wd, m.d, m.f, M->hbuf, M->S, m.f, bn_dec, kEpiAddF32, M->x, m.d, nullptr, b, stop,
               nd ? 1 : 2);
     if (nd) {
-      d.o2.nondet = d.down2.nondet = true;
+      d.qkv2.nondet = d.o2.nondet = d.down2.nondet = true;
+      gemm_set_schedule(d.qkv2, 0);
       gemm_set_schedule(d.o2, 0);
       gemm_set_schedule(d.down2, 0);
     }
     gemm_partition(d.qkv, d.qkv2);
     gemm_partition(d.o, d.o2);
     gemm_partition(d.down, d.down2);
+    gemm_plan(d.gu2, w.wgu, 2 * m.f, m.d, M->xn, M->S, m.d, bn_dec, kEpiSwiGLU, M->hbuf, m.f, nullptr, b, stop, 8);
+    gemm_set_table(d.gu2, std::vector<int>(M->S + 1, 0));  // idle unless the autotuner picks it
     gemm_plan(p.qkv, w.wqkv, m.qkv_dim, m.d, M->xn, M->M_pf, m.d, 256, kEpiBF16, M->qkv, m.qkv_dim, w.bqkv,
               M->pf_rows, nullptr);
     gemm_plan(p.o, w.wo, m.d, m.qd, M->attn, M->M_pf, m.qd, 256, kEpiAddF32, M->x, m.d, nullptr, M->pf_rows,
@@ -267,6 +373,7 @@ Model* model_create(Engine& e) {
     M->pf.push_back(p);
   }
   gemm_plan(M->lm_dec, M->lm_head, m.V, m.d, M->xn, M->S, m.d, bn_dec, kEpiF32, M->logits, m.V, nullptr, b, stop, 2, true);
+  if (ec.gemm_autotune) autotune_decode(e, M);
   M->inv_temp = ec.greedy ? 1.f / std::max(ec.temperature, 1e-6f) : 1.f / ec.temperature;
   if (ec.temperature <= 0.f) M->inv_temp = 1.f;
   AB_CUDA(cudaStreamSynchronize(s));
@@ -276,14 +383,16 @@ Model* model_create(Engine& e) {
 void model_destroy(Model* M) {
   if (!M) return;
   ModelDev& m = M->md;
-  void* ptrs[] = {M->wbuf,     M->x,        M->xn,        M->qkv,       M->qrot,      M->attn,     M->hbuf,
+  void* ptrs[] = {M->wbuf,     M->x,        M->xn,        M->qkv,       M->qkv32,     M->qrot,     M->attn,     M->hbuf,
                   M->logits,   M->part_o,   M->part_ml,   m.row_tok,    m.row_pos,    m.row_btrow, m.h_ctx,
                   m.h_last_tok, m.h_shared, m.g_ctx,      m.g_last_tok, m.g_npages,   m.bt,        m.rope,
-                  M->pf_rows,  M->seg_start, M->seg_group, M->ga_g,     M->ga_len,    M->ga_last,  m.kv,
-                  m.free_pages, m.split_prefix, m.att_counter, m.att_ctl};
+                  M->pf_rows,  M->ga_g,     M->ga_len,    M->ga_last,  m.kv,
+                  m.free_pages, m.split_prefix, m.att_counter, m.att_ctl, M->pf_blocks, M->rs_items,
+                  M->rs_pieces};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   if (M->host_stage) cudaFreeHost(M->host_stage);
+  if (M->pf_blocks_host) cudaFreeHost(M->pf_blocks_host);
   delete M;
 }
 
@@ -305,13 +414,51 @@ void model_open_group(Engine& e, int group_slot, const int32_t* prompt, int prom
   AB_REQUIRE(prompt_len <= e.cfg.max_prompt, AB_ERR_CONTRACT, "prompt longer than max_prompt");
   for (int i = 0; i < prompt_len; ++i)
     AB_REQUIRE(prompt[i] >= 0 && prompt[i] < M->md.V, AB_ERR_CONTRACT, "prompt token out of vocabulary");
-  M->pending.push_back({group_slot, std::vector<int32_t>(prompt, prompt + prompt_len)});
+  M->pending.push_back({group_slot, std::vector<int32_t>(prompt, prompt + prompt_len), false});
+  if (e.cfg.kv_resume) M->prompts[group_slot] = M->pending.back().prompt;
 }
 
 static void check_kv(Engine& e) {
   AB_CUDA(cudaMemcpyAsync(&e.ctl_host->error, &e.d.ctl->error, sizeof(int32_t), cudaMemcpyDeviceToHost, e.stream));
   AB_CUDA(cudaStreamSynchronize(e.stream));
   if (e.ctl_host->error == kErrOutOfKV) throw Error(AB_ERR_OUT_OF_KV, "KV page pool exhausted");
+}
+
+// Append the causal-attention blocks (<= 64 rows) of one run of rows of a sequence.
+static int add_blocks(Model* M, int nb, int row0, int n, int btrow, int pos0) {
+  for (int i = 0; i < n; i += 64) {
+    AB_REQUIRE(nb < M->pf_blocks_cap, AB_ERR_CONFIG, "prefill block list overflow");
+    M->pf_blocks_host[nb++] = make_int4(row0 + i, std::min(64, n - i), btrow, pos0 + i);
+  }
+  return nb;
+}
+
+// Prefill forward over R rows already described on the device (row_tok / row_pos / row_btrow):
+// writes every row's K / V into its pages.  Attention blocks go longest-context first.
+static void prefill_rows(Engine& e, int R, int nb) {
+  Model* M = e.model;
+  ModelDev& m = M->md;
+  cudaStream_t s = e.stream;
+  std::sort(M->pf_blocks_host, M->pf_blocks_host + nb,
+            [](const int4& x, const int4& y) { return x.w + x.y > y.w + y.y; });
+  AB_CUDA(cudaMemcpyAsync(M->pf_blocks, M->pf_blocks_host, sizeof(int4) * nb, cudaMemcpyHostToDevice, s));
+  AB_CUDA(cudaMemcpyAsync(M->pf_rows, &R, sizeof(int), cudaMemcpyHostToDevice, s));
+  launch_embed(m, M->embed, M->x, nullptr, R, nullptr, s);
+  for (int l = 0; l < m.L; ++l) {
+    const LayerW& w = M->layers[l];
+    const Model::Plans& p = M->pf[l];
+    launch_rmsnorm(M->x, w.attn_norm, M->xn, m.d, m.eps, nullptr, R, nullptr, s);
+    gemm_launch(p.qkv, s);
+    launch_rope_kv(m, l, M->qkv, w.q_norm, w.k_norm, M->qrot, nullptr, R, nullptr, s);
+    launch_prefill_flash(m, l, M->qrot, M->attn, M->pf_blocks, nb, s);
+    gemm_launch(p.o, s);
+    launch_rmsnorm(M->x, w.mlp_norm, M->xn, m.d, m.eps, nullptr, R, nullptr, s);
+    gemm_launch(p.gu, s);
+    gemm_launch(p.down, s);
+  }
+  AB_CUDA(cudaGetLastError());
+  AB_CUDA(cudaStreamSynchronize(s));  // host staging is reused by the next chunk
+  e.launches += 1 + 8 * (int64_t)m.L;
 }
 
 // Prefill every pending prompt group (positions 0..len-2) in packed chunks.
@@ -333,67 +480,138 @@ static void flush_prefill(Engine& e) {
     int32_t* tok = hs;
     int32_t* pos = tok + R;
     int32_t* btr = pos + R;
-    int32_t* segs = btr + R;
-    int32_t* segg = segs + ng + 1;
-    int32_t* gg = segg + ng;
+    int32_t* gg = btr + R;
     int32_t* gl = gg + ng;
     int32_t* glast = gl + ng;
-    int r = 0;
+    int r = 0, na = 0, nb = 0;
     for (int j = 0; j < ng; ++j) {
       const auto& pg = M->pending[k + j];
       const int len = (int)pg.prompt.size() - 1;
-      segs[j] = r;
-      segg[j] = pg.g;
-      gg[j] = pg.g;
-      gl[j] = len;
-      glast[j] = pg.prompt[len];
+      if (!pg.in_place) {
+        gg[na] = pg.g;
+        gl[na] = len;
+        glast[na] = pg.prompt[len];
+        ++na;
+      }
+      M->g_ctx_host[pg.g] = len;
+      nb = add_blocks(M, nb, r, len, m.H + pg.g, 0);
       for (int t = 0; t < len; ++t, ++r) {
         tok[r] = pg.prompt[t];
         pos[r] = t;
         btr[r] = m.H + pg.g;
       }
     }
-    segs[ng] = R;
     AB_CUDA(cudaMemcpyAsync(m.row_tok, tok, sizeof(int32_t) * R, cudaMemcpyHostToDevice, s));
     AB_CUDA(cudaMemcpyAsync(m.row_pos, pos, sizeof(int32_t) * R, cudaMemcpyHostToDevice, s));
     AB_CUDA(cudaMemcpyAsync(m.row_btrow, btr, sizeof(int32_t) * R, cudaMemcpyHostToDevice, s));
-    AB_CUDA(cudaMemcpyAsync(M->seg_start, segs, sizeof(int32_t) * (ng + 1), cudaMemcpyHostToDevice, s));
-    AB_CUDA(cudaMemcpyAsync(M->seg_group, segg, sizeof(int32_t) * ng, cudaMemcpyHostToDevice, s));
-    AB_CUDA(cudaMemcpyAsync(M->ga_g, gg, sizeof(int32_t) * ng, cudaMemcpyHostToDevice, s));
-    AB_CUDA(cudaMemcpyAsync(M->ga_len, gl, sizeof(int32_t) * ng, cudaMemcpyHostToDevice, s));
-    AB_CUDA(cudaMemcpyAsync(M->ga_last, glast, sizeof(int32_t) * ng, cudaMemcpyHostToDevice, s));
-    AB_CUDA(cudaMemcpyAsync(M->pf_rows, &R, sizeof(int), cudaMemcpyHostToDevice, s));
-    launch_group_alloc(e.d, m, M->ga_g, M->ga_len, M->ga_last, ng, s);
-    int max_len = 0;
-    for (int j = 0; j < ng; ++j) max_len = std::max(max_len, gl[j]);
-    launch_embed(m, M->embed, M->x, nullptr, R, nullptr, s);
-    for (int l = 0; l < m.L; ++l) {
-      const LayerW& w = M->layers[l];
-      const Model::Plans& p = M->pf[l];
-      launch_rmsnorm(M->x, w.attn_norm, M->xn, m.d, m.eps, nullptr, R, nullptr, s);
-      gemm_launch(p.qkv, s);
-      launch_rope_kv(m, l, M->qkv, w.q_norm, w.k_norm, M->qrot, nullptr, R, nullptr, s);
-      launch_prefill_attention(m, l, M->qrot, M->attn, M->seg_start, M->seg_group, ng, R, max_len, s);
-      gemm_launch(p.o, s);
-      launch_rmsnorm(M->x, w.mlp_norm, M->xn, m.d, m.eps, nullptr, R, nullptr, s);
-      gemm_launch(p.gu, s);
-      gemm_launch(p.down, s);
+    if (na) {
+      AB_CUDA(cudaMemcpyAsync(M->ga_g, gg, sizeof(int32_t) * na, cudaMemcpyHostToDevice, s));
+      AB_CUDA(cudaMemcpyAsync(M->ga_len, gl, sizeof(int32_t) * na, cudaMemcpyHostToDevice, s));
+      AB_CUDA(cudaMemcpyAsync(M->ga_last, glast, sizeof(int32_t) * na, cudaMemcpyHostToDevice, s));
+      launch_group_alloc(e.d, m, M->ga_g, M->ga_len, M->ga_last, na, s);
+      e.launches += 1;
     }
-    AB_CUDA(cudaGetLastError());
-    AB_CUDA(cudaStreamSynchronize(s));  // host staging is reused by the next chunk
+    prefill_rows(e, R, nb);
     e.prefill_tokens += R;
-    e.launches += 2 + 8 * (int64_t)m.L;
     k = k1;
   }
   M->pending.clear();
   check_kv(e);
 }
 
+// KV re-prefill mode: drop the private KV pages of samples leaving the live batch with generated
+// tokens (the abort of an APRIL step); they are rebuilt by prefill when the sample is resubmitted.
+void model_evict(Engine& e, const int32_t* handles, const int32_t* gen, int n) {
+  Model* M = e.model;
+  int k = 0;
+  for (int i = 0; i < n; ++i)
+    if (gen[i] > 0 && !M->evicted[handles[i]]) {
+      e.stage_i32_host[k++] = handles[i];
+      M->evicted[handles[i]] = 1;
+    }
+  if (!k) return;
+  AB_CUDA(cudaMemcpyAsync(e.stage_i32_dev, e.stage_i32_host, sizeof(int32_t) * k, cudaMemcpyHostToDevice, e.stream));
+  launch_release_handles(e.d, M->md, e.stage_i32_dev, k, e.stream);
+  e.launches += 1;
+  AB_CUDA(cudaStreamSynchronize(e.stream));
+}
+
+// Rebuild the KV of resubmitted evicted samples: re-fork the group prompt pages, then prefill
+// the prompt's last token and every generated token but the newest (which the next decode
+// iteration feeds), in chunks of <= M_pf rows; a sample may span chunks (in position order).
+static void resume_reprefill(Engine& e, const ab_sample_desc* descs, int n) {
+  Model* M = e.model;
+  ModelDev& m = M->md;
+  cudaStream_t s = e.stream;
+  std::vector<int4> items;
+  for (int i = 0; i < n; ++i)
+    if (descs[i].gen_len > 0 && M->evicted[descs[i].handle]) {
+      items.push_back(make_int4(descs[i].handle, descs[i].group_slot, descs[i].gen_len, 0));
+      M->evicted[descs[i].handle] = 0;
+    }
+  if (items.empty()) return;
+  AB_CUDA(cudaMemcpyAsync(M->rs_items, items.data(), sizeof(int4) * items.size(), cudaMemcpyHostToDevice, s));
+  launch_resume_fork(e.d, m, M->rs_items, (int)items.size(), s);
+  e.launches += 2;
+  check_kv(e);
+  std::vector<int4> pieces;
+  int R = 0, nb = 0;
+  auto run_chunk = [&]() {
+    if (!R) return;
+    pieces.push_back(make_int4(0, 0, 0, R));  // sentinel: end row of the last piece
+    AB_CUDA(cudaMemcpyAsync(M->rs_pieces, pieces.data(), sizeof(int4) * pieces.size(), cudaMemcpyHostToDevice, s));
+    launch_extend_rows(e.d, m, M->rs_pieces, (int)pieces.size() - 1, s);
+    e.launches += 1;
+    prefill_rows(e, R, nb);  // synchronises: the piece list may be rebuilt
+    e.reprefill_tokens += R;
+    pieces.clear();
+    R = nb = 0;
+  };
+  for (const int4& it : items) {
+    const int h = it.x, g = it.y, gen = it.z;
+    for (int j0 = 0; j0 < gen;) {
+      if (R == M->M_pf) run_chunk();
+      const int cnt = std::min(gen - j0, M->M_pf - R);
+      pieces.push_back(make_int4(h, g, j0, R));
+      nb = add_blocks(M, nb, R, cnt, h, M->g_ctx_host[g] + j0);
+      R += cnt;
+      j0 += cnt;
+    }
+  }
+  run_chunk();
+}
+
+void model_begin_step(Engine& e, int64_t version) {
+  Model* M = e.model;
+  if (!e.cfg.kv_resume) return;
+  // new policy weights: every resident prompt group's KV is recomputed in place (the paused
+  // samples' KV was already dropped at the abort).  Queued here and run by the step's first
+  // submit, so that its cost lands inside the step's rollout wall time (scheduler clock0 is
+  // read after begin_step).
+  if (M->last_version >= 0 && version != M->last_version) {
+    for (auto& kv : M->prompts) {
+      bool queued = false;
+      for (auto& pg : M->pending) queued |= pg.g == kv.first;
+      if (!queued) M->pending.push_back({kv.first, kv.second, true});
+    }
+  }
+  M->last_version = version;
+}
+
 void model_submit(Engine& e, const ab_sample_desc* descs_dev, int n) {
+  const auto t0 = std::chrono::steady_clock::now();
+  bool recompute = false;
+  for (auto& pg : e.model->pending) recompute |= pg.in_place;
   flush_prefill(e);
+  if (recompute) e.reprefill_seconds += std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
   launch_fork_groups(e.d, e.model->md, descs_dev, n, e.stream);
   AB_CUDA(cudaGetLastError());
   check_kv(e);
+  if (e.cfg.kv_resume) {
+    const auto t1 = std::chrono::steady_clock::now();
+    resume_reprefill(e, e.stage_desc_host, n);  // synchronous
+    e.reprefill_seconds += std::chrono::duration<double>(std::chrono::steady_clock::now() - t1).count();
+  }
 }
 
 void model_release(Engine& e, const int32_t* handles_dev, int n) {
@@ -404,13 +622,27 @@ void model_release(Engine& e, const int32_t* handles_dev, int n) {
 void model_release_group(Engine& e, int group_slot) {
   Model* M = e.model;
   // a group still waiting for prefill is simply dropped
+  M->prompts.erase(group_slot);
+  bool resident = true;
   for (size_t i = 0; i < M->pending.size(); ++i)
     if (M->pending[i].g == group_slot) {
+      resident = M->pending[i].in_place;
       M->pending.erase(M->pending.begin() + i);
-      return;
+      break;
     }
+  if (!resident) return;
   launch_group_release(e.d, M->md, group_slot, e.stream);
   AB_CUDA(cudaGetLastError());
+}
+
+// kernels one decode iteration launches (plans with an all-zero table are skipped)
+int64_t model_iter_launches(Model* M) {
+  int64_t n = 5;  // prep, embed, final norm, lm_head, sampler
+  for (const auto& p : M->dec) {
+    n += 4;  // 2 norms, rope / KV write, attention
+    for (const GemmPlan* g : {&p.qkv, &p.qkv2, &p.o, &p.o2, &p.gu, &p.gu2, &p.down, &p.down2}) n += g->idle ? 0 : 1;
+  }
+  return n;
 }
 
 void model_iteration(Engine& e, int64_t run_iter, bool timed) {
@@ -442,7 +674,7 @@ void model_iteration(Engine& e, int64_t run_iter, bool timed) {
     }
     {
       ScopedTimer t(e, timed, "rope_kv", run_iter);
-      launch_rope_kv(m, l, M->qkv, w.q_norm, w.k_norm, M->qrot, b, S, stop, s);
+      launch_rope_kv_f32(m, l, M->qkv32, w.bqkv, w.q_norm, w.k_norm, M->qrot, b, S, stop, s);
     }
     {
       ScopedTimer t(e, timed, "attention", run_iter);
@@ -461,6 +693,7 @@ void model_iteration(Engine& e, int64_t run_iter, bool timed) {
     {
       ScopedTimer t(e, timed, "gemm_gate_up", run_iter);
       gemm_launch(p.gu, s);
+      gemm_launch(p.gu2, s);
     }
     {
       ScopedTimer t(e, timed, "gemm_down", run_iter);

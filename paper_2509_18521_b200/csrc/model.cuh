@@ -58,14 +58,20 @@ void launch_rmsnorm(const float* x, const bf16* w, bf16* out, int d, float eps, 
                     const int* stop, cudaStream_t s);
 void launch_rope_kv(const ModelDev& m, int layer, const bf16* qkv, const bf16* q_norm, const bf16* k_norm, bf16* q_out,
                     const int* rows_dev, int rows_cap, const int* stop, cudaStream_t s);
+void launch_rope_kv_f32(const ModelDev& m, int layer, float* qkv, const bf16* bias, const bf16* q_norm,
+                        const bf16* k_norm, bf16* q_out, const int* rows_dev, int rows_cap, const int* stop,
+                        cudaStream_t s);
 // attention.cu
 void make_kv_tmap(CUtensorMap* map, const ModelDev& m);
 int decode_attention_ctas(const ModelDev& m);  // persistent grid of the decode attention kernel
 void launch_decode_attention(const CUtensorMap& map, const EngineDev& e, const ModelDev& m, int layer, const bf16* q,
                              bf16* out, float* part_o, float* part_ml, int max_splits, int chunk, cudaStream_t s);
-void launch_prefill_attention(const ModelDev& m, int layer, const bf16* q, bf16* out, const int* seg_start,
-                              const int* seg_group, int n_seg, int rows, int max_len, cudaStream_t s);
+// causal flash prefill over the paged pool; blocks[i] = {first row, rows (<= 64), block-table row, first position}
+void launch_prefill_flash(const ModelDev& m, int layer, const bf16* q, bf16* out, const int4* blocks, int n_blocks,
+                          cudaStream_t s);
 void launch_fork_groups(const EngineDev& e, const ModelDev& m, const ab_sample_desc* descs, int n, cudaStream_t s);
+void launch_resume_fork(const EngineDev& e, const ModelDev& m, const int4* items, int n, cudaStream_t s);
+void launch_extend_rows(const EngineDev& e, const ModelDev& m, const int4* pieces, int n_pieces, cudaStream_t s);
 void launch_release_handles(const EngineDev& e, const ModelDev& m, const int32_t* handles, int n, cudaStream_t s);
 void launch_group_alloc(const EngineDev& e, const ModelDev& m, const int* groups, const int* lens,
                         const int* last_tok, int n, cudaStream_t s);

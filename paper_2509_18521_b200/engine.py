@@ -95,7 +95,8 @@ class Engine:
                  sampling: SamplingConfig | None = None, max_handles: int | None = None,
                  max_groups: int | None = None, device: int = 0, record_payload: bool | None = None,
                  prompt_len: int = 256, page_size: int = 16, kv_pages: int = 0, weight_seed: int = 0,
-                 weight_std: float = 0.02, prompt_source=None, nondeterministic_gemm: bool = False):
+                 weight_std: float = 0.02, prompt_source=None, nondeterministic_gemm: bool = False,
+                 kv_resume: str = "retain", gemm_autotune: bool = True):
         self.config = config
         self.global_seed = global_seed
         self.model = model
@@ -112,6 +113,14 @@ class Engine:
         # fp32 residual GEMMs may split K with TMA reduce-add (faster at mid-size batches; the split
         # summation order is then not fixed run to run)
         self.nondeterministic_gemm = bool(nondeterministic_gemm)
+        # "retain": a paused partial keeps its KV pages across steps (exact while weights are fixed);
+        # "reprefill": the abort drops them and the resume re-prefills prompt + carried tokens, the
+        # cost APRIL pays when the policy weights change between steps
+        if kv_resume not in ("retain", "reprefill"):
+            raise ConfigError(f"kv_resume must be 'retain' or 'reprefill', not {kv_resume!r}")
+        self.kv_resume = kv_resume
+        # time the decode GEMM schedules on this GPU at creation (cached per process and shape)
+        self.gemm_autotune = bool(gemm_autotune)
         self.prompt_source = prompt_source or (
             lambda iid: synthetic_prompt(global_seed, iid, prompt_len, model.vocab)) if model else None
         if record_payload is None:
@@ -153,6 +162,8 @@ class Engine:
         c.record_payload = int(self._record)
         c.weight_seed, c.weight_std = self.weight_seed, self.weight_std
         c.nondeterministic_gemm = int(self.nondeterministic_gemm)
+        c.kv_resume = int(self.kv_resume == "reprefill")
+        c.gemm_autotune = int(self.gemm_autotune)
         m = None
         if self.model is not None:
             sp = self.model

@@ -22,13 +22,14 @@ MARGIN_EPS = 0.05   # logit units
 LOGP_TOL = 0.05     # nats
 
 
-def _engine(spec, prompts, S=8, l_max=64, page=16, greedy=True, temperature=1.0, P=None, nondet=False):
-    P = P or len(next(iter(prompts.values())))
+def _engine(spec, prompts, S=8, l_max=64, page=16, greedy=True, temperature=1.0, P=None, nondet=False,
+            kv_resume="retain"):
+    P = P or max(len(p) for p in prompts.values())
     return pb.LengthDrivenEngine(
         pb.EngineConfig(max_slots=S, l_max=l_max), global_seed=3, model=spec,
         sampling=pb.SamplingConfig(temperature=temperature, greedy=greedy), prompt_len=P, page_size=page,
         kv_pages=1024, max_handles=64, max_groups=16, prompt_source=lambda iid: prompts[iid],
-        nondeterministic_gemm=nondet)
+        nondeterministic_gemm=nondet, kv_resume=kv_resume)
 
 
 def _prompts(spec, n, P):
@@ -74,9 +75,16 @@ def test_greedy_tokens_match_oracle(preset, layers, nondet):
         assert s.total_tokens == s.target_length and len(s.token_ids()) == s.target_length
     # greedy + shared prompt: all samples of a group generate the same sequence, so
     # the longest one is scored against the oracle and the others must be its prefixes
+    # (deterministic schedules only: with reduce-added split-K the rows of one batch may sum
+    # their K splits in different orders, so each sample is scored against the oracle instead)
     for iid in (0, 1):
         grp = [s for s in samples if s.instance_id == iid]
         top = max(grp, key=lambda s: s.total_tokens)
+        if nondet:
+            for s in grp:
+                flips += _check_greedy(dec, prompts[iid], s.token_ids(), s.behavior_logprob_trace())
+                total += s.total_tokens
+            continue
         for s in grp:
             assert s.token_ids() == top.token_ids()[: s.total_tokens]
             np.testing.assert_allclose(s.behavior_logprob_trace(), top.behavior_logprob_trace()[: s.total_tokens],
@@ -190,3 +198,70 @@ def test_sequence_logprobs_reduce_the_resident_payload():
         assert len(full) == s.target_length
         assert abs(sm - float(np.sum(full[:n]))) < 1e-9 * max(1.0, abs(sm))
     eng.close()
+
+
+@pytest.mark.parametrize("preset,layers,page", [("tiny", None, 16), ("qwen2.5-1.5b", 2, 64), ("qwen3-4b", 1, 16)])
+def test_long_prompt_prefill_matches_oracle(preset, layers, page):
+    """Prompt prefill through the flash prefill kernel: several 64-row blocks per prompt, prompts
+    of different lengths packed in one chunk, pages of 16 and 64 tokens."""
+    spec = pb.PRESETS[preset]
+    if layers:
+        spec = spec.truncated(layers)
+    prompts = {0: pb.synthetic_prompt(11, 0, 203, spec.vocab), 1: pb.synthetic_prompt(11, 1, 77, spec.vocab)}
+    eng = _engine(spec, prompts, page=page, l_max=256)
+    eng.begin_step(0)
+    samples = []
+    for iid in (0, 1):
+        s = RolloutSample(iid, 0)
+        s.target_length = 12
+        eng.submit(s)
+        samples.append(s)
+    _drain(eng)
+    dec = CpuDecoder(spec, eng.export_weights())
+    flips = sum(_check_greedy(dec, prompts[s.instance_id], s.token_ids(), s.behavior_logprob_trace())
+                for s in samples)
+    assert flips <= 2
+    eng.close()
+
+
+@pytest.mark.parametrize("preset,layers,page", [("tiny", None, 16), ("qwen2.5-1.5b", 2, 64), ("qwen3-4b", 1, 16)])
+def test_reprefill_resume_matches_oracle(preset, layers, page):
+    """KV re-prefill mode: the abort drops the paused samples' KV, the resubmit
+    rebuilds it by prefill (prompt tail + carried tokens), and decoding continues on it.  Tokens
+    after the resume are checked against the oracle teacher-forced on the full history."""
+    spec = pb.PRESETS[preset]
+    if layers:
+        spec = spec.truncated(layers)
+    prompts = _prompts(spec, 2, 37)
+    eng = _engine(spec, prompts, page=page, l_max=200, kv_resume="reprefill")
+    free0 = eng.stats().kv_pages_free
+    eng.begin_step(0)
+    samples = []
+    for iid in (0, 1):
+        for j in range(2):
+            s = RolloutSample(iid, j)
+            s.target_length = 90 + 17 * j + 5 * iid
+            eng.submit(s)
+            samples.append(s)
+    for _ in range(70):
+        eng.decode_iteration()
+    paused = eng.abort_active()
+    assert len(paused) == 4 and all(p.total_tokens == 70 for p in paused)
+    pf0 = eng.stats().prefill_tokens
+    eng.begin_step(1)  # new version: the resident groups' prompt KV is recomputed in place
+    for p in paused:
+        eng.submit(p)
+    _drain(eng)
+    assert eng.stats().prefill_tokens == pf0 + 2 * 36
+    st = eng.stats()
+    assert st.reprefill_tokens == 4 * 70
+    dec = CpuDecoder(spec, eng.export_weights())
+    flips = 0
+    for s in samples:
+        assert [g.token_count for g in s.segments] == [70, s.target_length - 70]
+        flips += _check_greedy(dec, prompts[s.instance_id], s.token_ids(), s.behavior_logprob_trace())
+    assert flips <= max(3, sum(s.target_length for s in samples) // 25)
+    eng.discard(samples)
+    assert eng.stats().kv_pages_free == free0
+    eng.close()
+

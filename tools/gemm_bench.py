@@ -15,13 +15,23 @@ import torch  # noqa: E402
 
 from paper_2509_18521_b200 import _capi  # noqa: E402
 
-SHAPES = {  # name: (N, K, epi)   Qwen2.5-1.5B decode projections
-    "qkv": (2048, 1536, 0),
-    "o": (1536, 1536, 2),
-    "gate_up": (17920, 1536, 3),
-    "down": (1536, 8960, 2),
-    "lm_head": (151936, 1536, 1),
+MODEL_SHAPES = {  # name: (N, K, epi)   decode projections per model shape
+    "qwen2.5-1.5b": {
+        "qkv": (2048, 1536, 0),
+        "o": (1536, 1536, 2),
+        "gate_up": (17920, 1536, 3),
+        "down": (1536, 8960, 2),
+        "lm_head": (151936, 1536, 1),
+    },
+    "qwen3-4b": {
+        "qkv": (6144, 2560, 2),
+        "o": (2560, 4096, 2),
+        "gate_up": (19456, 2560, 3),
+        "down": (2560, 9728, 2),
+        "lm_head": (151936, 2560, 1),
+    },
 }
+SHAPES = MODEL_SHAPES["qwen2.5-1.5b"]
 
 
 def run(N, K, M, epi, bn, reps, split, cublas=True):
@@ -98,8 +108,11 @@ def main():
     ap.add_argument("--split", type=int, default=1)
     ap.add_argument("--sweep", action="store_true")
     ap.add_argument("--pair", action="store_true", help="time the CTA-pair plans (cluster of 2)")
+    ap.add_argument("--model", default="qwen2.5-1.5b", choices=sorted(MODEL_SHAPES))
     ap.add_argument("--mode", type=int, default=0, help="2: operand fill only, 4: MMA only (debug timing)")
     args = ap.parse_args()
+    global SHAPES
+    SHAPES = MODEL_SHAPES[args.model]
     if args.mode:
         _capi.call("ab_debug_gemm_trace", args.mode, None)
     if args.sweep:

@@ -1,0 +1,14 @@
+mkdir -p gpurun_out
+export AB_AUTOTUNE_LOG=1
+timeout 200 python tools/autotune_probe.py --model tiny --slots 8 --det > gpurun_out/at_tiny.log 2>&1
+timeout 300 python tools/autotune_probe.py --model qwen3-4b --slots 64 > gpurun_out/at_c3.log 2>&1
+timeout 400 python tools/autotune_probe.py --model qwen2.5-1.5b --slots 1024 > gpurun_out/at_c2.log 2>&1
+
+mkdir -p gpurun_out
+export AB_AUTOTUNE_LOG=1
+timeout 900 python -m pytest tests/test_model_gpu.py tests/test_engine_gpu.py -m gpu -q -x 2>&1 | tail -25 > gpurun_out/pytest_model.log
+for cfg in "1024 1400" "256 2000" "64 3000"; do
+  set -- $cfg
+  ( time timeout 400 python tools/decode_microbench.py --batch $1 --ctx $2 --iters 16 > gpurun_out/micro_b$1.json 2> gpurun_out/tune_c2_b$1.log ) 2>> gpurun_out/times.log
+done
+( time timeout 400 python tools/decode_microbench.py --model qwen3-4b --batch 64 --ctx 3000 --iters 16 > gpurun_out/micro_c3_b64.json 2> gpurun_out/tune_c3.log ) 2>> gpurun_out/times.log
