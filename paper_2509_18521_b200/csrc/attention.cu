@@ -27,6 +27,7 @@ namespace ab {
 namespace {
 
 constexpr float kLog2e = 1.4426950408889634f;
+__constant__ int c_pdl_mask = 7;  // see gemm.cu
 constexpr int kTok = 64;        // tokens per tile
 constexpr int kCons = 4;        // consumer warps (16 tokens each)
 constexpr int kThreads = (kCons + 1) * 32;
@@ -126,7 +127,8 @@ __global__ void __launch_bounds__(kThreads, 2)
                   float* __restrict__ part_ml, int max_splits) {
   using Cfg = AttCfg<HD>;
   pdl_wait();
-  // (no early launch_dependents: the successor pre-launches when this grid drains)
+  // the successor (the O GEMM) may start its pre-wait prologue on SMs this persistent grid leaves
+  if (c_pdl_mask & 2) pdl_launch();
   const Ctl* c = e.ctl;
   if (c->stop) return;
   const int b = c->b;
@@ -626,6 +628,8 @@ void launch_prefill_flash(const ModelDev& m, int layer, const bf16* q, bf16* out
   else
     launch_pf<64>(m, layer, q, out, blocks, n_blocks, s);
 }
+
+void set_pdl_mask_attention(int mask) { AB_CUDA(cudaMemcpyToSymbol(c_pdl_mask, &mask, sizeof(int))); }
 
 void make_kv_tmap(CUtensorMap* map, const ModelDev& m) {
   AB_REQUIRE(m.gq <= kMergeRows, AB_ERR_CONFIG, "decode attention supports GQA groups of at most 8");

@@ -337,6 +337,7 @@ int choose_sched(int rows, int N, int K, int max_bn, int cs, int ncl, int force,
 // [4] last MMA committed, [5] epilogue sees the accumulator, [6] epilogue done, [7] exit,
 // [8] split: partial parked, [11] split: cluster barrier passed, [12] first chunk fetched.
 __device__ unsigned long long g_gemm_trace[160 * 16];
+__constant__ int c_pdl_mask = 7;  // early launch_dependents: 1 GEMM, 2 attention, 4 RMSNorm (AB_PDL_MASK)
 __device__ __forceinline__ void trace_mark(int on, int k) {
   if (on & 1) {
     unsigned long long t;
@@ -387,18 +388,28 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
-  pdl_wait();  // everything below reads what the previous kernel of the stream wrote
-  // (no early launch_dependents: the successor pre-launches when this grid drains)
+  // Programmatic dependent launch: the live row count, the stop flag and the schedule table are
+  // read BEFORE griddepcontrol.wait.  They are written only at iteration boundaries (admit /
+  // prep / finish), several kernels upstream, and every kernel of the chain waits before it
+  // triggers its own dependents, so they are final when this grid can start.  The weights are
+  // constant, so the weight producer also runs ahead of the wait (prefetching the first stages
+  // while the previous kernel drains); only the activation producer and the epilogue, which read
+  // or write what earlier kernels produced, wait.
   const int stop = stop_dev ? *stop_dev : 0;
   const int rows_raw = rows_dev ? *rows_dev : M_cap;
   const int rows = min(rows_raw, M_cap);
-  if (stop || rows <= 0) return;
+  // A CTA with no work still waits before it exits: a grid that completed early would let its
+  // own dependents (which wait only on it) overtake the grids before it.
+  if (stop || rows <= 0) return pdl_wait();
   const int code = sched_tab[rows];
-  if (code == 0) return;
+  if (code == 0) {  // an idle partner plan: let the successor go, then wait
+    if (c_pdl_mask & 1) pdl_launch();
+    return pdl_wait();
+  }
   const Sched sc = sched_from(code, rows, N, K);
   const int cs = (int)cluster_nctarank();
   const bool split = sc.splits > 1 && !sc.red;  // cluster split-K
-  if (kPair != (sc.pair != 0)) return;  // the host never builds such a table
+  if (kPair != (sc.pair != 0)) return pdl_wait();  // the host never builds such a table
   const int crank = (split || pair) ? (int)cluster_ctarank() : 0;
   const int prank = pair ? (crank & 1) : 0;
   const int rank = split ? crank % sc.splits : 0;  // K slice within the tile's rank group
@@ -411,7 +422,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int u_step = split ? ((int)gridDim.x / cs) * per_cl : pair ? (int)gridDim.x / 2 : (int)gridDim.x;
   const int n_units = sc.units;  // tiles, or (tile, split) pairs for reduce-added split-K
   if ((split || pair) ? ((int)blockIdx.x / cs) * per_cl >= sc.tiles : u_first >= n_units)
-    return;  // uniform per cluster
+    return pdl_wait();  // uniform per cluster
 
   // the 3-D TMA views this schedule loads from
   const CUtensorMap* mw = sc.wn == 256 && !sc.pair ? &tw3_256 : &tw3;
@@ -435,6 +446,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   const uint32_t tmem = *tmem_slot;
   const uint32_t leader = (uint32_t)(crank & ~1);
   if (threadIdx.x == 0) trace_mark(trace, 1);
+  if (c_pdl_mask & 1) pdl_launch();  // the successor may start its own pre-wait prologue
+  if (warp >= 2) pdl_wait();         // activation producer (warp 6) and epilogue (warps 2-5)
 
   // A unit's k-block pairs are visited in a rotated order (start offset spread by row tile):
   // the CTAs that share a weight tile then read different k slices of it at any moment instead
@@ -1246,6 +1259,8 @@ void make_tmap_bf16(CUtensorMap* m, const void* ptr, int64_t rows, int64_t cols,
                            CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   AB_REQUIRE(r == CUDA_SUCCESS, AB_ERR_CUDA, "cuTensorMapEncodeTiled (KV) failed (" + std::to_string((int)r) + ")");
 }
+
+void set_pdl_mask_gemm(int mask) { AB_CUDA(cudaMemcpyToSymbol(c_pdl_mask, &mask, sizeof(int))); }
 
 void gemm_launch(const GemmPlan& p, cudaStream_t s) {
   if (p.idle) return;

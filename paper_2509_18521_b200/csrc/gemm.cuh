@@ -54,6 +54,7 @@ void gemm_plan(GemmPlan& p, const __nv_bfloat16* W, int N, int K, const __nv_bfl
 // launch exits at once.  Both plans are launched every time.
 void gemm_partition(GemmPlan& a, GemmPlan& b);
 void gemm_launch(const GemmPlan& p, cudaStream_t s);
+void set_pdl_mask_gemm(int mask);  // early launch_dependents (programmatic dependent launch) per kernel class
 // Autotuning (engine creation): the fixed schedule codes valid for the plan at `rows`; the
 // median device time (us) of `reps` launches of one code at `rows` (L2 flushed before each by
 // a memset of `flush`); install a per-row-count table built from measurements.

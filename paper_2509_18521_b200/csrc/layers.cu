@@ -18,6 +18,7 @@ namespace ab {
 namespace {
 
 constexpr float kLog2e = 1.4426950408889634f;
+__constant__ int c_pdl_mask = 7;  // see gemm.cu
 
 __device__ __forceinline__ bool stopped(const int* stop) { return stop != nullptr && *stop != 0; }
 
@@ -87,14 +88,19 @@ __global__ void __launch_bounds__(kPrepThreads) k_prep_decode(EngineDev e, Model
     m.row_pos[i] = pos;
     m.row_btrow[i] = h;
     ctx_sum += (unsigned long long)(pos + 1);
+    int page = 0;
     if (pos % m.P == 0) {
       const int idx = pop_page(c);
       if (idx < 0 || pos / m.P >= m.MP) {
         fail = true;
       } else {
-        m.bt[(size_t)h * m.MP + pos / m.P] = m.free_pages[idx];
+        page = m.free_pages[idx];
+        m.bt[(size_t)h * m.MP + pos / m.P] = page;
       }
+    } else {
+      page = m.bt[(size_t)h * m.MP + pos / m.P];
     }
+    m.row_pslot[i] = page * m.P + pos % m.P;  // KV page and slot of the token written this iteration
   }
   __shared__ int s_w[32];
   __shared__ unsigned long long s_u[32];
@@ -215,22 +221,25 @@ __global__ void __launch_bounds__(256) k_rmsnorm_v(const float* __restrict__ x, 
                                                    bf16* __restrict__ out, float eps, const int* rows_dev,
                                                    int rows_cap, const int* stop) {
   pdl_wait();
-  // (no early launch_dependents: the successor pre-launches when this grid drains)
-  if (stopped(stop)) return;
-  const int rows = rows_dev ? min(*rows_dev, rows_cap) : rows_cap;
+  if (c_pdl_mask & 4) pdl_launch();  // the next GEMM's CTAs start their prologue alongside
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int r = blockIdx.x * (blockDim.x >> 5) + warp;
-  if (r >= rows) return;
+  if (r >= rows_cap) return;
   constexpr int D = NV * 128;
   const float4* xr = reinterpret_cast<const float4*>(x + (size_t)r * D);
   const uint2* wv = reinterpret_cast<const uint2*>(w);
   float4 v[NV];
-  uint2 wr[NV];  // the norm weights are loaded together with x: one memory round trip
+  uint2 wr[NV];
+  // the row, the norm weights, the stop flag and the live row count are all loaded in one memory
+  // round trip (the row is in bounds for any count <= rows_cap; it is discarded if not live)
+  const int st = stop ? *stop : 0;
+  const int rows = rows_dev ? *rows_dev : rows_cap;
 #pragma unroll
   for (int i = 0; i < NV; ++i) {
     v[i] = xr[i * 32 + lane];
     wr[i] = __ldg(wv + i * 32 + lane);
   }
+  if (st || r >= min(rows, rows_cap)) return;
   float ss = 0.f;
 #pragma unroll
   for (int i = 0; i < NV; ++i) ss += v[i].x * v[i].x + v[i].y * v[i].y + v[i].z * v[i].z + v[i].w * v[i].w;
@@ -344,64 +353,76 @@ __global__ void k_rope_kv_f32(ModelDev m, int layer, float* __restrict__ qkv, co
                               const bf16* __restrict__ qn, const bf16* __restrict__ kn, bf16* __restrict__ qout,
                               const int* rows_dev, int rows_cap, const int* stop) {
   pdl_wait();
-  if (stopped(stop)) return;
-  const int rows = rows_dev ? min(*rows_dev, rows_cap) : rows_cap;
+  // every per-row index is loaded up front in parallel (the prep kernel resolved the KV page)
   const int r = blockIdx.x;
-  if (r >= rows) return;
+  const int st = stop ? *stop : 0;
+  const int rows = rows_dev ? min(*rows_dev, rows_cap) : rows_cap;
+  const int pos = m.row_pos[r];
+  const int ps = m.row_pslot[r];
+  if (st || r >= rows) return;
   constexpr int NP = HD / 64;  // rotation pairs per lane
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
-  const int pos = m.row_pos[r];
-  const int page = m.bt[(size_t)m.row_btrow[r] * m.MP + pos / m.P], slot = pos % m.P;
+  const int page = ps / m.P, slot = ps - page * m.P;
   const float2* rp = m.rope + (size_t)pos * (HD / 2);
   float* src = qkv + (size_t)r * m.qkv_dim;
+  static_assert(NP == 1 || NP == 2, "rotation pairs per lane");
   for (int head = warp + blockIdx.y * nw; head < m.hq + 2 * m.hk; head += nw * gridDim.y) {
+    // every load of the head is issued before any store (the zeroing stores would otherwise
+    // order the rotation-table and norm-weight loads behind them: one memory round trip)
+    const bool is_v = head >= m.hq + m.hk, is_q = head < m.hq;
     float* hv = src + head * HD;
-    float a[NP], b[NP];
-    static_assert(NP == 1 || NP == 2, "rotation pairs per lane");
-    float ba[NP] = {}, bb[NP] = {};
-    if (bias) {
-      load_pairs<NP>(bias + head * HD + lane * NP, ba);
-      load_pairs<NP>(bias + head * HD + lane * NP + HD / 2, bb);
-    }
+    float* pa = hv + lane * NP;
+    float* pb = hv + lane * NP + HD / 2;
+    float a[NP], b[NP], ba[NP] = {}, bb[NP] = {}, wa[NP] = {}, wb[NP] = {};
+    float2 cs[NP];
     if constexpr (NP == 2) {
-      float2* pa = reinterpret_cast<float2*>(hv + lane * 2);
-      float2* pb = reinterpret_cast<float2*>(hv + lane * 2 + HD / 2);
-      const float2 va = __ldcg(pa), vb = __ldcg(pb);
+      const float2 va = *reinterpret_cast<const float2*>(pa), vb = *reinterpret_cast<const float2*>(pb);
       a[0] = va.x;
       a[1] = va.y;
       b[0] = vb.x;
       b[1] = vb.y;
-      __stcg(pa, make_float2(0.f, 0.f));
-      __stcg(pb, make_float2(0.f, 0.f));
     } else {
-      a[0] = __ldcg(hv + lane);
-      b[0] = __ldcg(hv + lane + HD / 2);
-      __stcg(hv + lane, 0.f);
-      __stcg(hv + lane + HD / 2, 0.f);
+      a[0] = *pa;
+      b[0] = *pb;
+    }
+    if (bias) {
+      load_pairs<NP>(bias + head * HD + lane * NP, ba);
+      load_pairs<NP>(bias + head * HD + lane * NP + HD / 2, bb);
+    }
+#pragma unroll
+    for (int j = 0; j < NP; ++j) cs[j] = __ldg(rp + lane * NP + j);  // (unconditional: issued with the rest)
+    if (!is_v) {
+      if (m.qk_norm) {
+        const bf16* nw_ = is_q ? qn : kn;
+        load_pairs<NP>(nw_ + lane * NP, wa);
+        load_pairs<NP>(nw_ + lane * NP + HD / 2, wb);
+      }
+    }
+    if constexpr (NP == 2) {
+      *reinterpret_cast<float2*>(pa) = make_float2(0.f, 0.f);
+      *reinterpret_cast<float2*>(pb) = make_float2(0.f, 0.f);
+    } else {
+      *pa = 0.f;
+      *pb = 0.f;
     }
 #pragma unroll
     for (int j = 0; j < NP; ++j) {
       a[j] = __bfloat162float(__float2bfloat16(a[j] + ba[j]));
       b[j] = __bfloat162float(__float2bfloat16(b[j] + bb[j]));
     }
-    if (head >= m.hq + m.hk) {  // V: straight into the page
+    if (is_v) {  // V: straight into the page
       const int kvh = head - m.hq - m.hk;
       bf16* dst = m.kv + m.kv_off(layer, page, 1, kvh, slot);
       store_pairs<NP>(dst + lane * NP, a);
       store_pairs<NP>(dst + lane * NP + HD / 2, b);
       continue;
     }
-    const bool is_q = head < m.hq;
     if (m.qk_norm) {
       float ss = 0.f;
 #pragma unroll
       for (int j = 0; j < NP; ++j) ss += a[j] * a[j] + b[j] * b[j];
       ss = warp_sum(ss);
       const float rs = rsqrtf(ss / (float)HD + m.eps);
-      const bf16* nw_ = is_q ? qn : kn;
-      float wa[NP], wb[NP];
-      load_pairs<NP>(nw_ + lane * NP, wa);
-      load_pairs<NP>(nw_ + lane * NP + HD / 2, wb);
 #pragma unroll
       for (int j = 0; j < NP; ++j) {
         a[j] = __bfloat162float(__float2bfloat16(a[j] * rs * wa[j]));
@@ -411,9 +432,8 @@ __global__ void k_rope_kv_f32(ModelDev m, int layer, float* __restrict__ qkv, co
     float oa[NP], ob[NP];
 #pragma unroll
     for (int j = 0; j < NP; ++j) {
-      const float2 cs = rp[lane * NP + j];
-      oa[j] = a[j] * cs.x - b[j] * cs.y;
-      ob[j] = b[j] * cs.x + a[j] * cs.y;
+      oa[j] = a[j] * cs[j].x - b[j] * cs[j].y;
+      ob[j] = b[j] * cs[j].x + a[j] * cs[j].y;
     }
     bf16* dst = is_q ? qout + (size_t)r * m.qd + head * HD : m.kv + m.kv_off(layer, page, 0, head - m.hq, slot);
     store_pairs<NP>(dst + lane * NP, oa);
@@ -576,6 +596,8 @@ __global__ void k_group_release(EngineDev e, ModelDev m, int g) {
 // ---------------------------------------------------------------------------
 // launchers
 // ---------------------------------------------------------------------------
+
+void set_pdl_mask_layers(int mask) { AB_CUDA(cudaMemcpyToSymbol(c_pdl_mask, &mask, sizeof(int))); }
 
 void launch_init_weights(bf16* w, size_t n, uint64_t seed, uint64_t tensor_id, float std, float constant,
                          cudaStream_t s) {

@@ -45,6 +45,8 @@ struct Model {
     // gemm_partition gives each row count to the faster of the pair of plans
     GemmPlan qkv2, o2, down2;
     GemmPlan gu2;  // decode gate-up on a cluster-of-8 (non-pair) plan: small row counts (autotuned)
+    // prefill only: CTA-pair alternatives of the four projections (autotuned against the 1-SM plans)
+    GemmPlan qkv_p, o_p, gu_p, down_p;
   };
   std::vector<Plans> dec, pf;
   GemmPlan lm_dec;
@@ -110,6 +112,7 @@ static void autotune_decode(Engine& e, Model* M) {
   ladder.push_back(S);
   void* flush = nullptr;
   const size_t flush_bytes = (size_t)192 << 20;  // > L2 (126 MB)
+  int cur_cap = S;  // table size - 1 of the plans being tuned
   auto key_of = [&](const std::vector<GemmPlan*>& g) {
     std::string k;
     for (auto* p : g)
@@ -123,7 +126,7 @@ static void autotune_decode(Engine& e, Model* M) {
     auto it = cache.find(key);
     if (it != cache.end()) return it->second;
     if (!flush) AB_CUDA(cudaMalloc(&flush, flush_bytes));
-    std::vector<std::vector<int>> tabs(g.size(), std::vector<int>(S + 1, 0));
+    std::vector<std::vector<int>> tabs(g.size(), std::vector<int>(cur_cap + 1, 0));
     int lo = 1;
     for (int r : ladder) {
       double best = 1e30;
@@ -153,18 +156,27 @@ static void autotune_decode(Engine& e, Model* M) {
     return tabs;
   };
   const int L = (int)M->dec.size();
-  auto apply = [&](GemmPlan Model::Plans::*a, GemmPlan Model::Plans::*b) {
-    std::vector<GemmPlan*> g = {&(M->dec[0].*a), &(M->dec[0].*b)};
+  auto apply = [&](std::vector<Model::Plans>& v, GemmPlan Model::Plans::*a, GemmPlan Model::Plans::*b) {
+    std::vector<GemmPlan*> g = {&(v[0].*a), &(v[0].*b)};
     const auto tabs = tune(g);
     for (int l = 0; l < L; ++l) {
-      gemm_set_table(M->dec[l].*a, tabs[0]);
-      gemm_set_table(M->dec[l].*b, tabs[1]);
+      gemm_set_table(v[l].*a, tabs[0]);
+      gemm_set_table(v[l].*b, tabs[1]);
     }
   };
-  apply(&Model::Plans::qkv, &Model::Plans::qkv2);
-  apply(&Model::Plans::o, &Model::Plans::o2);
-  apply(&Model::Plans::down, &Model::Plans::down2);
-  apply(&Model::Plans::gu, &Model::Plans::gu2);
+  apply(M->dec, &Model::Plans::qkv, &Model::Plans::qkv2);
+  apply(M->dec, &Model::Plans::o, &Model::Plans::o2);
+  apply(M->dec, &Model::Plans::down, &Model::Plans::down2);
+  apply(M->dec, &Model::Plans::gu, &Model::Plans::gu2);
+  // prefill chunks (up to M_pf rows): 1-SM plans against CTA-pair plans on a coarse ladder
+  ladder.clear();
+  for (int r = 64; r < M->M_pf; r *= 4) ladder.push_back(r);
+  ladder.push_back(M->M_pf);
+  cur_cap = M->M_pf;
+  apply(M->pf, &Model::Plans::qkv, &Model::Plans::qkv_p);
+  apply(M->pf, &Model::Plans::o, &Model::Plans::o_p);
+  apply(M->pf, &Model::Plans::gu, &Model::Plans::gu_p);
+  apply(M->pf, &Model::Plans::down, &Model::Plans::down_p);
   if (flush) AB_CUDA(cudaFree(flush));
   // the timing runs accumulated into the decode workspaces: the QKV accumulator must start at zero
   AB_CUDA(cudaMemsetAsync(M->qkv32, 0, sizeof(float) * (size_t)S * M->md.qkv_dim, s));
@@ -182,6 +194,14 @@ Model* model_create(Engine& e) {
   AB_REQUIRE(ec.page_size >= 16 && ec.page_size % 16 == 0, AB_ERR_CONFIG, "page_size must be a multiple of 16");
   AB_REQUIRE(ec.max_prompt >= 2, AB_ERR_CONFIG, "max_prompt must be >= 2");
   AB_REQUIRE(ec.top_p >= 1.f, AB_ERR_CONFIG, "top_p < 1 is not supported by this build");
+  {
+    // which kernels trigger their dependents early (bit 1 GEMM, 2 attention, 4 RMSNorm; default all)
+    const char* pm = getenv("AB_PDL_MASK");
+    const int mask = pm ? atoi(pm) : 7;
+    set_pdl_mask_gemm(mask);
+    set_pdl_mask_attention(mask);
+    set_pdl_mask_layers(mask);
+  }
   Model* M = new Model();
   M->cfg = c;
   ModelDev& m = M->md;
@@ -276,6 +296,7 @@ Model* model_create(Engine& e) {
   m.row_tok = dalloc<int32_t>(R);
   m.row_pos = dalloc<int32_t>(R);
   m.row_btrow = dalloc<int32_t>(R);
+  m.row_pslot = dalloc<int32_t>(R);
   m.split_prefix = dalloc<int32_t>(M->S + 1);
   m.att_counter = dalloc<int32_t>((size_t)M->S * m.hk);
   m.att_items = dalloc<int32_t>((size_t)M->S * M->max_splits + 1);
@@ -315,6 +336,7 @@ Model* model_create(Engine& e) {
   }
   AB_REQUIRE(np >= 1, AB_ERR_CONFIG, "no HBM left for the KV pool");
   AB_REQUIRE((size_t)np * page_bytes + ((size_t)1 << 30) <= free_b, AB_ERR_CONFIG, "KV pool does not fit in HBM");
+  AB_REQUIRE(np * m.P < (int64_t(1) << 31), AB_ERR_CONFIG, "KV pool too large for 32-bit token slots");
   m.NP = np;
   m.kv = dalloc<bf16>((size_t)np * page_bytes / 2);
   m.free_pages = dalloc<int32_t>(np);
@@ -369,6 +391,16 @@ Model* model_create(Engine& e) {
               nullptr);
     gemm_plan(p.down, w.wd, m.d, m.f, M->hbuf, M->M_pf, m.f, 256, kEpiAddF32, M->x, m.d, nullptr, M->pf_rows,
               nullptr);
+    gemm_plan(p.qkv_p, w.wqkv, m.qkv_dim, m.d, M->xn, M->M_pf, m.d, 256, kEpiBF16, M->qkv, m.qkv_dim, w.bqkv,
+              M->pf_rows, nullptr, 2, true);
+    gemm_plan(p.o_p, w.wo, m.d, m.qd, M->attn, M->M_pf, m.qd, 256, kEpiAddF32, M->x, m.d, nullptr, M->pf_rows,
+              nullptr, 2, true);
+    gemm_plan(p.gu_p, w.wgu, 2 * m.f, m.d, M->xn, M->M_pf, m.d, 256, kEpiSwiGLU, M->hbuf, m.f, nullptr,
+              M->pf_rows, nullptr, 2, true);
+    gemm_plan(p.down_p, w.wd, m.d, m.f, M->hbuf, M->M_pf, m.f, 256, kEpiAddF32, M->x, m.d, nullptr, M->pf_rows,
+              nullptr, 2, true);
+    for (GemmPlan* pp : {&p.qkv_p, &p.o_p, &p.gu_p, &p.down_p})  // idle unless the autotuner picks them
+      gemm_set_table(*pp, std::vector<int>(M->M_pf + 1, 0));
     M->dec.push_back(d);
     M->pf.push_back(p);
   }
@@ -384,7 +416,7 @@ void model_destroy(Model* M) {
   if (!M) return;
   ModelDev& m = M->md;
   void* ptrs[] = {M->wbuf,     M->x,        M->xn,        M->qkv,       M->qkv32,     M->qrot,     M->attn,     M->hbuf,
-                  M->logits,   M->part_o,   M->part_ml,   m.row_tok,    m.row_pos,    m.row_btrow, m.h_ctx,
+                  M->logits,   M->part_o,   M->part_ml,   m.row_tok,    m.row_pos,    m.row_btrow, m.row_pslot, m.h_ctx,
                   m.h_last_tok, m.h_shared, m.g_ctx,      m.g_last_tok, m.g_npages,   m.bt,        m.rope,
                   M->pf_rows,  M->ga_g,     M->ga_len,    M->ga_last,  m.kv,
                   m.free_pages, m.split_prefix, m.att_counter, m.att_ctl, M->pf_blocks, M->rs_items,
@@ -449,16 +481,24 @@ static void prefill_rows(Engine& e, int R, int nb) {
     const Model::Plans& p = M->pf[l];
     launch_rmsnorm(M->x, w.attn_norm, M->xn, m.d, m.eps, nullptr, R, nullptr, s);
     gemm_launch(p.qkv, s);
+    gemm_launch(p.qkv_p, s);
     launch_rope_kv(m, l, M->qkv, w.q_norm, w.k_norm, M->qrot, nullptr, R, nullptr, s);
     launch_prefill_flash(m, l, M->qrot, M->attn, M->pf_blocks, nb, s);
     gemm_launch(p.o, s);
+    gemm_launch(p.o_p, s);
     launch_rmsnorm(M->x, w.mlp_norm, M->xn, m.d, m.eps, nullptr, R, nullptr, s);
     gemm_launch(p.gu, s);
+    gemm_launch(p.gu_p, s);
     gemm_launch(p.down, s);
+    gemm_launch(p.down_p, s);
   }
   AB_CUDA(cudaGetLastError());
   AB_CUDA(cudaStreamSynchronize(s));  // host staging is reused by the next chunk
-  e.launches += 1 + 8 * (int64_t)m.L;
+  int64_t g = 0;
+  for (const GemmPlan* pp : {&M->pf[0].qkv, &M->pf[0].qkv_p, &M->pf[0].o, &M->pf[0].o_p, &M->pf[0].gu,
+                             &M->pf[0].gu_p, &M->pf[0].down, &M->pf[0].down_p})
+    g += pp->idle ? 0 : 1;
+  e.launches += 1 + (4 + g) * (int64_t)m.L;
 }
 
 // Prefill every pending prompt group (positions 0..len-2) in packed chunks.

@@ -33,6 +33,7 @@ struct ModelDev {
   int32_t* row_tok;
   int32_t* row_pos;
   int32_t* row_btrow;
+  int32_t* row_pslot;     // [S] decode: page * P + slot of the row's new token (k_prep_decode)
   int32_t* split_prefix;  // [S+1] attention work list: exclusive prefix of KV splits per live row
   int32_t* att_counter;   // [S * hk] split-combine arrival counters (self-resetting)
   int32_t* att_items;     // [S * max_splits] work list: row | split << 16
@@ -67,6 +68,8 @@ int decode_attention_ctas(const ModelDev& m);  // persistent grid of the decode 
 void launch_decode_attention(const CUtensorMap& map, const EngineDev& e, const ModelDev& m, int layer, const bf16* q,
                              bf16* out, float* part_o, float* part_ml, int max_splits, int chunk, cudaStream_t s);
 // causal flash prefill over the paged pool; blocks[i] = {first row, rows (<= 64), block-table row, first position}
+void set_pdl_mask_attention(int mask);
+void set_pdl_mask_layers(int mask);
 void launch_prefill_flash(const ModelDev& m, int layer, const bf16* q, bf16* out, const int4* blocks, int n_blocks,
                           cudaStream_t s);
 void launch_fork_groups(const EngineDev& e, const ModelDev& m, const ab_sample_desc* descs, int n, cudaStream_t s);
