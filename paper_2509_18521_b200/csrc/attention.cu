@@ -27,7 +27,7 @@ namespace ab {
 namespace {
 
 constexpr float kLog2e = 1.4426950408889634f;
-__constant__ int c_pdl_mask = 7;  // see gemm.cu
+__constant__ int c_pdl_mask = 6;  // see gemm.cu
 constexpr int kTok = 64;        // tokens per tile
 constexpr int kCons = 4;        // consumer warps (16 tokens each)
 constexpr int kThreads = (kCons + 1) * 32;

@@ -337,7 +337,7 @@ int choose_sched(int rows, int N, int K, int max_bn, int cs, int ncl, int force,
 // [4] last MMA committed, [5] epilogue sees the accumulator, [6] epilogue done, [7] exit,
 // [8] split: partial parked, [11] split: cluster barrier passed, [12] first chunk fetched.
 __device__ unsigned long long g_gemm_trace[160 * 16];
-__constant__ int c_pdl_mask = 7;  // early launch_dependents: 1 GEMM, 2 attention, 4 RMSNorm (AB_PDL_MASK)
+__constant__ int c_pdl_mask = 6;  // early launch_dependents: 1 GEMM, 2 attention, 4 RMSNorm (AB_PDL_MASK)
 __device__ __forceinline__ void trace_mark(int on, int k) {
   if (on & 1) {
     unsigned long long t;
@@ -622,6 +622,9 @@ __global__ void __launch_bounds__(kThreads, 1)
       trace_mark(trace, 4);
     }
     }
+    // mask bit 8: trigger the dependents once this CTA's last MMA is issued (its epilogue then
+    // overlaps the successor's launch and pre-wait prologue)
+    if (lane == 0 && (c_pdl_mask & 8)) pdl_launch();
   } else if (warp < 6) {
     // epilogue warps 2..5 -> TMEM lane quadrants 2,3,0,1
     const int quad = warp & 3;

@@ -18,7 +18,7 @@ namespace ab {
 namespace {
 
 constexpr float kLog2e = 1.4426950408889634f;
-__constant__ int c_pdl_mask = 7;  // see gemm.cu
+__constant__ int c_pdl_mask = 6;  // see gemm.cu
 
 __device__ __forceinline__ bool stopped(const int* stop) { return stop != nullptr && *stop != 0; }
 
