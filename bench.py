@@ -137,7 +137,8 @@ def learner_glue(pb, w, out, target_token=0, comm=None):
             merged.update(part)
         mine = merged
     rewards = [mine[s.sample_id] for s in samples]
-    return pb.batch_advantages(rewards, w["g"], w["adv"])
+    pb.batch_advantages(rewards, w["g"], w["adv"])
+    return float(sum(rewards) / len(rewards)) if rewards else 0.0
 
 
 def run_steps(pb, w, sched, eng, k0, n, timed_e2e=False, comm=None):
@@ -146,13 +147,13 @@ def run_steps(pb, w, sched, eng, k0, n, timed_e2e=False, comm=None):
         h2d0 = eng.io_bytes()
         t0 = time.perf_counter()
         out = sched.run_step(k)
-        if timed_e2e:
-            learner_glue(pb, w, out, comm=comm)
+        reward = learner_glue(pb, w, out, comm=comm) if timed_e2e else 0.0
         t1 = time.perf_counter()
         h2d1 = eng.io_bytes()
         recs.append(dict(step=k, tokens=out.tokens_generated, wall=out.rollout_wall_time, host=t1 - t0,
                          iters=out.iterations, carried=out.carried_in_tokens,
-                         h2d=h2d1[0] - h2d0[0], d2h=h2d1[1] - h2d0[1], buffer=out.buffer_size_after))
+                         h2d=h2d1[0] - h2d0[0], d2h=h2d1[1] - h2d0[1], buffer=out.buffer_size_after,
+                         outcome=out, reward=reward))
     return recs
 
 
@@ -234,6 +235,9 @@ def main():
     ap.add_argument("--profile-every", type=int, default=8)
     ap.add_argument("--ref-step-s", type=float, default=12.0)
     ap.add_argument("--seed", type=int, default=0)
+    ap.add_argument("--out", default=None,
+                    help="also write the reference's run outputs (steps.jsonl, summary.json, samples.csv per arm, "
+                         "comparison.json) for the e2e APRIL steps and the sync steps into this directory")
     ap.add_argument("--kv-resume", default="reprefill", choices=["retain", "reprefill"],
                     help="paused partials: re-prefill prompt + carried tokens at resume (the cost APRIL pays when "
                          "weights change every step; inside the rollout wall time) or keep their KV resident")
@@ -314,11 +318,13 @@ def main():
         if dp:
             front_s = DataParallelEngine(GpuLocal(eng_s), comm, w["slots"])
         sch_s = make_scheduler(pb, w, front_s, "baseline", seed, world if dp else 1)
-        rs = run_steps(pb, w, sch_s, eng_s, 0, args.sync_steps)
+        rs = run_steps(pb, w, sch_s, eng_s, 0, args.sync_steps, timed_e2e=args.out is not None, comm=comm)
         sync = {"tokens_per_s": sum(r["tokens"] for r in rs) / sum(r["wall"] for r in rs),
                 "ms_per_step": 1e3 * statistics.mean(r["wall"] for r in rs), "steps": len(rs),
                 "iterations_per_step": statistics.mean(r["iters"] for r in rs)}
         eng_s.close()
+        if args.out and rank == 0:
+            write_outputs(pb, w, args, rec_e2e, rs, world)
 
     # DP: every rank's scheduler already counts the whole job's tokens; replicas: per rank
     total_tokens = tokens if dp else tokens * world
@@ -378,6 +384,34 @@ def main():
         dist.barrier()
         dist.destroy_process_group()
     return 0
+
+
+def write_outputs(pb, w, args, rec_april, rec_sync, world):
+    """The reference CLI's run outputs (cli.py:50-129) for the e2e APRIL steps and the sync steps."""
+    from paper_2509_18521_b200 import report
+    from paper_2509_18521_b200.metrics import build_step_report
+
+    cfg = {"engine": {"backend": "b200", "slots": w["slots"], "max_len": w["l_max"], "model": w["model"],
+                      "kv_resume": args.kv_resume},
+           "run": {"seed": args.seed, "steps": args.steps, "gpus": world},
+           "scheduler": {"rollout_batch_size": w["n"], "samples_per_prompt": w["g"],
+                         "over_sampling_batch_size": w["n_prime"]},
+           "train": {"advantage": w["adv"]},
+           "workload": {"length_dist": "lognormal", "mu": w["mu"], "sigma": w["sigma"], "rho": w["rho"]}}
+    summaries = {}
+    for mode, recs in (("april", rec_april), ("baseline", rec_sync)):
+        # GPU runs have no cost-model peak: idle fraction against the best step of the run
+        peak = max(r["tokens"] / r["wall"] for r in recs if r["wall"] > 0)
+        reps = [build_step_report(r["outcome"], peak, r["host"] - r["wall"], r["reward"]) for r in recs]
+        man = [row for r in recs for row in report.manifest_rows(r["outcome"].step, r["outcome"].batch)]
+        summaries[mode] = pb.summarize_run(reps, buffer_high_water=max(r["buffer"] for r in recs))
+        report.write_run_outputs(os.path.join(args.out, f"{mode}-seed{args.seed}"), reps, summaries[mode],
+                                 dict(cfg, scheduler=dict(cfg["scheduler"], mode=mode)), manifest=man)
+    tp = {m: statistics.mean(r["tokens"] / r["wall"] for r in recs) for m, recs in (("april", rec_april),
+                                                                                  ("baseline", rec_sync))}
+    entry = {"seed": args.seed, "baseline": summaries["baseline"].to_json_dict(),
+             "april": summaries["april"].to_json_dict(), "improvement": tp["april"] / tp["baseline"] - 1.0}
+    report.write_comparison(args.out, [entry], cfg)
 
 
 def _ncu_traffic(workload):

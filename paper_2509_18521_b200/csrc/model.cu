@@ -49,7 +49,7 @@ struct Model {
     GemmPlan qkv_p, o_p, gu_p, down_p;
   };
   std::vector<Plans> dec, pf;
-  GemmPlan lm_dec;
+  GemmPlan lm_dec, lm_dec2;  // lm_head: CTA pair / 1-SM alternative (autotuned)
   int* pf_rows = nullptr;  // device row count for prefill GEMMs
   CUtensorMap kvmap;         // TMA view of the KV pool for the decode attention
   int32_t *ga_g = nullptr, *ga_len = nullptr, *ga_last = nullptr;
@@ -168,6 +168,11 @@ static void autotune_decode(Engine& e, Model* M) {
   apply(M->dec, &Model::Plans::o, &Model::Plans::o2);
   apply(M->dec, &Model::Plans::down, &Model::Plans::down2);
   apply(M->dec, &Model::Plans::gu, &Model::Plans::gu2);
+  {
+    const auto tabs = tune({&M->lm_dec, &M->lm_dec2});
+    gemm_set_table(M->lm_dec, tabs[0]);
+    gemm_set_table(M->lm_dec2, tabs[1]);
+  }
   // prefill chunks (up to M_pf rows): 1-SM plans against CTA-pair plans on a coarse ladder
   ladder.clear();
   for (int r = 64; r < M->M_pf; r *= 4) ladder.push_back(r);
@@ -406,6 +411,8 @@ Model* model_create(Engine& e) {
     M->pf.push_back(p);
   }
   gemm_plan(M->lm_dec, M->lm_head, m.V, m.d, M->xn, M->S, m.d, bn_dec, kEpiF32, M->logits, m.V, nullptr, b, stop, 2, true);
+  gemm_plan(M->lm_dec2, M->lm_head, m.V, m.d, M->xn, M->S, m.d, bn_dec, kEpiF32, M->logits, m.V, nullptr, b, stop, 1);
+  gemm_set_table(M->lm_dec2, std::vector<int>(M->S + 1, 0));  // idle unless the autotuner picks it
   if (ec.gemm_autotune) autotune_decode(e, M);
   M->inv_temp = ec.greedy ? 1.f / std::max(ec.temperature, 1e-6f) : 1.f / ec.temperature;
   if (ec.temperature <= 0.f) M->inv_temp = 1.f;
@@ -678,7 +685,7 @@ void model_release_group(Engine& e, int group_slot) {
 
 // kernels one decode iteration launches (plans with an all-zero table are skipped)
 int64_t model_iter_launches(Model* M) {
-  int64_t n = 5;  // prep, embed, final norm, lm_head, sampler
+  int64_t n = 4 + (M->lm_dec.idle ? 0 : 1) + (M->lm_dec2.idle ? 0 : 1);  // prep, embed, final norm, lm_head, sampler
   for (const auto& p : M->dec) {
     n += 4;  // 2 norms, rope / KV write, attention
     for (const GemmPlan* g : {&p.qkv, &p.qkv2, &p.o, &p.o2, &p.gu, &p.gu2, &p.down, &p.down2}) n += g->idle ? 0 : 1;
@@ -749,6 +756,7 @@ void model_iteration(Engine& e, int64_t run_iter, bool timed) {
   {
     ScopedTimer t(e, timed, "gemm_lm_head", run_iter);
     gemm_launch(M->lm_dec, s);
+    gemm_launch(M->lm_dec2, s);
   }
   {
     ScopedTimer t(e, timed, "sampler", run_iter);
