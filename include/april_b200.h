@@ -197,6 +197,12 @@ int ab_engine_read_payload(ab_engine* e, const int32_t* handles, const int32_t* 
 // Reference: the build's addition for SURVEY.md §8a row a17 (GSPO length-normalised log-prob);
 // the reference computes sequence log-probs on the host (src/april_sim/policy.py:133-137).
 int ab_engine_sequence_logprobs(ab_engine* e, const int32_t* handles, int n, double* sums, int32_t* lens);
+/* Trainer-side recompute (the toy trainer's logp_now, policy.py:157-176): teacher-forced
+ * log-probs of response tokens under the CURRENT weights, at the engine's temperature.  Host arrays:
+ * sequence k = tokens[offs[k] .. offs[k+1]) (prompt + response), prompt_lens[k] >= 1 tokens of prompt;
+ * logprobs receives sum_k (len_k - prompt_lens[k]) values, per sequence in token order. */
+int ab_engine_score(ab_engine* e, const int32_t* tokens, const int64_t* offs, const int32_t* prompt_lens, int n,
+                    double* logprobs);
 int ab_engine_release(ab_engine* e, const int32_t* handles, int n);
 int ab_engine_stats(ab_engine* e, ab_stats* out);
 int ab_engine_profile(ab_engine* e, int enable, int sample_every);

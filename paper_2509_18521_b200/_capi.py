@@ -110,6 +110,7 @@ _SIGS = {
     "ab_engine_active": [P, I32P, I32P, C.c_int, C.POINTER(C.c_int)],
     "ab_engine_read_payload": [P, I32P, I32P, I32P, C.c_int, I32P, F64P],
     "ab_engine_sequence_logprobs": [P, I32P, C.c_int, F64P, I32P],
+    "ab_engine_score": [P, I32P, C.POINTER(C.c_int64), I32P, C.c_int, F64P],
     "ab_engine_release": [P, I32P, C.c_int],
     "ab_engine_stats": [P, C.POINTER(Stats)],
     "ab_engine_profile": [P, C.c_int, C.c_int],

@@ -980,6 +980,16 @@ int ab_engine_sequence_logprobs(ab_engine* e, const int32_t* handles, int n, dou
   return ab::guard([&] { ab::seq_logprob(*e->impl, handles, n, sums, lens); });
 }
 
+int ab_engine_score(ab_engine* e, const int32_t* tokens, const int64_t* offs, const int32_t* prompt_lens, int n,
+                    double* logprobs) {
+  return ab::guard([&] {
+    Engine& g = *e->impl;
+    AB_REQUIRE(g.model != nullptr, AB_ERR_CONTRACT, "scoring needs the transformer model");
+    AB_REQUIRE(n >= 0 && tokens && offs && prompt_lens && logprobs, AB_ERR_CONTRACT, "score: null argument");
+    if (n) ab::model_score(g, tokens, offs, prompt_lens, n, logprobs);
+  });
+}
+
 int ab_engine_release(ab_engine* e, const int32_t* handles, int n) {
   return ab::guard([&] {
     Engine& g = *e->impl;

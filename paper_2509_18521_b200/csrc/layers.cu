@@ -541,6 +541,80 @@ __global__ void k_extend_rows(EngineDev e, ModelDev m, const int4* pieces, int n
   }
 }
 
+// Log-prob scoring: scratch block-table rows get pages for `len` positions each
+// (items[k] = {bt row, positions}), released afterwards by k_score_release.
+__global__ void k_score_alloc(EngineDev e, ModelDev m, const int2* items, int n) {
+  Ctl* c = e.ctl;
+  const int k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= n) return;
+  const int2 it = items[k];
+  int32_t* row = m.bt + (size_t)it.x * m.MP;
+  const int need = (it.y + m.P - 1) / m.P;
+  for (int j = 0; j < need; ++j) {
+    const int idx = pop_page(c);
+    if (idx < 0 || j >= m.MP) {
+      atomicCAS(&c->error, kErrNone, kErrOutOfKV);
+      for (int q = j; q < need; ++q) row[q] = -1;
+      return;
+    }
+    row[j] = m.free_pages[idx];
+  }
+}
+
+__global__ void k_score_release(EngineDev e, ModelDev m, const int2* items, int n) {
+  Ctl* c = e.ctl;
+  const int k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= n) return;
+  const int2 it = items[k];
+  const int32_t* row = m.bt + (size_t)it.x * m.MP;
+  int need = (it.y + m.P - 1) / m.P;
+  while (need > 0 && row[need - 1] < 0) --need;  // (a failed allocation left -1 entries)
+  const long long base =
+      (long long)atomicAdd(reinterpret_cast<unsigned long long*>(&c->kv_free_top), (unsigned long long)need);
+  for (int j = 0; j < need; ++j) m.free_pages[base + j] = row[j];
+}
+
+// dst[i] = src[rows[i]] for bf16 rows of width d (d % 8 == 0)
+__global__ void k_gather_rows(const bf16* __restrict__ src, bf16* __restrict__ dst, const int* __restrict__ rows,
+                              int n, int d) {
+  const int i = blockIdx.x;
+  if (i >= n) return;
+  const uint4* s = reinterpret_cast<const uint4*>(src + (size_t)rows[i] * d);
+  uint4* o = reinterpret_cast<uint4*>(dst + (size_t)i * d);
+  for (int j = threadIdx.x; j < d / 8; j += blockDim.x) o[j] = s[j];
+}
+
+// out[i] = log softmax(logits[i] / T)[target[i]]   (one block per row, fp64 reduction)
+__global__ void __launch_bounds__(256) k_logp_rows(const float* __restrict__ logits, int V,
+                                                   const int* __restrict__ target, int n, float inv_temp,
+                                                   double* __restrict__ out) {
+  const int i = blockIdx.x;
+  if (i >= n) return;
+  const float* z = logits + (size_t)i * V;
+  __shared__ float s_m[8];
+  __shared__ double s_s[8];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  float mx = -FLT_MAX;
+  for (int j = threadIdx.x; j < V; j += blockDim.x) mx = fmaxf(mx, z[j]);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+  if (lane == 0) s_m[w] = mx;
+  __syncthreads();
+  mx = s_m[0];
+  for (int k = 1; k < 8; ++k) mx = fmaxf(mx, s_m[k]);
+  double sum = 0.0;
+  for (int j = threadIdx.x; j < V; j += blockDim.x) sum += (double)__expf((z[j] - mx) * inv_temp);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
+  if (lane == 0) s_s[w] = sum;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double S = 0.0;
+    for (int k = 0; k < 8; ++k) S += s_s[k];
+    out[i] = (double)((z[target[i]] - mx) * inv_temp) - log(S);
+  }
+}
+
 __global__ void k_release(EngineDev e, ModelDev m, const int32_t* handles, int n) {
   Ctl* c = e.ctl;
   const int k = blockIdx.x * blockDim.x + threadIdx.x;
@@ -690,6 +764,20 @@ void launch_resume_fork(const EngineDev& e, const ModelDev& m, const int4* items
 
 void launch_extend_rows(const EngineDev& e, const ModelDev& m, const int4* pieces, int n_pieces, cudaStream_t s) {
   k_extend_rows<<<n_pieces, 256, 0, s>>>(e, m, pieces, n_pieces);
+}
+
+void launch_score_alloc(const EngineDev& e, const ModelDev& m, const int2* items, int n, cudaStream_t s) {
+  k_score_alloc<<<ceil_div(n, 64), 64, 0, s>>>(e, m, items, n);
+}
+void launch_score_release(const EngineDev& e, const ModelDev& m, const int2* items, int n, cudaStream_t s) {
+  k_score_release<<<ceil_div(n, 64), 64, 0, s>>>(e, m, items, n);
+}
+void launch_gather_rows(const bf16* src, bf16* dst, const int* rows, int n, int d, cudaStream_t s) {
+  k_gather_rows<<<n, 128, 0, s>>>(src, dst, rows, n, d);
+}
+void launch_logp_rows(const float* logits, int V, const int* target, int n, float inv_temp, double* out,
+                      cudaStream_t s) {
+  k_logp_rows<<<n, 256, 0, s>>>(logits, V, target, n, inv_temp, out);
 }
 
 void launch_release_handles(const EngineDev& e, const ModelDev& m, const int32_t* handles, int n, cudaStream_t s) {

@@ -50,6 +50,12 @@ struct Model {
   };
   std::vector<Plans> dec, pf;
   GemmPlan lm_dec, lm_dec2;  // lm_head: CTA pair / 1-SM alternative (autotuned)
+  // log-prob scoring (model_score): gathered final-norm rows -> lm_head -> log-softmax at the targets
+  GemmPlan lm_score;
+  bf16* score_a = nullptr;
+  int *score_rows = nullptr, *score_idx = nullptr, *score_tgt = nullptr;
+  double* score_out = nullptr;
+  int2* score_items = nullptr;
   int* pf_rows = nullptr;  // device row count for prefill GEMMs
   CUtensorMap kvmap;         // TMA view of the KV pool for the decode attention
   int32_t *ga_g = nullptr, *ga_len = nullptr, *ga_last = nullptr;
@@ -74,6 +80,8 @@ struct Model {
 };
 
 namespace {
+
+constexpr int kScoreRows = 64;  // scratch block-table rows: sequences scored per batch
 
 template <typename T>
 T* dalloc(size_t n) {
@@ -313,7 +321,7 @@ Model* model_create(Engine& e) {
   m.g_ctx = dalloc<int32_t>(m.G_cap);
   m.g_last_tok = dalloc<int32_t>(m.G_cap);
   m.g_npages = dalloc<int32_t>(m.G_cap);
-  m.bt = dalloc<int32_t>((size_t)(m.H + m.G_cap) * m.MP);
+  m.bt = dalloc<int32_t>((size_t)(m.H + m.G_cap + kScoreRows) * m.MP);  // + scratch rows for scoring
   m.rope = dalloc<float2>((size_t)m.max_pos * (m.hd / 2));
   launch_rope_table(m.rope, m.max_pos, m.hd, c.rope_theta, s);
   M->pf_rows = dalloc<int>(1);
@@ -411,6 +419,14 @@ Model* model_create(Engine& e) {
     M->pf.push_back(p);
   }
   gemm_plan(M->lm_dec, M->lm_head, m.V, m.d, M->xn, M->S, m.d, bn_dec, kEpiF32, M->logits, m.V, nullptr, b, stop, 2, true);
+  M->score_a = dalloc<bf16>((size_t)M->S * m.d);
+  M->score_rows = dalloc<int>(1);
+  M->score_idx = dalloc<int>(M->S);
+  M->score_tgt = dalloc<int>(M->S);
+  M->score_out = dalloc<double>(M->S);
+  M->score_items = dalloc<int2>(kScoreRows);
+  gemm_plan(M->lm_score, M->lm_head, m.V, m.d, M->score_a, M->S, m.d, bn_dec, kEpiF32, M->logits, m.V, nullptr,
+            M->score_rows, nullptr, 2, true);
   gemm_plan(M->lm_dec2, M->lm_head, m.V, m.d, M->xn, M->S, m.d, bn_dec, kEpiF32, M->logits, m.V, nullptr, b, stop, 1);
   gemm_set_table(M->lm_dec2, std::vector<int>(M->S + 1, 0));  // idle unless the autotuner picks it
   if (ec.gemm_autotune) autotune_decode(e, M);
@@ -428,7 +444,8 @@ void model_destroy(Model* M) {
                   m.h_last_tok, m.h_shared, m.g_ctx,      m.g_last_tok, m.g_npages,   m.bt,        m.rope,
                   M->pf_rows,  M->ga_g,     M->ga_len,    M->ga_last,  m.kv,
                   m.free_pages, m.split_prefix, m.att_counter, m.att_ctl, M->pf_blocks, M->rs_items,
-                  M->rs_pieces};
+                  M->rs_pieces, M->score_a, M->score_rows, M->score_idx, M->score_tgt, M->score_out,
+                  M->score_items};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   if (M->host_stage) cudaFreeHost(M->host_stage);
@@ -627,6 +644,96 @@ static void resume_reprefill(Engine& e, const ab_sample_desc* descs, int n) {
     }
   }
   run_chunk();
+}
+
+// Teacher-forced log-probs of response tokens under the current weights (the trainer's
+// recompute of pi_theta on a mixed-policy batch).  Sequence k = tokens[offs[k], offs[k+1]), its first
+// plen[k] tokens the prompt; out receives, per sequence in order, log pi(token_p | tokens_<p) / T for
+// p = plen .. len-1.  Runs the prefill pass over positions 0..len-2 into scratch block-table rows
+// (pages borrowed from the pool and returned), then the final norm, lm_head and a log-softmax at the
+// target token for the rows that predict a response token.
+void model_score(Engine& e, const int32_t* tokens, const int64_t* offs, const int32_t* plen, int n, double* out) {
+  Model* M = e.model;
+  ModelDev& m = M->md;
+  cudaStream_t s = e.stream;
+  flush_prefill(e);
+  std::vector<int64_t> ob(n + 1, 0);
+  for (int k = 0; k < n; ++k) {
+    const int64_t len = offs[k + 1] - offs[k];
+    AB_REQUIRE(plen[k] >= 1 && len > plen[k], AB_ERR_CONTRACT, "score: every sequence needs a prompt and a response");
+    AB_REQUIRE(len <= (int64_t)m.max_pos, AB_ERR_CONTRACT, "score: sequence longer than the engine's positions");
+    for (int64_t p = offs[k]; p < offs[k + 1]; ++p)
+      AB_REQUIRE(tokens[p] >= 0 && tokens[p] < m.V, AB_ERR_CONTRACT, "score: token out of vocabulary");
+    ob[k + 1] = ob[k] + (len - plen[k]);
+  }
+  const int row0 = m.H + m.G_cap;
+  std::vector<int32_t> tok, pos, btr;
+  std::vector<int> tgt_row, tgt_tok;
+  std::vector<int64_t> tgt_out;
+  auto run_targets = [&]() {
+    for (size_t c0 = 0; c0 < tgt_row.size(); c0 += M->S) {
+      const int cnt = (int)std::min<size_t>(M->S, tgt_row.size() - c0);
+      AB_CUDA(cudaMemcpyAsync(M->score_idx, tgt_row.data() + c0, sizeof(int) * cnt, cudaMemcpyHostToDevice, s));
+      AB_CUDA(cudaMemcpyAsync(M->score_tgt, tgt_tok.data() + c0, sizeof(int) * cnt, cudaMemcpyHostToDevice, s));
+      AB_CUDA(cudaMemcpyAsync(M->score_rows, &cnt, sizeof(int), cudaMemcpyHostToDevice, s));
+      launch_gather_rows(M->xn, M->score_a, M->score_idx, cnt, m.d, s);
+      gemm_launch(M->lm_score, s);
+      launch_logp_rows(M->logits, m.V, M->score_tgt, cnt, M->inv_temp, M->score_out, s);
+      std::vector<double> h(cnt);
+      AB_CUDA(cudaMemcpyAsync(h.data(), M->score_out, sizeof(double) * cnt, cudaMemcpyDeviceToHost, s));
+      AB_CUDA(cudaStreamSynchronize(s));
+      for (int i = 0; i < cnt; ++i) out[tgt_out[c0 + i]] = h[i];
+      e.launches += 3;
+    }
+  };
+  for (int k0 = 0; k0 < n; k0 += kScoreRows) {
+    const int nb_items = std::min(kScoreRows, n - k0);
+    std::vector<int2> items(nb_items);
+    for (int i = 0; i < nb_items; ++i) items[i] = make_int2(row0 + i, (int)(offs[k0 + i + 1] - offs[k0 + i] - 1));
+    AB_CUDA(cudaMemcpyAsync(M->score_items, items.data(), sizeof(int2) * nb_items, cudaMemcpyHostToDevice, s));
+    launch_score_alloc(e.d, m, M->score_items, nb_items, s);
+    e.launches += 1;
+    check_kv(e);
+    int R = 0, nb = 0;
+    tok.clear(), pos.clear(), btr.clear(), tgt_row.clear(), tgt_tok.clear(), tgt_out.clear();
+    auto run_chunk = [&]() {
+      if (!R) return;
+      AB_CUDA(cudaMemcpyAsync(m.row_tok, tok.data(), sizeof(int32_t) * R, cudaMemcpyHostToDevice, s));
+      AB_CUDA(cudaMemcpyAsync(m.row_pos, pos.data(), sizeof(int32_t) * R, cudaMemcpyHostToDevice, s));
+      AB_CUDA(cudaMemcpyAsync(m.row_btrow, btr.data(), sizeof(int32_t) * R, cudaMemcpyHostToDevice, s));
+      prefill_rows(e, R, nb);
+      launch_rmsnorm(M->x, M->final_norm, M->xn, m.d, m.eps, nullptr, R, nullptr, s);
+      e.launches += 1;
+      run_targets();
+      tok.clear(), pos.clear(), btr.clear(), tgt_row.clear(), tgt_tok.clear(), tgt_out.clear();
+      R = nb = 0;
+    };
+    for (int i = 0; i < nb_items; ++i) {
+      const int k = k0 + i;
+      const int32_t* seq = tokens + offs[k];
+      const int len = (int)(offs[k + 1] - offs[k]);
+      for (int p0 = 0; p0 < len - 1;) {
+        if (R == M->M_pf) run_chunk();
+        const int cnt = std::min(len - 1 - p0, M->M_pf - R);
+        nb = add_blocks(M, nb, R, cnt, row0 + i, p0);
+        for (int p = p0; p < p0 + cnt; ++p, ++R) {
+          tok.push_back(seq[p]);
+          pos.push_back(p);
+          btr.push_back(row0 + i);
+          if (p >= plen[k] - 1) {
+            tgt_row.push_back(R);
+            tgt_tok.push_back(seq[p + 1]);
+            tgt_out.push_back(ob[k] + (p - (plen[k] - 1)));
+          }
+        }
+        p0 += cnt;
+      }
+    }
+    run_chunk();
+    launch_score_release(e.d, m, M->score_items, nb_items, s);
+    e.launches += 1;
+    AB_CUDA(cudaStreamSynchronize(s));
+  }
 }
 
 void model_begin_step(Engine& e, int64_t version) {

@@ -75,6 +75,11 @@ void launch_prefill_flash(const ModelDev& m, int layer, const bf16* q, bf16* out
 void launch_fork_groups(const EngineDev& e, const ModelDev& m, const ab_sample_desc* descs, int n, cudaStream_t s);
 void launch_resume_fork(const EngineDev& e, const ModelDev& m, const int4* items, int n, cudaStream_t s);
 void launch_extend_rows(const EngineDev& e, const ModelDev& m, const int4* pieces, int n_pieces, cudaStream_t s);
+void launch_score_alloc(const EngineDev& e, const ModelDev& m, const int2* items, int n, cudaStream_t s);
+void launch_score_release(const EngineDev& e, const ModelDev& m, const int2* items, int n, cudaStream_t s);
+void launch_gather_rows(const bf16* src, bf16* dst, const int* rows, int n, int d, cudaStream_t s);
+void launch_logp_rows(const float* logits, int V, const int* target, int n, float inv_temp, double* out,
+                      cudaStream_t s);
 void launch_release_handles(const EngineDev& e, const ModelDev& m, const int32_t* handles, int n, cudaStream_t s);
 void launch_group_alloc(const EngineDev& e, const ModelDev& m, const int* groups, const int* lens,
                         const int* last_tok, int n, cudaStream_t s);

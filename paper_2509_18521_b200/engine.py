@@ -468,6 +468,38 @@ class Engine:
         self._release(drained)  # zero-token samples hold no device state worth keeping
         return out
 
+    def score(self, prompts, responses) -> list:
+        """Teacher-forced log-probs (at the engine's temperature) of each response token under the
+        CURRENT weights: the trainer's recompute of pi_theta on a mixed-policy batch (SURVEY §8 f2;
+        policy.py:157-176 uses it against the behaviour log-probs).  prompts / responses: sequences of
+        token ids; returns one float64 array per response."""
+        if self._model_kind != capi.MODEL_TRANSFORMER:
+            raise ContractViolation("scoring needs the transformer model")
+        if len(prompts) != len(responses):
+            raise ContractViolation("score: one prompt per response")
+        n = len(prompts)
+        if n == 0:
+            return []
+        self._flush()
+        seqs = [np.concatenate([np.asarray(p, dtype=np.int32), np.asarray(r, dtype=np.int32)])
+                for p, r in zip(prompts, responses)]
+        toks = np.ascontiguousarray(np.concatenate(seqs), dtype=np.int32)
+        offs = np.zeros(n + 1, dtype=np.int64)
+        offs[1:] = np.cumsum([len(s) for s in seqs])
+        plen = np.ascontiguousarray([len(p) for p in prompts], dtype=np.int32)
+        nres = [len(r) for r in responses]
+        out = np.empty(sum(nres), dtype=np.float64)
+        capi.call("ab_engine_score", self._h, toks.ctypes.data_as(capi.I32P),
+                  offs.ctypes.data_as(C.POINTER(C.c_int64)), plen.ctypes.data_as(capi.I32P), n,
+                  out.ctypes.data_as(capi.F64P))
+        self._h2d += toks.nbytes + offs.nbytes + plen.nbytes
+        self._d2h += out.nbytes
+        return list(np.split(out, np.cumsum(nres)[:-1]))
+
+    def recompute_logprobs(self, samples) -> list:
+        """score() of delivered samples against their prompts (prompt_source) and generated tokens."""
+        return self.score([self.prompt_source(s.instance_id) for s in samples], [s.token_ids() for s in samples])
+
     def sequence_logprobs(self, samples):
         """(sum of behaviour log-probs over all generated tokens, token count) per sample, reduced
         on the device from the resident partial-rollout payload (GSPO's length-normalised sequence

@@ -265,3 +265,38 @@ def test_reprefill_resume_matches_oracle(preset, layers, page):
     assert eng.stats().kv_pages_free == free0
     eng.close()
 
+
+
+@pytest.mark.parametrize("preset,layers", [("tiny", None), ("qwen2.5-1.5b", 2), ("qwen3-4b", 1)])
+def test_score_recomputes_behaviour_logprobs(preset, layers):
+    """Trainer-side recompute: teacher-forced log-probs of delivered responses under the
+    current weights match the oracle's, and (same weights) the behaviour log-probs recorded while
+    sampling; one response longer than a page, prompts of different lengths."""
+    spec = pb.PRESETS[preset]
+    if layers:
+        spec = spec.truncated(layers)
+    prompts = {0: pb.synthetic_prompt(11, 0, 23, spec.vocab), 1: pb.synthetic_prompt(11, 1, 40, spec.vocab)}
+    eng = _engine(spec, prompts, greedy=False, temperature=0.9, l_max=128)
+    free0 = eng.stats().kv_pages_free
+    eng.begin_step(0)
+    samples = []
+    for iid, L in ((0, 70), (0, 9), (1, 33)):
+        s = RolloutSample(iid, len(samples))
+        s.target_length = L
+        eng.submit(s)
+        samples.append(s)
+    _drain(eng)
+    now = eng.recompute_logprobs(samples)
+    assert eng.stats().kv_pages_free == free0  # the scratch pages went back to the pool
+    dec = CpuDecoder(spec, eng.export_weights())
+    for s, lp in zip(samples, now):
+        beh = np.asarray(s.behavior_logprob_trace())
+        assert lp.shape == beh.shape
+        assert np.max(np.abs(lp - beh)) < LOGP_TOL
+        sc = dec.score([int(t) for t in prompts[s.instance_id]], s.token_ids(), temperature=0.9)
+        ref = np.array([r["logp"] for r in sc])
+        assert np.max(np.abs(lp - ref)) < LOGP_TOL
+    ratios, masks, _ = pb.policy.clipped_ratio_terms(now, [s.behavior_logprob_trace() for s in samples],
+                                                     [1.0, -1.0, 0.5])
+    assert all(np.all(np.abs(r - 1.0) < 0.06) for r in ratios)
+    eng.close()
