@@ -10,6 +10,7 @@
 #include <cuda_bf16.h>
 
 #include <cfloat>
+#include <cstdlib>
 
 #include "model.cuh"
 
@@ -19,6 +20,7 @@ namespace {
 
 constexpr float kLog2e = 1.4426950408889634f;
 __constant__ int c_pdl_mask = 6;  // see gemm.cu
+__constant__ int c_rope_zero = 1;  // debug timing only (AB_ROPE_NOZERO): 0 skips the workspace re-zero
 
 __device__ __forceinline__ bool stopped(const int* stop) { return stop != nullptr && *stop != 0; }
 
@@ -398,12 +400,14 @@ __global__ void k_rope_kv_f32(ModelDev m, int layer, float* __restrict__ qkv, co
         load_pairs<NP>(nw_ + lane * NP + HD / 2, wb);
       }
     }
-    if constexpr (NP == 2) {
-      *reinterpret_cast<float2*>(pa) = make_float2(0.f, 0.f);
-      *reinterpret_cast<float2*>(pb) = make_float2(0.f, 0.f);
-    } else {
-      *pa = 0.f;
-      *pb = 0.f;
+    if (c_rope_zero) {
+      if constexpr (NP == 2) {
+        *reinterpret_cast<float2*>(pa) = make_float2(0.f, 0.f);
+        *reinterpret_cast<float2*>(pb) = make_float2(0.f, 0.f);
+      } else {
+        *pa = 0.f;
+        *pb = 0.f;
+      }
     }
 #pragma unroll
     for (int j = 0; j < NP; ++j) {
@@ -671,7 +675,11 @@ __global__ void k_group_release(EngineDev e, ModelDev m, int g) {
 // launchers
 // ---------------------------------------------------------------------------
 
-void set_pdl_mask_layers(int mask) { AB_CUDA(cudaMemcpyToSymbol(c_pdl_mask, &mask, sizeof(int))); }
+void set_pdl_mask_layers(int mask) {
+  AB_CUDA(cudaMemcpyToSymbol(c_pdl_mask, &mask, sizeof(int)));
+  const int z = getenv("AB_ROPE_NOZERO") ? 0 : 1;  // timing experiments only: results are then wrong
+  AB_CUDA(cudaMemcpyToSymbol(c_rope_zero, &z, sizeof(int)));
+}
 
 void launch_init_weights(bf16* w, size_t n, uint64_t seed, uint64_t tensor_id, float std, float constant,
                          cudaStream_t s) {
