@@ -549,6 +549,34 @@ class Engine:
                                                                                                     c.value)
         return out
 
+    def load_weights(self, tensors: dict) -> None:
+        """Install new policy weights (the weight-version swap between RL steps).
+        `tensors` maps export_weights() names to bf16 tensors of the same shape (host or device).
+        Call between steps; with kv_resume="reprefill" the next begin_step(version) recomputes the
+        resident prompt KV and resumed partials are re-prefilled under the new weights."""
+        import torch
+
+        if not self.idle:
+            raise ContractViolation("load_weights requires an idle engine")
+        n = C.c_int()
+        capi.call("ab_engine_weight_count", self._h, C.byref(n))
+        name = C.create_string_buffer(128)
+        index = {}
+        for i in range(n.value):
+            r, c = C.c_int64(), C.c_int64()
+            capi.call("ab_engine_weight_info", self._h, i, name, 128, C.byref(r), C.byref(c))
+            index[name.value.decode()] = (i, r.value, c.value)
+        for k, t in tensors.items():
+            if k not in index:
+                raise ConfigError(f"unknown weight {k!r}")
+            i, r, c = index[k]
+            t = t.detach().to(torch.bfloat16).contiguous()
+            if tuple(t.shape) != (r, c) and t.numel() != r * c:
+                raise ConfigError(f"weight {k!r}: expected {r}x{c}, got {tuple(t.shape)}")
+            capi.call("ab_engine_set_weight", self._h, i, C.c_void_p(t.data_ptr()), r * c * 2)
+            if not t.is_cuda:
+                self._h2d += r * c * 2
+
     # -- profiling ---------------------------------------------------------------------------
 
     def profile(self, enable: bool = True, sample_every: int = 8) -> None:

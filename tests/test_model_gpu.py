@@ -300,3 +300,46 @@ def test_score_recomputes_behaviour_logprobs(preset, layers):
                                                      [1.0, -1.0, 0.5])
     assert all(np.all(np.abs(r - 1.0) < 0.06) for r in ratios)
     eng.close()
+
+
+def test_weight_swap_then_reprefill_resume_follows_new_weights():
+    """SURVEY §8 f4 + f1: new policy weights are installed between steps; the resumed partials' KV is
+    re-prefilled under them, so every token generated after the resume is the new model's choice given
+    the whole (mixed-policy) history.  Checked teacher-forced against the oracle with the new weights."""
+    spec = pb.PRESETS["qwen2.5-1.5b"].truncated(2)
+    prompts = _prompts(spec, 1, 30)
+    eng = _engine(spec, prompts, page=16, l_max=128, kv_resume="reprefill")
+    eng.begin_step(0)
+    samples = []
+    for j in range(2):
+        s = RolloutSample(0, j)
+        s.target_length = 60 + 5 * j
+        eng.submit(s)
+        samples.append(s)
+    for _ in range(25):
+        eng.decode_iteration()
+    paused = eng.abort_active()
+    w = eng.export_weights()
+    g = torch.Generator().manual_seed(7)
+    new = {}
+    for k, t in w.items():
+        if "norm" in k:
+            continue
+        new[k] = (t.float() + 0.02 * torch.randn(t.shape, generator=g)).to(torch.bfloat16)
+    eng.load_weights(new)
+    eng.begin_step(1)
+    for p in paused:
+        eng.submit(p)
+    _drain(eng)
+    dec = CpuDecoder(spec, eng.export_weights())
+    for s in samples:
+        toks, lps = s.token_ids(), s.behavior_logprob_trace()
+        sc = dec.score([int(t) for t in prompts[0]], toks)
+        flips = 0
+        for k in range(25, len(toks)):
+            if sc[k]["argmax"] != toks[k]:
+                flips += 1
+                assert sc[k]["margin"] < MARGIN_EPS, (k, sc[k])
+            assert abs(lps[k] - sc[k]["logp"]) < LOGP_TOL, (k, lps[k], sc[k])
+        assert flips <= 4
+    eng.close()
