@@ -181,6 +181,10 @@ int ab_engine_begin_step(ab_engine* e, int64_t version, const double* cf_logits)
 /* transformer: prefill a prompt group's shared prefix into KV pages */
 int ab_engine_open_group(ab_engine* e, int32_t group_slot, const int32_t* prompt, int32_t prompt_len);
 int ab_engine_release_group(ab_engine* e, int32_t group_slot);
+/* KV memory hand-off (kv_resume = 1 only): free the KV pool of an idle engine for a
+ * co-located trainer, then re-acquire it (resident prompt KV is recomputed by the next submit). */
+int ab_engine_release_memory(ab_engine* e);
+int ab_engine_resume_memory(ab_engine* e);
 int ab_engine_submit(ab_engine* e, const ab_sample_desc* descs, int n);
 /* preset per-group completed-sample counts: n pairs (group_slot, count) */
 int ab_engine_set_group_done(ab_engine* e, const int32_t* slot_count_pairs, int n);

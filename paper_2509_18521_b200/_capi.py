@@ -99,7 +99,8 @@ _SIGS = {
     "ab_engine_weight_info": [P, C.c_int, C.c_char_p, C.c_int, C.POINTER(C.c_int64), C.POINTER(C.c_int64)],
     "ab_engine_get_weight": [P, C.c_int, P, C.c_size_t],
     "ab_engine_set_weight": [P, C.c_int, P, C.c_size_t],
-    "ab_engine_set_weight": [P, C.c_int, P, C.c_size_t],
+    "ab_engine_release_memory": [P],
+    "ab_engine_resume_memory": [P],
     "ab_engine_begin_step": [P, C.c_int64, F64P],
     "ab_engine_open_group": [P, C.c_int32, I32P, C.c_int32],
     "ab_engine_release_group": [P, C.c_int32],

@@ -1012,6 +1012,33 @@ int ab_engine_open_group(ab_engine* e, int32_t group_slot, const int32_t* prompt
   });
 }
 
+// KV memory hand-off: free the KV pool while a co-located trainer runs, then
+// re-acquire it.  Re-prefill mode only (paused partials hold no KV there); the resident prompt KV
+// is recomputed by the next submit.  The captured iteration graphs embed the pool address and are
+// re-captured.
+int ab_engine_release_memory(ab_engine* e) {
+  return ab::guard([&] {
+    Engine& g = *e->impl;
+    AB_REQUIRE(g.model != nullptr, AB_ERR_CONTRACT, "engine has no transformer model");
+    AB_REQUIRE(g.cfg.kv_resume == 1, AB_ERR_CONTRACT, "releasing the KV pool needs kv_resume = reprefill");
+    sync_ctl(g);
+    AB_REQUIRE(g.ctl_host->b == 0 && g.ctl_host->q_tail == g.ctl_host->q_head, AB_ERR_CONTRACT,
+               "release_memory requires an idle engine");
+    ab::model_release_memory(g);
+  });
+}
+
+int ab_engine_resume_memory(ab_engine* e) {
+  return ab::guard([&] {
+    Engine& g = *e->impl;
+    AB_REQUIRE(g.model != nullptr, AB_ERR_CONTRACT, "engine has no transformer model");
+    ab::model_resume_memory(g);
+    if (g.iter_graph) cudaGraphExecDestroy(g.iter_graph);
+    if (g.prof_graph) cudaGraphExecDestroy(g.prof_graph);
+    g.iter_graph = g.prof_graph = nullptr;
+  });
+}
+
 int ab_engine_release_group(ab_engine* e, int32_t group_slot) {
   return ab::guard([&] {
     Engine& g = *e->impl;

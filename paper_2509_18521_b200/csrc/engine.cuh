@@ -134,6 +134,8 @@ void model_submit(Engine& e, const ab_sample_desc* descs_dev, int n);  // after 
 void model_release(Engine& e, const int32_t* handles_dev, int n);
 void model_evict(Engine& e, const int32_t* handles_host, const int32_t* gen, int n);  // kv_resume: drop private KV
 void model_begin_step(Engine& e, int64_t version);
+void model_release_memory(Engine& e);
+void model_resume_memory(Engine& e);
 void model_score(Engine& e, const int32_t* tokens, const int64_t* offs, const int32_t* plen, int n, double* out);
 int64_t model_iter_launches(Model* m);
 void model_iteration(Engine& e, int64_t run_iter, bool timed);         // pages + forward + sampler

@@ -76,6 +76,8 @@ struct Model {
   std::vector<char> evicted;
   int4 *rs_items = nullptr, *rs_pieces = nullptr;
   int64_t last_version = -1;
+  size_t kv_bytes = 0;
+  bool kv_released = false;
   float inv_temp = 1.f;
 };
 
@@ -353,6 +355,7 @@ Model* model_create(Engine& e) {
   AB_REQUIRE(np * m.P < (int64_t(1) << 31), AB_ERR_CONFIG, "KV pool too large for 32-bit token slots");
   m.NP = np;
   m.kv = dalloc<bf16>((size_t)np * page_bytes / 2);
+  M->kv_bytes = (size_t)np * page_bytes;
   m.free_pages = dalloc<int32_t>(np);
   {
     std::vector<int32_t> fp(np);
@@ -736,6 +739,31 @@ void model_score(Engine& e, const int32_t* tokens, const int64_t* offs, const in
   }
 }
 
+void model_release_memory(Engine& e) {
+  Model* M = e.model;
+  AB_REQUIRE(!M->kv_released, AB_ERR_CONTRACT, "KV pool already released");
+  AB_CUDA(cudaStreamSynchronize(e.stream));
+  AB_CUDA(cudaFree(M->md.kv));
+  M->md.kv = nullptr;
+  M->kv_released = true;
+}
+
+void model_resume_memory(Engine& e) {
+  Model* M = e.model;
+  AB_REQUIRE(M->kv_released, AB_ERR_CONTRACT, "KV pool is not released");
+  void* p = nullptr;
+  AB_CUDA(cudaMalloc(&p, M->kv_bytes));
+  M->md.kv = reinterpret_cast<bf16*>(p);
+  make_kv_tmap(&M->kvmap, M->md);
+  M->kv_released = false;
+  // the pool's contents are gone: every resident prompt group is prefilled again in place
+  for (auto& kv : M->prompts) {
+    bool queued = false;
+    for (auto& pg : M->pending) queued |= pg.g == kv.first;
+    if (!queued) M->pending.push_back({kv.first, kv.second, true});
+  }
+}
+
 void model_begin_step(Engine& e, int64_t version) {
   Model* M = e.model;
   if (!e.cfg.kv_resume) return;
@@ -754,6 +782,7 @@ void model_begin_step(Engine& e, int64_t version) {
 }
 
 void model_submit(Engine& e, const ab_sample_desc* descs_dev, int n) {
+  AB_REQUIRE(!e.model->kv_released, AB_ERR_CONTRACT, "KV pool released: call resume_memory first");
   const auto t0 = std::chrono::steady_clock::now();
   bool recompute = false;
   for (auto& pg : e.model->pending) recompute |= pg.in_place;

@@ -577,6 +577,15 @@ class Engine:
             if not t.is_cuda:
                 self._h2d += r * c * 2
 
+    def release_memory(self) -> None:
+        """Free the KV pool of an idle engine (kv_resume="reprefill") so a co-located trainer can use
+        the HBM between rollout steps (torch_memory_saver-style pause)."""
+        capi.call("ab_engine_release_memory", self._h)
+
+    def resume_memory(self) -> None:
+        """Re-acquire the KV pool; resident prompt KV is recomputed by the next submit."""
+        capi.call("ab_engine_resume_memory", self._h)
+
     # -- profiling ---------------------------------------------------------------------------
 
     def profile(self, enable: bool = True, sample_every: int = 8) -> None:

@@ -343,3 +343,40 @@ def test_weight_swap_then_reprefill_resume_follows_new_weights():
             assert abs(lps[k] - sc[k]["logp"]) < LOGP_TOL, (k, lps[k], sc[k])
         assert flips <= 4
     eng.close()
+
+
+def test_kv_memory_release_and_resume():
+    """SURVEY §8 f4 memory hand-off: between steps the KV pool is freed (HBM returns to the device)
+    and re-acquired; resident prompt KV is recomputed and the resumed partials are re-prefilled, so
+    decoding continues exactly as the model dictates (oracle, teacher-forced)."""
+    spec = pb.PRESETS["tiny"]
+    prompts = _prompts(spec, 2, 21)
+    eng = _engine(spec, prompts, l_max=128, kv_resume="reprefill")
+    eng.begin_step(0)
+    samples = []
+    for iid in (0, 1):
+        s = RolloutSample(iid, 0)
+        s.target_length = 50 + 7 * iid
+        eng.submit(s)
+        samples.append(s)
+    for _ in range(20):
+        eng.decode_iteration()
+    paused = eng.abort_active()
+    free_before = torch.cuda.mem_get_info()[0]
+    eng.release_memory()
+    assert torch.cuda.mem_get_info()[0] > free_before  # the pool went back to the device
+    with pytest.raises(pb.ContractViolation):
+        eng.submit(paused[0])
+        eng._flush()
+    eng._pending.clear()
+    eng._queue.clear()
+    eng.resume_memory()
+    eng.begin_step(1)
+    for p in paused:
+        eng.submit(p)
+    _drain(eng)
+    dec = CpuDecoder(spec, eng.export_weights())
+    flips = sum(_check_greedy(dec, prompts[s.instance_id], s.token_ids(), s.behavior_logprob_trace())
+                for s in samples)
+    assert flips <= 3
+    eng.close()
