@@ -137,10 +137,11 @@ static void autotune_decode(Engine& e, Model* M) {
     if (it != cache.end()) return it->second;
     if (!flush) AB_CUDA(cudaMalloc(&flush, flush_bytes));
     std::vector<std::vector<int>> tabs(g.size(), std::vector<int>(cur_cap + 1, 0));
-    int lo = 1;
-    for (int r : ladder) {
-      double best = 1e30;
-      int bp = -1, bc = 0;
+    // per ladder row, each plan's best (time, code)
+    std::vector<std::vector<std::pair<double, int>>> best(ladder.size(),
+                                                          std::vector<std::pair<double, int>>(g.size(), {1e30, 0}));
+    for (size_t li = 0; li < ladder.size(); ++li) {
+      const int r = ladder[li];
       for (size_t i = 0; i < g.size(); ++i)
         for (int c : gemm_candidates(*g[i], r)) {
           if (log_all) {
@@ -148,18 +149,38 @@ static void autotune_decode(Engine& e, Model* M) {
             fflush(stderr);
           }
           const double us = gemm_time_code(*g[i], r, c, 3, flush, flush_bytes, s);
-          if (us < best) {
-            best = us;
-            bp = (int)i;
-            bc = c;
-          }
+          if (us < best[li][i].first) best[li][i] = {us, c};
         }
-      if (bp >= 0)
-        for (int x = lo; x <= r; ++x) tabs[bp][x] = bc;
+    }
+    // A plan that is launched costs ~2 us even when its table entry is 0 (the launch, the wait on
+    // its predecessor, the exit): keep both plans only if the second one saves more than that at
+    // some row count; otherwise run every row count on the single best plan.
+    constexpr double kIdleUs = 2.0;
+    std::vector<double> tot(g.size(), 0.0);
+    bool need_both = false;
+    for (size_t li = 0; li < ladder.size(); ++li)
+      for (size_t i = 0; i < g.size(); ++i) tot[i] += best[li][i].first;
+    int single = 0;
+    for (size_t i = 1; i < g.size(); ++i)
+      if (tot[i] < tot[single]) single = (int)i;
+    for (size_t li = 0; li < ladder.size() && g.size() > 1; ++li) {
+      double mn = 1e30;
+      for (size_t i = 0; i < g.size(); ++i) mn = std::min(mn, best[li][i].first);
+      if (best[li][single].first - mn > kIdleUs) need_both = true;
+    }
+    int lo = 1;
+    for (size_t li = 0; li < ladder.size(); ++li) {
+      const int r = ladder[li];
+      int bp = single;
+      if (need_both)
+        for (size_t i = 0; i < g.size(); ++i)
+          if (best[li][i].first < best[li][bp].first) bp = (int)i;
+      if (best[li][bp].first < 1e29)
+        for (int x = lo; x <= r; ++x) tabs[bp][x] = best[li][bp].second;
       if (log)
-        fprintf(stderr, "[autotune] N=%d K=%d epi=%d rows=%d plan=%d (cluster %d%s) code=0x%x %.1f us\n", g[0]->N,
-                g[0]->K, g[0]->epi, r, bp, bp >= 0 ? g[bp]->cluster : 0, bp >= 0 && g[bp]->pair ? " pair" : "", bc,
-                best);
+        fprintf(stderr, "[autotune] N=%d K=%d epi=%d rows=%d plan=%d (cluster %d%s) code=0x%x %.1f us (%s)\n", g[0]->N,
+                g[0]->K, g[0]->epi, r, bp, g[bp]->cluster, g[bp]->pair ? " pair" : "", best[li][bp].second,
+                best[li][bp].first, need_both ? "both plans" : "single plan");
       lo = r + 1;
     }
     cache[key] = tabs;
