@@ -403,7 +403,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (stop || rows <= 0) return pdl_wait();
   const int code = sched_tab[rows];
   if (code == 0) {  // an idle partner plan: let the successor go, then wait
-    if (c_pdl_mask & 1) pdl_launch();
+    if ((c_pdl_mask & 1) || (trace & 0x100)) pdl_launch();
     return pdl_wait();
   }
   const Sched sc = sched_from(code, rows, N, K);
@@ -446,7 +446,9 @@ __global__ void __launch_bounds__(kThreads, 1)
   const uint32_t tmem = *tmem_slot;
   const uint32_t leader = (uint32_t)(crank & ~1);
   if (threadIdx.x == 0) trace_mark(trace, 1);
-  if (c_pdl_mask & 1) pdl_launch();  // the successor may start its own pre-wait prologue
+  // the successor may start its own pre-wait prologue (per plan: only where the successor is a small
+  // kernel that does not compete for this grid's SMs, e.g. the RMSNorm after the residual GEMMs)
+  if ((c_pdl_mask & 1) || (trace & 0x100)) pdl_launch();
   if (warp >= 2) pdl_wait();         // activation producer (warp 6) and epilogue (warps 2-5)
 
   // A unit's k-block pairs are visited in a rotated order (start offset spread by row tile):
@@ -1084,10 +1086,12 @@ void launch_t(const GemmPlan& p, cudaStream_t s) {
   cfg.numAttrs = 2;
   if (p.pair)
     AB_CUDA(cudaLaunchKernelEx(&cfg, k_gemm_tc<EPI, true>, p.tw3, p.tw3_256, p.ta3_32, p.ta3_64, p.ta3, p.ta3_256, p.tx_ns, p.tx_sw, p.N, p.K, p.M_cap, p.rows_dev, p.stop_dev,
-                               p.out, p.ldo, p.bias, p.sched, g_trace_on));
+                               p.out, p.ldo, p.bias, p.sched,
+                               g_trace_on | (p.early_trigger ? 0x100 : 0)));
   else
     AB_CUDA(cudaLaunchKernelEx(&cfg, k_gemm_tc<EPI, false>, p.tw3, p.tw3_256, p.ta3_32, p.ta3_64, p.ta3, p.ta3_256, p.tx_ns, p.tx_sw, p.N, p.K, p.M_cap, p.rows_dev, p.stop_dev,
-                               p.out, p.ldo, p.bias, p.sched, g_trace_on));
+                               p.out, p.ldo, p.bias, p.sched,
+                               g_trace_on | (p.early_trigger ? 0x100 : 0)));
 }
 
 }  // namespace

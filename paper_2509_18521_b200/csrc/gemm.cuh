@@ -44,6 +44,7 @@ struct GemmPlan {
   int force = 0;
   const int* sched = nullptr;  // device table: packed schedule per live row count [0, M_cap]
   bool idle = false;           // the table is all zeros: gemm_launch skips the launch
+  bool early_trigger = false;  // launch_dependents right after setup (successor = a small kernel)
 };
 
 void gemm_plan(GemmPlan& p, const __nv_bfloat16* W, int N, int K, const __nv_bfloat16* A, int M_cap, int64_t lda,

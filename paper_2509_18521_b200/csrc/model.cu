@@ -419,6 +419,13 @@ Model* model_create(Engine& e) {
     gemm_partition(d.qkv, d.qkv2);
     gemm_partition(d.o, d.o2);
     gemm_partition(d.down, d.down2);
+    {
+      // the residual GEMMs are followed by an RMSNorm: AB_GEMM_TRIGGER=1 lets it launch and wait while
+      // they run (measured neutral at b = 64-1024, so off by default)
+      const char* gt = getenv("AB_GEMM_TRIGGER");
+      const bool et = gt ? atoi(gt) != 0 : false;
+      d.o.early_trigger = d.o2.early_trigger = d.down.early_trigger = d.down2.early_trigger = et;
+    }
     gemm_plan(d.gu2, w.wgu, 2 * m.f, m.d, M->xn, M->S, m.d, bn_dec, kEpiSwiGLU, M->hbuf, m.f, nullptr, b, stop, 8);
     gemm_set_table(d.gu2, std::vector<int>(M->S + 1, 0));  // idle unless the autotuner picks it
     gemm_plan(p.qkv, w.wqkv, m.qkv_dim, m.d, M->xn, M->M_pf, m.d, 256, kEpiBF16, M->qkv, m.qkv_dim, w.bqkv,
