@@ -9,6 +9,7 @@
 // torch-CPU oracle in oracle/cpu_model.py.
 #include <cuda_bf16.h>
 
+#include <algorithm>
 #include <cfloat>
 #include <cstdlib>
 
@@ -68,7 +69,8 @@ __device__ __forceinline__ int pop_page(Ctl* c) {
 // allocate a KV page when the row crosses a page boundary, and build the
 // attention work list (exclusive prefix of KV splits per row).
 constexpr int kPrepThreads = 1024;
-constexpr unsigned long long kItemsPerCta = 3;  // attention work items per persistent CTA (dynamic cursor)
+// attention work items per persistent CTA (dynamic cursor); AB_ATT_ITEMS overrides (tuning)
+__constant__ unsigned long long c_items_per_cta = 3;
 
 // Per-iteration decode prologue: gather the live rows, allocate KV pages for the
 // token about to be written, and build the attention work list.  The KV split
@@ -116,7 +118,8 @@ __global__ void __launch_bounds__(kPrepThreads) k_prep_decode(EngineDev e, Model
   if (threadIdx.x == 0) {
     unsigned long long tot = 0;
     for (int k = 0; k < kPrepThreads / 32; ++k) tot += s_u[k];
-    const unsigned long long per = (tot * (unsigned long long)m.hk + kItemsPerCta * att_ctas - 1) / (kItemsPerCta * att_ctas);
+    const unsigned long long ipc = c_items_per_cta;
+    const unsigned long long per = (tot * (unsigned long long)m.hk + ipc * att_ctas - 1) / (ipc * att_ctas);
     int ch = (int)min(per, (unsigned long long)(1 << 30));
     ch = (ch + 63) & ~63;
     s_chunk = max(ch, min_chunk);
@@ -679,6 +682,9 @@ void set_pdl_mask_layers(int mask) {
   AB_CUDA(cudaMemcpyToSymbol(c_pdl_mask, &mask, sizeof(int)));
   const int z = getenv("AB_ROPE_NOZERO") ? 0 : 1;  // timing experiments only: results are then wrong
   AB_CUDA(cudaMemcpyToSymbol(c_rope_zero, &z, sizeof(int)));
+  const char* ai = getenv("AB_ATT_ITEMS");
+  const unsigned long long items = ai ? (unsigned long long)std::max(1, atoi(ai)) : 3ull;
+  AB_CUDA(cudaMemcpyToSymbol(c_items_per_cta, &items, sizeof(items)));
 }
 
 void launch_init_weights(bf16* w, size_t n, uint64_t seed, uint64_t tensor_id, float std, float constant,
