@@ -128,9 +128,12 @@ def learner_glue(pb, w, out, target_token=0, comm=None):
     samples = out.batch_samples()
     mine = {}
     for s in samples:
+        # ownership first: a sample generated on another rank is a local mirror whose segments
+        # carry no payload (tokens None), and token_ids() would raise on it
+        if comm is not None and any(seg.tokens is None for seg in s.segments):
+            continue
         toks = s.token_ids()
-        if comm is None or len(toks) == s.total_tokens:  # this rank holds the payload
-            mine[s.sample_id] = sum(1 for t in toks if t % 4 == target_token) / len(toks) if toks else 0.0
+        mine[s.sample_id] = sum(1 for t in toks if t % 4 == target_token) / len(toks) if toks else 0.0
     if comm is not None:
         merged = {}
         for part in comm.allgather(mine):

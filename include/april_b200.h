@@ -222,6 +222,15 @@ int ab_engine_set_iteration(ab_engine* e, int64_t iteration_index);
 int ab_group_advantages(const double* rewards, int n_groups, int group_size, int mode, double eps, double* adv,
                         int32_t* zero_std_flags, int device);
 
+/* K7: clipped-ratio terms of a mixed-policy batch, host arrays.  Response k owns
+ * tokens [offs[k], offs[k+1]) of logp_now / logp_beh; adv[k] its advantage.  Token level: ratios and
+ * clipped get offs[n] entries (r = exp(now - beh); clipped iff A > 0 and r > 1 + eps_clip_high or
+ * A < 0 and r < 1 - eps_clip, the clip rule of src/april_sim/policy.py:153-177); sequence_level
+ * (GSPO): one ratio exp(mean_t(now - beh)) per response.  surrogate[k] = sum min(r A, clip(r) A). */
+int ab_clipped_ratio_terms(const double* logp_now, const double* logp_beh, const int64_t* offs, int n,
+                           const double* adv, double eps_clip, double eps_clip_high, int sequence_level,
+                           double* ratios, int32_t* clipped, double* surrogate, int device);
+
 /* Test entry points (device pointers; used by tests/test_kernels_gpu.py). */
 int ab_debug_gemm(const void* W, const void* A, void* out, const void* bias, int N, int K, int M, int BN, int epi);
 int ab_debug_gemm_time(const void* W, const void* A, void* out, const void* bias, int N, int K, int M, int BN, int epi,
@@ -234,6 +243,14 @@ int ab_debug_gemm_clusters(int cluster, int* out);
 int ab_debug_gemm_trace(int on, unsigned long long* out);
 int ab_debug_trace_mark(int slot);
 /* K1's per-row routine on device logits [rows, V] and draws u [rows] (tests/test_sampler.py) */
+/* K3 over a caller-built single-layer paged pool (tests/test_attention_gpu.py); device pointers:
+ * q and out [rows, n_kv_heads*gq*head_dim] bf16, kv [n_pages][2][n_kv_heads][page_size][head_dim] bf16,
+ * block_table [rows, max_pages] int32; host ctx[rows] = attended tokens per row.  chunk > 0 forces the
+ * KV split size (multiple of 64), chunk <= 0 uses the engine's per-iteration choice (min split -chunk
+ * or 256); *chunk_used receives it. */
+int ab_debug_decode_attn(const void* q, const void* kv, int64_t n_pages, int page_size, int n_kv_heads, int head_dim,
+                         int gq, const int32_t* block_table, int max_pages, const int32_t* ctx, int rows, int chunk,
+                         void* out, int* chunk_used);
 int ab_debug_sample_rows(const float* logits, int rows, int V, float temperature, int greedy, float top_p,
                          const double* u, int* tok, double* logp);
 

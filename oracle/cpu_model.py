@@ -68,10 +68,14 @@ def random_weights(spec, seed: int = 0, std: float = 0.02) -> dict:
 
 
 class CpuDecoder:
-    def __init__(self, spec, weights: dict, threads: int | None = None):
+    """round_bf16=False drops the engine's bf16 activation roundings (pure fp32 math on the bf16
+    weights): the form `tests/test_cpu_model_pin.py` checks against transformers' Qwen2 / Qwen3."""
+
+    def __init__(self, spec, weights: dict, threads: int | None = None, round_bf16: bool = True):
         if threads:
             torch.set_num_threads(threads)
         self.s = spec
+        self._bf = _bf if round_bf16 else (lambda x: x)
         w = {k: v.float() for k, v in weights.items()}
         self.embed = w["embed"]
         self.lm_head = w.get("lm_head", self.embed)
@@ -92,7 +96,7 @@ class CpuDecoder:
         self.inv_freq = inv
 
     def _rms(self, x, w):
-        return _bf(x * torch.rsqrt(x.pow(2).mean(-1, keepdim=True) + self.s.norm_eps) * w)
+        return self._bf(x * torch.rsqrt(x.pow(2).mean(-1, keepdim=True) + self.s.norm_eps) * w)
 
     def _rope(self, x, pos):  # x [T, H, hd] fp32, pos [T]
         ang = pos.float()[:, None] * self.inv_freq[None, :]
@@ -117,15 +121,15 @@ class CpuDecoder:
             qkv = xn @ L["wqkv"].t()
             if L["bqkv"] is not None:
                 qkv = qkv + L["bqkv"]
-            qkv = _bf(qkv)
+            qkv = self._bf(qkv)
             q = qkv[:, : hq * hd].view(T, hq, hd)
             k = qkv[:, hq * hd: (hq + hk) * hd].view(T, hk, hd)
             v = qkv[:, (hq + hk) * hd:].view(T, hk, hd)
             if L["q_norm"] is not None:
                 q = self._rms(q, L["q_norm"])
                 k = self._rms(k, L["k_norm"])
-            q = _bf(self._rope(q, pos))
-            k = _bf(self._rope(k, pos))
+            q = self._bf(self._rope(q, pos))
+            k = self._bf(self._rope(k, pos))
             cache[l]["k"].append(k)
             cache[l]["v"].append(v)
             K = torch.cat(cache[l]["k"], 0)
@@ -138,13 +142,15 @@ class CpuDecoder:
             mask = torch.arange(n)[None, :] > (start_pos + torch.arange(T))[:, None]
             sc = sc.masked_fill(mask[None], float("-inf"))
             p = torch.softmax(sc, dim=-1)
-            att = _bf(torch.einsum("htn,nhd->thd", p, Vx).reshape(T, hq * hd))
+            att = self._bf(torch.einsum("htn,nhd->thd", p, Vx).reshape(T, hq * hd))
             x = x + att @ L["wo"].t()
             xn = self._rms(x, L["mlp_norm"])
-            h = _bf(torch.nn.functional.silu(xn @ L["wg"].t()) * (xn @ L["wu"].t()))
+            h = self._bf(torch.nn.functional.silu(xn @ L["wg"].t()) * (xn @ L["wu"].t()))
             x = x + h @ L["wd"].t()
         if not want_logits:
             return None
+        if want_logits == "all":
+            return self._rms(x, self.final_norm) @ self.lm_head.t()
         xn = self._rms(x[-1:], self.final_norm)
         return (xn @ self.lm_head.t())[0]
 
@@ -170,29 +176,46 @@ class CpuDecoder:
                 qkv = xn @ L["wqkv"].t()
                 if L["bqkv"] is not None:
                     qkv = qkv + L["bqkv"]
-                qkv = _bf(qkv)
+                qkv = self._bf(qkv)
                 q = qkv[:, : hq * hd].view(batch, hq, hd)
                 k = qkv[:, hq * hd: (hq + hk) * hd].view(batch, hk, hd)
                 v = qkv[:, (hq + hk) * hd:].view(batch, hk, hd)
                 if L["q_norm"] is not None:
                     q = self._rms(q, L["q_norm"])
                     k = self._rms(k, L["k_norm"])
-                q = _bf(self._rope(q, pos))
+                q = self._bf(self._rope(q, pos))
                 K, V = caches[l]
-                K[:, n - 1] = _bf(self._rope(k, pos))
+                K[:, n - 1] = self._bf(self._rope(k, pos))
                 V[:, n - 1] = v
                 qg = q.view(batch, hk, hq // hk, hd)
                 sc = torch.einsum("bgqd,bngd->bgqn", qg, K[:, :n]) / math.sqrt(hd)
                 att = torch.einsum("bgqn,bngd->bgqd", torch.softmax(sc, -1), V[:, :n])
-                x = x + _bf(att.reshape(batch, hq * hd)) @ L["wo"].t()
+                x = x + self._bf(att.reshape(batch, hq * hd)) @ L["wo"].t()
                 xn = self._rms(x, L["mlp_norm"])
-                h = _bf(torch.nn.functional.silu(xn @ L["wg"].t()) * (xn @ L["wu"].t()))
+                h = self._bf(torch.nn.functional.silu(xn @ L["wg"].t()) * (xn @ L["wu"].t()))
                 x = x + h @ L["wd"].t()
             z = self._rms(x, self.final_norm) @ self.lm_head.t()
             toks = torch.argmax(z, -1)
         dt = time.perf_counter() - t0
         return {"tokens": batch * iters, "seconds": dt, "tokens_per_s": batch * iters / dt,
                 "threads": torch.get_num_threads()}
+
+    @torch.no_grad()
+    def score_all(self, prompt: list[int], generated: list[int], temperature: float = 1.0):
+        """Teacher-forced scoring of a whole generated sequence in ONE causal pass (same math as
+        forward() token by token, but matrix-matrix; used for the full-depth greedy tests).
+        Returns numpy arrays per generated position: oracle argmax, margin z[argmax] - z[token],
+        log_softmax(z / T)[token], top-2 margin."""
+        seq = list(prompt) + list(generated[:-1])
+        z = self.forward(seq, self.new_cache(), 0, want_logits="all")[len(prompt) - 1:]
+        tok = torch.tensor(list(generated), dtype=torch.long)
+        am = torch.argmax(z, -1)
+        zt = z.gather(1, tok[:, None])[:, 0]
+        margin = z.gather(1, am[:, None])[:, 0] - zt
+        lp = torch.log_softmax(z.double() / temperature, dim=-1).gather(1, tok[:, None])[:, 0]
+        top2 = torch.topk(z, 2, dim=-1).values
+        return dict(argmax=am.numpy(), margin=margin.numpy(), logp=lp.numpy(),
+                    top2=(top2[:, 0] - top2[:, 1]).numpy())
 
     @torch.no_grad()
     def score(self, prompt: list[int], generated: list[int], temperature: float = 1.0):

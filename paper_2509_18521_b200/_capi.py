@@ -90,6 +90,7 @@ class KernelStat(C.Structure):
 P = C.c_void_p
 I32P = C.POINTER(C.c_int32)
 F64P = C.POINTER(C.c_double)
+I64P = C.POINTER(C.c_int64)
 
 # name -> argtypes; restype is always int (status)
 _SIGS = {
@@ -120,6 +121,8 @@ _SIGS = {
     "ab_engine_synchronize": [P],
     "ab_engine_set_iteration": [P, C.c_int64],
     "ab_group_advantages": [F64P, C.c_int, C.c_int, C.c_int, C.c_double, F64P, I32P, C.c_int],
+    "ab_clipped_ratio_terms": [F64P, F64P, I64P, C.c_int, F64P, C.c_double, C.c_double, C.c_int, F64P, I32P,
+                               F64P, C.c_int],
     "ab_debug_gemm": [P, P, P, P, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int],
     "ab_debug_gemm_time": [P, P, P, P, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int,
                            C.POINTER(C.c_float)],
@@ -127,6 +130,8 @@ _SIGS = {
     "ab_debug_gemm_clusters": [C.c_int, C.POINTER(C.c_int)],
     "ab_debug_gemm_trace": [C.c_int, P],
     "ab_debug_trace_mark": [C.c_int],
+    "ab_debug_decode_attn": [P, P, C.c_int64, C.c_int, C.c_int, C.c_int, C.c_int, P, C.c_int, I32P, C.c_int,
+                             C.c_int, P, C.POINTER(C.c_int)],
     "ab_debug_sample_rows": [P, C.c_int, C.c_int, C.c_float, C.c_int, C.c_float, P, P, P],
 }
 EXPORTS = sorted(_SIGS) + ["ab_last_error", "ab_version"]

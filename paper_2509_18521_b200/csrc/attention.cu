@@ -18,7 +18,9 @@
 #include <cuda.h>
 #include <cuda_bf16.h>
 
+#include <algorithm>
 #include <cfloat>
+#include <vector>
 
 #include "model.cuh"
 
@@ -652,4 +654,117 @@ void launch_decode_attention(const CUtensorMap& map, const EngineDev& e, const M
     launch_t<64>(map, e, m, layer, q, out, part_o, part_ml, max_splits, s);
 }
 
+// The KV split size k_prep_decode picks for an iteration (host restatement for the test entry):
+// about `items_per_cta` work items per persistent attention CTA, 64-token multiples, >= min_chunk.
+static int default_chunk(const ModelDev& m, const int32_t* ctx, int rows, int min_chunk) {
+  unsigned long long tot = 0;
+  for (int i = 0; i < rows; ++i) tot += (unsigned long long)ctx[i];
+  const unsigned long long ipc = 3, ctas = (unsigned long long)decode_attention_ctas(m);
+  unsigned long long per = (tot * (unsigned long long)m.hk + ipc * ctas - 1) / (ipc * ctas);
+  int ch = (int)std::min<unsigned long long>(per, 1ull << 30);
+  ch = (ch + 63) & ~63;
+  return std::max(ch, min_chunk);
+}
+
 }  // namespace ab
+
+// Test entry (tests/test_attention_gpu.py): one launch of K3 over a caller-built single-layer paged
+// pool.  Device pointers: q [rows, n_kv_heads * gq * head_dim] bf16; kv [n_pages][2][n_kv_heads]
+// [page_size][head_dim] bf16 (the engine's per-layer page layout); block_table [rows, max_pages]
+// int32 page ids; out [rows, n_kv_heads * gq * head_dim] bf16.  Host: ctx[rows] attended tokens per
+// row (the row's own new token included).  chunk > 0 forces the KV split size (multiple of 64;
+// ceil(ctx / chunk) <= 64 splits per row), chunk <= 0 uses the engine's per-iteration choice with
+// min split -chunk (0: the engine's minimum).  *chunk_used receives the split size.
+extern "C" int ab_debug_decode_attn(const void* q, const void* kv, int64_t n_pages, int page_size, int n_kv_heads,
+                                    int head_dim, int gq, const int32_t* block_table, int max_pages,
+                                    const int32_t* ctx, int rows, int chunk, void* out, int* chunk_used) {
+  using namespace ab;
+  try {
+    AB_REQUIRE(rows >= 1 && rows <= 4096, AB_ERR_CONTRACT, "rows must lie in [1, 4096]");
+    AB_REQUIRE(head_dim == 64 || head_dim == 128, AB_ERR_CONTRACT, "head_dim must be 64 or 128");
+    AB_REQUIRE(gq >= 1 && gq <= kMergeRows, AB_ERR_CONTRACT, "GQA group must lie in [1, 8]");
+    ModelDev m{};
+    m.L = 1;
+    m.hk = n_kv_heads;
+    m.gq = gq;
+    m.hq = gq * n_kv_heads;
+    m.hd = head_dim;
+    m.qd = m.hq * m.hd;
+    m.kvd = m.hk * m.hd;
+    m.P = page_size;
+    m.MP = max_pages;
+    m.NP = n_pages;
+    m.kv = (bf16*)kv;
+    int max_ctx = 1;
+    for (int i = 0; i < rows; ++i) {
+      AB_REQUIRE(ctx[i] >= 1 && ctx[i] <= max_pages * page_size, AB_ERR_CONTRACT, "context exceeds the block table");
+      max_ctx = std::max(max_ctx, ctx[i]);
+    }
+    // the engine's minimum split: >= 256 tokens and <= 64 splits for the longest row (model_create)
+    const int min_chunk = std::max(256, (ceil_div(max_ctx, kMaxSplits) + 63) / 64 * 64);
+    const int ch = chunk > 0 ? chunk : default_chunk(m, ctx, rows, chunk < 0 ? -chunk : min_chunk);
+    AB_REQUIRE(ch % 64 == 0, AB_ERR_CONTRACT, "chunk must be a multiple of 64");
+    const int max_splits = ceil_div(max_ctx, ch);
+    AB_REQUIRE(max_splits <= kMaxSplits, AB_ERR_CONTRACT, "more than 64 KV splits per row");
+    if (chunk_used) *chunk_used = ch;
+    // the work list k_prep_decode builds: (row, split) per row, exclusive prefix of split counts
+    std::vector<int32_t> pos(rows), btrow(rows), prefix(rows + 1, 0), items;
+    for (int i = 0; i < rows; ++i) {
+      pos[i] = ctx[i] - 1;
+      btrow[i] = i;
+      const int ns = ceil_div(ctx[i], ch);
+      prefix[i + 1] = prefix[i] + ns;
+      for (int s2 = 0; s2 < ns; ++s2) items.push_back(i | (s2 << 16));
+    }
+    const int att_ctl[2] = {ch, 0};
+    Ctl ctl{};
+    ctl.b = rows;
+    int32_t *d_pos, *d_btrow, *d_prefix, *d_items, *d_counter, *d_attctl;
+    float *part_o, *part_ml;
+    Ctl* d_ctl;
+    AB_CUDA(cudaMalloc(&d_pos, sizeof(int32_t) * rows));
+    AB_CUDA(cudaMalloc(&d_btrow, sizeof(int32_t) * rows));
+    AB_CUDA(cudaMalloc(&d_prefix, sizeof(int32_t) * (rows + 1)));
+    AB_CUDA(cudaMalloc(&d_items, sizeof(int32_t) * items.size()));
+    AB_CUDA(cudaMalloc(&d_counter, sizeof(int32_t) * rows * m.hk));
+    AB_CUDA(cudaMalloc(&d_attctl, sizeof(att_ctl)));
+    AB_CUDA(cudaMalloc(&d_ctl, sizeof(Ctl)));
+    AB_CUDA(cudaMalloc(&part_o, sizeof(float) * (size_t)rows * m.hq * max_splits * m.hd));
+    AB_CUDA(cudaMalloc(&part_ml, sizeof(float) * (size_t)rows * m.hq * max_splits * 2));
+    AB_CUDA(cudaMemcpy(d_pos, pos.data(), sizeof(int32_t) * rows, cudaMemcpyHostToDevice));
+    AB_CUDA(cudaMemcpy(d_btrow, btrow.data(), sizeof(int32_t) * rows, cudaMemcpyHostToDevice));
+    AB_CUDA(cudaMemcpy(d_prefix, prefix.data(), sizeof(int32_t) * (rows + 1), cudaMemcpyHostToDevice));
+    AB_CUDA(cudaMemcpy(d_items, items.data(), sizeof(int32_t) * items.size(), cudaMemcpyHostToDevice));
+    AB_CUDA(cudaMemset(d_counter, 0, sizeof(int32_t) * rows * m.hk));
+    AB_CUDA(cudaMemcpy(d_attctl, att_ctl, sizeof(att_ctl), cudaMemcpyHostToDevice));
+    AB_CUDA(cudaMemcpy(d_ctl, &ctl, sizeof(Ctl), cudaMemcpyHostToDevice));
+    m.row_pos = d_pos;
+    m.row_btrow = d_btrow;
+    m.split_prefix = d_prefix;
+    m.att_items = d_items;
+    m.att_counter = d_counter;
+    m.att_ctl = d_attctl;
+    m.bt = const_cast<int32_t*>(block_table);
+    EngineDev e{};
+    e.ctl = d_ctl;
+    CUtensorMap map;
+    make_kv_tmap(&map, m);
+    launch_decode_attention(map, e, m, 0, (const bf16*)q, (bf16*)out, part_o, part_ml, max_splits, ch, 0);
+    AB_CUDA(cudaGetLastError());
+    AB_CUDA(cudaDeviceSynchronize());
+    // the split-combine arrival counters must have reset themselves
+    std::vector<int32_t> cnt(rows * m.hk);
+    AB_CUDA(cudaMemcpy(cnt.data(), d_counter, sizeof(int32_t) * cnt.size(), cudaMemcpyDeviceToHost));
+    for (void* p : {(void*)d_pos, (void*)d_btrow, (void*)d_prefix, (void*)d_items, (void*)d_counter, (void*)d_attctl,
+                    (void*)d_ctl, (void*)part_o, (void*)part_ml})
+      cudaFree(p);
+    for (int v : cnt) AB_REQUIRE(v == 0, AB_ERR_CUDA, "split-combine arrival counter did not reset");
+    return AB_OK;
+  } catch (const Error& err) {
+    set_last_error(err.what());
+    return err.code;
+  } catch (const std::exception& err) {
+    set_last_error(err.what());
+    return AB_ERR_CUDA;
+  }
+}

@@ -59,10 +59,24 @@ __global__ void k_rope_table(float2* rope, int max_pos, int hd, float theta) {
 // per-iteration row preparation + KV page allocation
 // ---------------------------------------------------------------------------
 
+// Pop one page index off the free-page stack; on an empty stack fail WITHOUT side effects (the
+// top never goes negative, so later releases push to valid slots and no page is lost).
 __device__ __forceinline__ int pop_page(Ctl* c) {
-  const long long old = (long long)atomicAdd(reinterpret_cast<unsigned long long*>(&c->kv_free_top),
-                                             (unsigned long long)(-1ll));
-  return old - 1 >= 0 ? (int)(old - 1) : -1;
+  unsigned long long* top = reinterpret_cast<unsigned long long*>(&c->kv_free_top);
+  long long cur = *reinterpret_cast<volatile long long*>(top);
+  while (cur > 0) {
+    const long long prev = (long long)atomicCAS(top, (unsigned long long)cur, (unsigned long long)(cur - 1));
+    if (prev == cur) return (int)(cur - 1);
+    cur = prev;
+  }
+  return -1;
+}
+
+// Push one page back (error paths: undo a pop whose allocation is abandoned).
+__device__ __forceinline__ void push_page(Ctl* c, ModelDev& m, int page) {
+  const long long base =
+      (long long)atomicAdd(reinterpret_cast<unsigned long long*>(&c->kv_free_top), 1ull);
+  m.free_pages[base] = page;
 }
 
 // Single block: per live row, gather (token, position, block-table row),
@@ -85,6 +99,7 @@ __global__ void __launch_bounds__(kPrepThreads) k_prep_decode(EngineDev e, Model
   const int beg = min(b, (int)threadIdx.x * ipt), end = min(b, beg + ipt);
   unsigned long long ctx_sum = 0;
   bool fail = false;
+  int popped[4], n_popped = 0;  // ipt <= 4 (S <= 4096)
   for (int i = beg; i < end; ++i) {
     const int h = e.slot_handle[i];
     const int pos = m.h_ctx[h];
@@ -94,12 +109,13 @@ __global__ void __launch_bounds__(kPrepThreads) k_prep_decode(EngineDev e, Model
     ctx_sum += (unsigned long long)(pos + 1);
     int page = 0;
     if (pos % m.P == 0) {
-      const int idx = pop_page(c);
-      if (idx < 0 || pos / m.P >= m.MP) {
+      const int idx = pos / m.P < m.MP ? pop_page(c) : -1;
+      if (idx < 0) {
         fail = true;
       } else {
         page = m.free_pages[idx];
         m.bt[(size_t)h * m.MP + pos / m.P] = page;
+        popped[n_popped++] = page;
       }
     } else {
       page = m.bt[(size_t)h * m.MP + pos / m.P];
@@ -159,10 +175,15 @@ __global__ void __launch_bounds__(kPrepThreads) k_prep_decode(EngineDev e, Model
   if (threadIdx.x == kPrepThreads - 1) m.split_prefix[b] = s_w[31];
   if (c->run_iters < e.it_cap && ctx_sum)
     atomicAdd(reinterpret_cast<unsigned long long*>(&e.it_ctx[c->run_iters]), ctx_sum);
-  if (fail) {
-    atomicCAS(&c->error, kErrNone, kErrOutOfKV);
-    c->stop = 1;
-    c->stop_reason = -2;
+  // out of pages: the iteration is abandoned (every later kernel sees stop), so the pages this
+  // prep did pop go back to the stack (h_ctx did not advance; a retry pops them again)
+  if (__syncthreads_or(fail)) {
+    for (int k = 0; k < n_popped; ++k) push_page(c, m, popped[k]);
+    if (threadIdx.x == 0) {
+      atomicCAS(&c->error, kErrNone, kErrOutOfKV);
+      c->stop = 1;
+      c->stop_reason = -2;
+    }
   }
 }
 
@@ -515,8 +536,8 @@ __global__ void k_resume_fork(EngineDev e, ModelDev m, const int4* items, int n,
   for (int j = 0; j < nfull; ++j) hb[j] = gb[j];
   m.h_shared[h] = nfull;
   for (int j = nfull; j < need; ++j) {
-    const int idx = pop_page(c);
-    if (idx < 0 || j >= m.MP) {
+    const int idx = j < m.MP ? pop_page(c) : -1;
+    if (idx < 0) {
       atomicCAS(&c->error, kErrNone, kErrOutOfKV);
       m.h_ctx[h] = j * m.P;  // what is allocated, so a release frees exactly it
       return;
@@ -558,8 +579,8 @@ __global__ void k_score_alloc(EngineDev e, ModelDev m, const int2* items, int n)
   int32_t* row = m.bt + (size_t)it.x * m.MP;
   const int need = (it.y + m.P - 1) / m.P;
   for (int j = 0; j < need; ++j) {
-    const int idx = pop_page(c);
-    if (idx < 0 || j >= m.MP) {
+    const int idx = j < m.MP ? pop_page(c) : -1;
+    if (idx < 0) {
       atomicCAS(&c->error, kErrNone, kErrOutOfKV);
       for (int q = j; q < need; ++q) row[q] = -1;
       return;

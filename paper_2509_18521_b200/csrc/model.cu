@@ -606,6 +606,18 @@ static void flush_prefill(Engine& e) {
       AB_CUDA(cudaMemcpyAsync(M->ga_last, glast, sizeof(int32_t) * na, cudaMemcpyHostToDevice, s));
       launch_group_alloc(e.d, m, M->ga_g, M->ga_len, M->ga_last, na, s);
       e.launches += 1;
+      AB_CUDA(cudaMemcpyAsync(&e.ctl_host->error, &e.d.ctl->error, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+      AB_CUDA(cudaStreamSynchronize(s));
+      if (e.ctl_host->error == kErrOutOfKV) {
+        // the pool cannot hold this chunk's prompts: return what the chunk's groups got, drop them
+        // and every later pending group (not prefilled), clear the error, and report it
+        for (int j = 0; j < na; ++j) launch_group_release(e.d, m, gg[j], s);
+        AB_CUDA(cudaMemsetAsync(&e.d.ctl->error, 0, sizeof(int32_t), s));
+        AB_CUDA(cudaStreamSynchronize(s));
+        for (size_t j = k; j < M->pending.size(); ++j) M->prompts.erase(M->pending[j].g);
+        M->pending.erase(M->pending.begin() + k, M->pending.end());
+        throw Error(AB_ERR_OUT_OF_KV, "KV page pool exhausted (prompt prefill)");
+      }
     }
     prefill_rows(e, R, nb);
     e.prefill_tokens += R;

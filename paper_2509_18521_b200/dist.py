@@ -27,7 +27,7 @@ from __future__ import annotations
 from collections import deque
 
 from .errors import ContractViolation
-from .rollouts import ACTIVE, COMPLETED, PAUSED, PENDING
+from .rollouts import ACTIVE, PAUSED, PENDING
 
 _REASONS = ("stop_token", "target_length", "max_length")
 _CODE = {r: i for i, r in enumerate(_REASONS)}
@@ -311,4 +311,3 @@ class GpuLocal:
         return id(s) in self._queued_ids
 
 
-_ = COMPLETED

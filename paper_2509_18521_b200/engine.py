@@ -197,7 +197,7 @@ class Engine:
 
     @property
     def queued_count(self) -> int:
-        return len(self._queue) + 0
+        return len(self._queue)
 
     @property
     def idle(self) -> bool:
@@ -551,13 +551,23 @@ class Engine:
 
     def load_weights(self, tensors: dict) -> None:
         """Install new policy weights (the weight-version swap between RL steps).
-        `tensors` maps export_weights() names to bf16 tensors of the same shape (host or device).
-        Call between steps; with kv_resume="reprefill" the next begin_step(version) recomputes the
-        resident prompt KV and resumed partials are re-prefilled under the new weights."""
+        `tensors` maps export_weights() names to bf16 tensors of exactly the exported shape (host or
+        device).  Layout: "layers.{l}.wqkv" stacks the q, k, v projection rows; "layers.{l}.wgu" is
+        tile-interleaved -- per 128-row tile, 64 gate rows then the matching 64 up rows (an HF-style
+        [gate; up] concatenation must be re-tiled first, see oracle/cpu_model.py:split_gate_up for
+        the inverse).  Call between steps.  Only with kv_resume="reprefill": the next
+        begin_step(version) recomputes the resident prompt KV and resumed partials are re-prefilled
+        under the new weights.  With kv_resume="retain" resident KV would silently mix old-policy
+        keys/values with the new weights, so a swap while any prompt group (or parked partial) is
+        resident is refused."""
         import torch
 
         if not self.idle:
             raise ContractViolation("load_weights requires an idle engine")
+        if self.kv_resume == "retain" and (self._gslot or self._handle):
+            raise ContractViolation("load_weights with kv_resume='retain' while KV is resident (prompt groups or "
+                                    "parked partials computed under the old weights); use kv_resume='reprefill' "
+                                    "or discard them first")
         n = C.c_int()
         capi.call("ab_engine_weight_count", self._h, C.byref(n))
         name = C.create_string_buffer(128)
@@ -571,7 +581,7 @@ class Engine:
                 raise ConfigError(f"unknown weight {k!r}")
             i, r, c = index[k]
             t = t.detach().to(torch.bfloat16).contiguous()
-            if tuple(t.shape) != (r, c) and t.numel() != r * c:
+            if tuple(t.shape) != (r, c):
                 raise ConfigError(f"weight {k!r}: expected {r}x{c}, got {tuple(t.shape)}")
             capi.call("ab_engine_set_weight", self._h, i, C.c_void_p(t.data_ptr()), r * c * 2)
             if not t.is_cuda:

@@ -13,7 +13,7 @@ from dataclasses import dataclass, replace
 import numpy as np
 
 from .errors import ConfigError
-from .rng import LANE_PROMPT, key_words, philox_key
+from .rng import LANE_PROMPT, philox_key
 
 
 @dataclass(frozen=True)
@@ -99,5 +99,4 @@ def synthetic_prompt(seed: int, instance_id: int, length: int, vocab: int) -> np
     k = philox_key(seed, LANE_PROMPT, instance_id, 0)
     gen = np.random.Generator(np.random.Philox(key=k))
     u = gen.random(length)
-    _ = key_words
     return np.minimum(np.floor(u * (vocab - 1)), vocab - 2).astype(np.int32)

@@ -249,7 +249,7 @@ def test_exactly_once_delivery_over_long_run():  # :178-192
 
 def test_group_advantages_kernel_matches_numpy():
     rng = np.random.default_rng(1)
-    for g in (1, 2, 7, 8, 16, 33):
+    for g in (1, 2, 7, 8, 16, 33, 64, 65, 129, 200, 1500):  # > 128: numpy's recursive pairwise blocks
         r = rng.random(g * 11)
         for mode in ("mean_baseline", "mean_std_baseline"):
             a = pb.batch_advantages(r, g, mode, 1e-6)
@@ -264,3 +264,76 @@ def test_group_advantages_kernel_matches_numpy():
     # GSPO normalises like GRPO (its sequence ratio comes from Engine.sequence_logprobs)
     r = rng.random(8 * 5)
     assert np.array_equal(pb.batch_advantages(r, 8, "gspo"), pb.batch_advantages(r, 8, "mean_std_baseline"))
+
+
+def test_clipped_ratio_kernel_matches_oracle():
+    """K7 (trainer-side consumption) against the CPU restatement of the reference's clip
+    rule (oracle/trainer_ref.py; src/april_sim/policy.py:153-177): ratios and clip masks exact up to
+    exp's last ulp, surrogate sums within 1e-12 relative (warp-tree vs numpy summation order)."""
+    from oracle import trainer_ref
+
+    rng = np.random.default_rng(3)
+    lens = [0, 1, 5, 31, 32, 33, 700, 4096]
+    beh = [np.log(rng.uniform(1e-4, 1.0, n)) for n in lens]
+    now = [b + rng.normal(0.0, 0.3, b.size) for b in beh]
+    adv = rng.normal(0.0, 1.0, len(lens))
+    adv[2] = 0.0
+    for seq in (False, True):
+        r, m, tot = pb.clipped_ratio_terms(now, beh, adv, 0.2, 0.28, sequence_level=seq)
+        rr, mr, sr = trainer_ref.clipped_ratio_terms(now, beh, adv, 0.2, 0.28, sequence_level=seq)
+        for a, b, ma, mb in zip(r, rr, m, mr):
+            np.testing.assert_allclose(a, b, rtol=4e-16, atol=0)
+            assert np.array_equal(ma, mb)
+        assert abs(tot - sum(sr)) <= 1e-12 * max(1.0, sum(abs(x) for x in sr))
+    # identical policies: every ratio is 1 and nothing is clipped
+    r, m, _ = pb.clipped_ratio_terms(beh, beh, adv)
+    assert all(np.all(x == 1.0) for x in r) and not any(np.any(x) for x in m)
+    with pytest.raises(pb.ContractViolation):
+        pb.clipped_ratio_terms(now[:2], beh[:2][::-1], adv[:2])
+
+
+def test_out_of_kv_fails_without_leaking_pages():
+    """a failed page pop must leave the free-page stack intact.  A prompt group that does
+    not fit raises OutOfKV; releasing what it got restores the pool exactly, and decoding that
+    exhausts the pool mid-iteration stops with OutOfKV, the top never negative."""
+    from paper_2509_18521_b200 import _capi
+
+    spec = pb.PRESETS["tiny"]
+    prompts = {i: pb.synthetic_prompt(2, i, 100, spec.vocab) for i in range(8)}
+    eng = pb.LengthDrivenEngine(pb.EngineConfig(max_slots=8, l_max=512), model=spec, prompt_len=100,
+                                page_size=16, kv_pages=10, max_handles=32, max_groups=8,
+                                prompt_source=lambda iid: prompts[iid])
+    total = eng.stats().kv_pages_free
+    assert total == 10
+    eng.begin_step(0)
+    a = _sample(0, 0, 40)
+    eng.submit(a)  # group 0: 99 prompt positions -> 7 pages, the sample's tail page copy -> 1 page
+    eng._flush()
+    assert eng.stats().kv_pages_free == 10 - 8
+    b = _sample(1, 0, 40)
+    with pytest.raises(_capi.OutOfKV):  # group 1 needs 7 more pages, 2 are left
+        eng.submit(b)
+        eng._flush()
+    # the failed prefill returned its partial allocation: the 2 free pages are free again
+    assert eng.stats().kv_pages_free == 2
+    eng._queue.remove(b)
+    eng._release([b])
+    assert eng.stats().kv_pages_free == 2
+    while not eng.idle:  # the first sample still fits: 40 tokens from position 99 need 2 new pages
+        eng.decode_until_event()
+    assert a.total_tokens == 40
+    assert eng.stats().kv_pages_free == total  # everything went back
+    eng.close()
+    # decode exhaustion: two samples growing past the pool
+    eng = pb.LengthDrivenEngine(pb.EngineConfig(max_slots=8, l_max=512), model=spec, prompt_len=100,
+                                page_size=16, kv_pages=12, max_handles=32, max_groups=8,
+                                prompt_source=lambda iid: prompts[iid])
+    eng.begin_step(0)
+    for j in range(2):
+        eng.submit(_sample(0, j, 400))
+    with pytest.raises(_capi.OutOfKV):
+        while not eng.idle:
+            eng.decode_until_event()
+    free = eng.stats().kv_pages_free
+    assert 0 <= free < 2, free
+    eng.close()

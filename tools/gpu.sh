@@ -1,0 +1,51 @@
+#!/bin/bash
+# One documented entry point for the GPU-box runs (invoked through gpurun from the repo root):
+#   gpurun --timeout T -- 'bash tools/gpu.sh MODE [args]'
+# Outputs land in gpurun_out/ (scratch; summaries worth keeping are copied into profiles/).
+#   tests [pytest -k expr]   pytest -m gpu (optionally filtered), full log + per-test report dir
+#   smoke                    __graft_entry__ build + smoke
+#   bench [bench.py args]    one bench line
+#   launches B CTX [preset]  ncu launch list (gpu__time_duration) of decode iterations at (batch, ctx)
+#   ncu_attn B CTX           ncu --set full of the decode attention kernel
+#   sanitize                 compute-sanitizer racecheck + memcheck on the engine / attention tests
+set -u
+mkdir -p gpurun_out
+export AB_TEST_REPORT_DIR=gpurun_out/test_reports
+MODE=${1:-tests}
+shift || true
+nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,power.draw --format=csv > gpurun_out/smi.txt 2>&1
+case "$MODE" in
+  tests)
+    if [ $# -gt 0 ]; then K=(-k "$*"); else K=(); fi
+    timeout 3000 python -m pytest tests -m gpu -q -x -p no:cacheprovider -rs "${K[@]}" > gpurun_out/pytest_gpu.log 2>&1
+    echo "pytest rc=$?" >> gpurun_out/pytest_gpu.log
+    tail -5 gpurun_out/pytest_gpu.log ;;
+  smoke)
+    timeout 900 python -c "import __graft_entry__ as g; g.build(); g.smoke()" > gpurun_out/smoke.log 2>&1
+    echo "smoke rc=$?" >> gpurun_out/smoke.log; tail -3 gpurun_out/smoke.log ;;
+  bench)
+    timeout 3000 python bench.py "$@" > gpurun_out/bench.log 2> gpurun_out/bench.err
+    echo "bench rc=$?" >> gpurun_out/bench.err; tail -c 3000 gpurun_out/bench.log ;;
+  launches)
+    B=${1:-1024}; CTX=${2:-1400}; PRESET=${3:-qwen2.5-1.5b}
+    timeout 900 ncu --profile-from-start off --metrics gpu__time_duration.sum --clock-control none --csv \
+      --log-file gpurun_out/launches_${PRESET}_b${B}_c${CTX}.csv \
+      python tools/decode_microbench.py --model $PRESET --batch $B --ctx $CTX --iters 2 --ncu \
+      > gpurun_out/launches_${PRESET}_b${B}.log 2>&1
+    python tools/launch_summary.py gpurun_out/launches_${PRESET}_b${B}_c${CTX}.csv | tail -30 ;;
+  ncu_attn)
+    bash tools/gpu_ncu_attn.sh "$@" ;;
+  sanitize)
+    for tool in racecheck memcheck; do
+      timeout 1800 compute-sanitizer --tool $tool --error-exitcode 9 python -m pytest -q -x -p no:cacheprovider \
+        -m gpu tests/test_attention_gpu.py -k "b64 and c3 and page64 or mixed7 and c5" \
+        > gpurun_out/sanitize_${tool}_attention.log 2>&1
+      echo "rc=$?" >> gpurun_out/sanitize_${tool}_attention.log
+      timeout 1800 compute-sanitizer --tool $tool --error-exitcode 9 python -m pytest -q -x -p no:cacheprovider \
+        -m gpu tests/test_engine_gpu.py tests/test_replay_model_gpu.py -k "c1_tiny and april and reprefill or exactly_once or advantages" \
+        > gpurun_out/sanitize_${tool}_engine.log 2>&1
+      echo "rc=$?" >> gpurun_out/sanitize_${tool}_engine.log
+    done
+    tail -3 gpurun_out/sanitize_*.log ;;
+  *) echo "unknown mode $MODE"; exit 2 ;;
+esac
