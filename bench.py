@@ -177,50 +177,110 @@ def cpu_baseline(w, budget_s=15.0):
                       f"at context {ctx} ({r['seconds']:.1f} s)"}
 
 
+def _cpu_model_name():
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def _import_reference():
+    """The unmodified reference, installed into baseline/_ref."""
+    ref = os.path.join(ROOT, "baseline", "_ref")
+    if not os.path.isdir(os.path.join(ref, "april_sim")):
+        return None
+    sys.path.insert(0, ref)
+    import april_sim
+
+    return april_sim
+
+
+def reference_timings(w, a, budget_s=6.0):
+    """The reference's own CPU path on one core: (1) april_sim replaying the workload's length trace
+    through its Scheduler + LengthDrivenEngine (scheduling, abort, recycle; the decode is its d0+d1*b
+    cost model), wall seconds per APRIL step; (2) its PolicyDrivenEngine per-token path (Philox draw,
+    softmax, inverse CDF, STOP) on the toy policy, tokens per wall second."""
+    ecfg = a.EngineConfig(d0=0.05, d1=0.002, max_slots=w["slots"], l_max=w["l_max"])
+    eng = a.LengthDrivenEngine(ecfg)
+    scfg = a.SchedulerConfig(rollout_batch_size=w["n"], samples_per_prompt=w["g"],
+                             over_sampling_batch_size=w["n_prime"], mode="april")
+    sampler = a.LengthSampler(a.LengthDistribution.lognormal(w["mu"], w["sigma"], w["l_max"]), w["rho"], 0)
+    sched = a.Scheduler(scfg, eng, a.InstanceSource(group_size=w["g"]), sampler)
+    t0, k, toks = time.perf_counter(), 0, 0
+    while time.perf_counter() - t0 < budget_s and k < 50:
+        toks += sched.run_step(k).tokens_generated
+        k += 1
+    replay = {"steps": k, "seconds_per_step": (time.perf_counter() - t0) / k,
+              "simulated_tokens_per_wall_s": toks / (time.perf_counter() - t0), "cores": 1}
+    sim = a.build_simulation(a.toy_policy_config().with_overrides(**{"run.steps": 10_000}))
+    t0, toks, k = time.perf_counter(), 0, 0
+    while time.perf_counter() - t0 < budget_s:
+        toks += sim.run_step().tokens_generated
+        k += 1
+    policy = {"steps": k, "tokens_per_s": toks / (time.perf_counter() - t0), "cores": 1,
+              "note": "toy context-free policy (4 symbols + STOP), reference PolicyDrivenEngine + reinforce_update"}
+    return {"april_sim_replay": replay, "april_sim_policy_engine": policy}
+
+
 def reference_arm(args):
-    """--impl reference: the reference algorithm's CPU implementation (oracle port:
-    the scheduler/engine restatement oracle/sim_ref.py plus the fp32 decoder oracle/cpu_model.py)
-    on the host cores; each step is a bounded sample of the C2 rollout."""
+    """--impl reference: the reference's CPU path for this workload on the box's host cores.  The
+    scheduling half of every step is the unmodified reference (april_sim from baseline/_ref: its
+    Scheduler + LengthDrivenEngine replaying the same length trace, one core); the reference has no
+    decoder, so the decode half is a bounded sample of the same model's decode iterations on the CPU
+    (oracle/cpu_model.py, fp32, all host threads).  value = decoded tokens / wall time of the two."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return 0
     import torch
 
     import paper_2509_18521_b200 as pb
-    from oracle import sim_ref
     from oracle.cpu_model import CpuDecoder, random_weights
 
+    a = _import_reference()
     w = WORKLOADS[args.workload]
     spec = pb.PRESETS[w["model"]]
     dec = CpuDecoder(spec, random_weights(spec, 0))
     batch, ctx = 64, 1024
     probe = dec.decode_batch_rate(batch, ctx, 1)
     iters = max(1, min(32, int(args.ref_step_s / max(probe["seconds"], 1e-3))))
-    # the scheduling half of the reference path, same trace (APRIL step of the CPU simulator)
-    eng = sim_ref.OracleEngine(0.05, 0.002, w["slots"], w["l_max"])
-    sch = sim_ref.OracleScheduler(w["n"], w["g"], w["n_prime"], eng,
-                                  dist=sim_ref.TraceDist("lognormal", w["l_max"], w["mu"], w["sigma"]), rho=w["rho"])
+    sched = None
+    if a is not None:
+        ecfg = a.EngineConfig(d0=0.05, d1=0.002, max_slots=w["slots"], l_max=w["l_max"])
+        scfg = a.SchedulerConfig(rollout_batch_size=w["n"], samples_per_prompt=w["g"],
+                                 over_sampling_batch_size=w["n_prime"], mode="april")
+        sampler = a.LengthSampler(a.LengthDistribution.lognormal(w["mu"], w["sigma"], w["l_max"]), w["rho"], 0)
+        sched = a.Scheduler(scfg, a.LengthDrivenEngine(ecfg), a.InstanceSource(group_size=w["g"]), sampler)
     rates, times = [], []
     for k in range(args.warmup + args.steps):
         t0 = time.perf_counter()
-        sch.run_step(k)
+        if sched is not None:
+            sched.run_step(k)
         r = dec.decode_batch_rate(batch, ctx + 8 * k, iters, seed=k)
         dt = time.perf_counter() - t0
         if k >= args.warmup:
             rates.append(r["tokens"] / dt)
             times.append(dt)
     v = statistics.mean(rates)
+    sched_src = "april_sim (baseline/_ref, unmodified reference)" if a is not None else "reference not installed"
     line = {"impl": "reference", "metric": METRIC, "value": v, "unit": "tokens/s", "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * statistics.mean(times),
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
             "config": {"workload": args.workload, "shape": spec.name, "prompts": w["n"],
                        "samples_per_prompt": w["g"], "over_provision": w["n_prime"] / w["n"],
                        "max_len": w["l_max"]},
-            "cpu_baseline": {"value": v, "unit": "tokens/s", "cores": torch.get_num_threads(), "kind": "port",
-                             "sample": f"per step: one APRIL scheduling step of oracle/sim_ref.py + {iters} fp32 "
-                                       f"decode iterations x batch {batch} of the full-depth {spec.name} decoder "
-                                       f"(oracle/cpu_model.py) at context ~{ctx}"},
+            "cpu_baseline": {"value": v, "unit": "tokens/s", "cores": torch.get_num_threads(),
+                             "kind": "reference" if a is not None else "port", "cpu": _cpu_model_name(),
+                             "sample": f"per step: one APRIL scheduling step of {sched_src} replaying the "
+                                       f"{args.workload} trace + {iters} fp32 decode iterations x batch {batch} of "
+                                       f"the full-depth {spec.name} decoder (oracle/cpu_model.py; the reference "
+                                       f"has no decoder) at context ~{ctx}"},
             "e2e": {"value": v, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    if a is not None:
+        line["reference_cpu_path"] = reference_timings(w, a)
     print(json.dumps(line))
     return 0
 
@@ -232,7 +292,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--workload", default="C2", choices=sorted(WORKLOADS))
-    ap.add_argument("--sync-steps", type=int, default=2)
+    ap.add_argument("--sync-steps", type=int, default=5)
     ap.add_argument("--no-sync", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--profile-every", type=int, default=8)
@@ -281,7 +341,7 @@ def main():
         comm = TorchComm(device=f"cuda:{local}")
         front = DataParallelEngine(GpuLocal(eng), comm, w["slots"])
     sched = make_scheduler(pb, w, front, "april", seed, world if dp else 1)
-    run_steps(pb, w, sched, eng, 0, args.warmup)
+    run_steps(pb, w, sched, eng, 0, args.warmup, timed_e2e=True, comm=comm)
     if dist:
         dist.barrier()
     eng.profile(True, args.profile_every)
@@ -289,7 +349,9 @@ def main():
     launches0 = st0.kernel_launches
     with ClockSampler(local) as clk:
         t0 = time.perf_counter()
-        rec = run_steps(pb, w, sched, eng, args.warmup, args.steps)
+        # the same timed steps give `value` (device clock, begin_step -> park) and `e2e` (host wall
+        # clock of the public-API call plus the finished-response gather, rewards and advantages)
+        rec = run_steps(pb, w, sched, eng, args.warmup, args.steps, timed_e2e=True, comm=comm)
         t_dev = sum(r["wall"] for r in rec)
         if dist:
             import torch
@@ -307,8 +369,7 @@ def main():
     kstats = {k["name"]: k for k in eng.kernel_stats()}
     eng.profile(False)
     tokens = sum(r["tokens"] for r in rec)
-    # e2e: same steps, payload gathered to host + rewards + advantages, host wall clock
-    rec_e2e = run_steps(pb, w, sched, eng, args.warmup + args.steps, args.steps, timed_e2e=True, comm=comm)
+    rec_e2e = rec
     e2e_tps = sum(r["tokens"] for r in rec_e2e) / sum(r["host"] for r in rec_e2e)
     stats = eng.stats()
     eng.close()
@@ -321,7 +382,8 @@ def main():
         if dp:
             front_s = DataParallelEngine(GpuLocal(eng_s), comm, w["slots"])
         sch_s = make_scheduler(pb, w, front_s, "baseline", seed, world if dp else 1)
-        rs = run_steps(pb, w, sch_s, eng_s, 0, args.sync_steps, timed_e2e=args.out is not None, comm=comm)
+        run_steps(pb, w, sch_s, eng_s, 0, 1, timed_e2e=True, comm=comm)  # warm-up (graphs, autotune cache)
+        rs = run_steps(pb, w, sch_s, eng_s, 1, args.sync_steps, timed_e2e=True, comm=comm)
         sync = {"tokens_per_s": sum(r["tokens"] for r in rs) / sum(r["wall"] for r in rs),
                 "ms_per_step": 1e3 * statistics.mean(r["wall"] for r in rs), "steps": len(rs),
                 "iterations_per_step": statistics.mean(r["iters"] for r in rs)}

@@ -69,14 +69,18 @@ def random_weights(spec, seed: int = 0, std: float = 0.02) -> dict:
 
 class CpuDecoder:
     """round_bf16=False drops the engine's bf16 activation roundings (pure fp32 math on the bf16
-    weights): the form `tests/test_cpu_model_pin.py` checks against transformers' Qwen2 / Qwen3."""
+    weights): the form `tests/test_cpu_model_pin.py` checks against transformers' Qwen2 / Qwen3.
+    compute_dtype=torch.float64 keeps the roundings but sums in fp64: the distance between the fp32
+    and fp64 forms is the noise floor of the rounding scheme itself (tools/noise_floor.py)."""
 
-    def __init__(self, spec, weights: dict, threads: int | None = None, round_bf16: bool = True):
+    def __init__(self, spec, weights: dict, threads: int | None = None, round_bf16: bool = True,
+                 compute_dtype=torch.float32):
         if threads:
             torch.set_num_threads(threads)
         self.s = spec
-        self._bf = _bf if round_bf16 else (lambda x: x)
-        w = {k: v.float() for k, v in weights.items()}
+        dt = self.dt = compute_dtype  # float64: the same roundings with exact-ish sums (noise-floor runs)
+        self._bf = (lambda x: x.to(torch.bfloat16).to(dt)) if round_bf16 else (lambda x: x)
+        w = {k: v.to(dt) for k, v in weights.items()}
         self.embed = w["embed"]
         self.lm_head = w.get("lm_head", self.embed)
         self.final_norm = w["final_norm"].view(-1)
@@ -100,7 +104,7 @@ class CpuDecoder:
 
     def _rope(self, x, pos):  # x [T, H, hd] fp32, pos [T]
         ang = pos.float()[:, None] * self.inv_freq[None, :]
-        c, s = torch.cos(ang)[:, None, :], torch.sin(ang)[:, None, :]
+        c, s = torch.cos(ang)[:, None, :].to(self.dt), torch.sin(ang)[:, None, :].to(self.dt)
         h = x.shape[-1] // 2
         a, b = x[..., :h], x[..., h:]
         return torch.cat([a * c - b * s, b * c + a * s], dim=-1)

@@ -56,7 +56,7 @@ __global__ void k_group_advantages(const double* __restrict__ r, int n_groups, i
   const double mean = np_pairwise_sum(x, G) / G;
   auto sq = [&](int i) {
     const double c = x[i] - mean;
-    return c * c;
+    return __dmul_rn(c, c);  // rounded product, never contracted into the sum's FMA (numpy rounds it)
   };
   const double sd = sqrt(np_pairwise_sum_f(sq, 0, G) / G);
   for (int i = 0; i < G; ++i) {

@@ -396,7 +396,8 @@ ScopedTimer::~ScopedTimer() {
   if (idx < 0) return;
   cudaEvent_t b = e.take_event();
   cudaEventRecordWithFlags(b, e.stream, cudaEventRecordExternal);
-  e.prof_slots.push_back(Engine::ProfSlot{idx, a, b});
+  if ((int)e.prof_slots.size() <= e.variant) e.prof_slots.resize(e.variant + 1);
+  e.prof_slots[e.variant].push_back(Engine::ProfSlot{idx, a, b});
 }
 
 // Accumulate the profiled graph's event intervals for launch `run_iter`.
@@ -410,7 +411,8 @@ static void collect_prof(Engine& e) {
   AB_CUDA(cudaMemcpy(&b, e.d.it_b + it, sizeof(int32_t), cudaMemcpyDeviceToHost));
   AB_CUDA(cudaMemcpy(&ctx, e.d.it_ctx + it, sizeof(int64_t), cudaMemcpyDeviceToHost));
   if (b <= 0) return;  // iteration queued past the stop point: all kernels were no-ops
-  for (auto& s : e.prof_slots) {
+  if (e.prof_pending_variant >= (int)e.prof_slots.size()) return;
+  for (auto& s : e.prof_slots[e.prof_pending_variant]) {
     float ms = 0;
     AB_CUDA(cudaEventElapsedTime(&ms, s.a, s.b));
     auto& t = e.timers[s.timer];
@@ -581,12 +583,15 @@ static void destroy(Engine* e) {
   if (!e) return;
   cudaSetDevice(e->device);
   cudaStreamSynchronize(e->stream);
-  if (e->iter_graph) cudaGraphExecDestroy(e->iter_graph);
-  if (e->prof_graph) cudaGraphExecDestroy(e->prof_graph);
-  for (auto& s : e->prof_slots) {
-    cudaEventDestroy(s.a);
-    cudaEventDestroy(s.b);
-  }
+  for (auto g : e->iter_graphs)
+    if (g) cudaGraphExecDestroy(g);
+  for (auto g : e->prof_graphs)
+    if (g) cudaGraphExecDestroy(g);
+  for (auto& v : e->prof_slots)
+    for (auto& s : v) {
+      cudaEventDestroy(s.a);
+      cudaEventDestroy(s.b);
+    }
   if (e->model) model_destroy(e->model);
   EngineDev& d = e->d;
   void* ptrs[] = {d.ctl,     d.slot_handle, d.slot_tmp, d.slot_finish, d.slot_token, d.q_buf,  d.h_gen,
@@ -646,13 +651,13 @@ static void submit(Engine& e, const ab_sample_desc* descs, int n) {
 }
 
 static void launch_iteration(Engine& e, int64_t run_iter, bool timed = false) {
-  e.launches += 2 + (e.model ? model_iter_launches(e.model) : 1);
+  e.launches += 2 + (e.model ? model_iter_launches(e.model, e.variant) : 1);
   {
     ScopedTimer t(e, timed, "admit", run_iter);
     k_admit<<<1, 256, 0, e.stream>>>(e.d);
   }
   if (e.model) {
-    model_iteration(e, run_iter, timed);
+    model_iteration(e, run_iter, timed, e.variant);
   } else {
     ScopedTimer t(e, timed, "grow", run_iter);
     k_grow_cf<<<ceil_div(e.d.S, 128), 128, 0, e.stream>>>(e.d);
@@ -679,7 +684,8 @@ static cudaGraphExec_t capture_iteration(Engine& e, bool timed) {
   e.capturing_prof = false;
   AB_CUDA(cudaGraphInstantiate(&x, g, 0));
   AB_CUDA(cudaGraphDestroy(g));
-  e.graph_kernels = e.launches - before;
+  if ((int)e.graph_kernels.size() <= e.variant) e.graph_kernels.resize(e.variant + 1, 0);
+  e.graph_kernels[e.variant] = e.launches - before;
   e.launches = before;
   return x;
 }
@@ -690,17 +696,23 @@ static void launch_iteration_fast(Engine& e, int64_t run_iter, bool first_in_chu
     ++e.direct_launches;
     return;
   }
-  if (!e.iter_graph) e.iter_graph = capture_iteration(e, false);
+  const int v = e.variant;
+  if ((int)e.iter_graphs.size() <= v) {
+    e.iter_graphs.resize(v + 1, nullptr);
+    e.prof_graphs.resize(v + 1, nullptr);
+  }
+  if (!e.iter_graphs[v]) e.iter_graphs[v] = capture_iteration(e, false);
   bool prof = false;
   if (e.profile && first_in_chunk && e.prof_pending < 0) prof = (e.prof_count++ % e.sample_every) == 0;
   if (prof) {
-    if (!e.prof_graph) e.prof_graph = capture_iteration(e, true);
-    AB_CUDA(cudaGraphLaunch(e.prof_graph, e.stream));
+    if (!e.prof_graphs[v]) e.prof_graphs[v] = capture_iteration(e, true);
+    AB_CUDA(cudaGraphLaunch(e.prof_graphs[v], e.stream));
     e.prof_pending = run_iter;
+    e.prof_pending_variant = v;
   } else {
-    AB_CUDA(cudaGraphLaunch(e.iter_graph, e.stream));
+    AB_CUDA(cudaGraphLaunch(e.iter_graphs[v], e.stream));
   }
-  e.launches += e.graph_kernels;
+  e.launches += e.graph_kernels[v];
 }
 
 static void run(Engine& e, const ab_run_args* a, ab_run_result* r, ab_event* ev, int ev_cap, ab_admit* adm,
@@ -712,12 +724,20 @@ static void run(Engine& e, const ab_run_args* a, ab_run_result* r, ab_event* ev,
     AB_CUDA(cudaMemsetAsync(e.d.it_b, 0, sizeof(int32_t) * e.d.it_cap, e.stream));
     AB_CUDA(cudaMemsetAsync(e.d.it_ctx, 0, sizeof(int64_t) * e.d.it_cap, e.stream));
   }
+  if (e.model) sync_ctl(e);  // live batch + queue: the first chunk's graph variant
   int64_t launched = 0;
   int chunk = 1;
   const int policy_chunk = 4;
   while (true) {
     int n = chunk;
     if (a->max_iters > 0) n = (int)std::min<int64_t>(n, std::max<int64_t>(1, a->max_iters - launched));
+    if (e.model) {
+      // admission only happens at iteration starts from the FIFO: no iteration of this chunk can
+      // have more live rows than the current batch plus the queue (capped at S)
+      const Ctl& c0 = *e.ctl_host;
+      const int bmax = (int)std::min<int64_t>(e.d.S, (int64_t)c0.b + (c0.q_tail - c0.q_head));
+      e.variant = model_variant_for(e.model, bmax);
+    }
     for (int i = 0; i < n; ++i) launch_iteration_fast(e, launched + i, i == 0);
     launched += n;
     sync_ctl(e);
@@ -1033,9 +1053,10 @@ int ab_engine_resume_memory(ab_engine* e) {
     Engine& g = *e->impl;
     AB_REQUIRE(g.model != nullptr, AB_ERR_CONTRACT, "engine has no transformer model");
     ab::model_resume_memory(g);
-    if (g.iter_graph) cudaGraphExecDestroy(g.iter_graph);
-    if (g.prof_graph) cudaGraphExecDestroy(g.prof_graph);
-    g.iter_graph = g.prof_graph = nullptr;
+    for (auto& x : g.iter_graphs)
+      if (x) cudaGraphExecDestroy(x), x = nullptr;
+    for (auto& x : g.prof_graphs)
+      if (x) cudaGraphExecDestroy(x), x = nullptr;
   });
 }
 

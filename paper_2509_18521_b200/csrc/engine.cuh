@@ -94,17 +94,19 @@ struct Engine {
   int64_t launches = 0;  // kernels launched (gpu_launches claim)
   bool use_graphs = true;
   int64_t direct_launches = 0;
-  cudaGraphExec_t iter_graph = nullptr;
-  int64_t graph_kernels = 0;
-  // profiling through a second captured graph with event-record nodes
-  cudaGraphExec_t prof_graph = nullptr;
+  // one captured iteration graph per decode plan variant (model_variant_for), plus a profiling
+  // twin with event-record nodes
+  std::vector<cudaGraphExec_t> iter_graphs, prof_graphs;
+  std::vector<int64_t> graph_kernels;
+  int variant = 0;  // variant of the chunk being launched
   bool capturing_prof = false;
   struct ProfSlot {
     int timer;
     cudaEvent_t a, b;
   };
-  std::vector<ProfSlot> prof_slots;
+  std::vector<std::vector<ProfSlot>> prof_slots;  // per variant's profiling graph
   int64_t prof_pending = -1;
+  int prof_pending_variant = 0;
   int64_t prof_count = 0;
   // profiling
   bool profile = false;
@@ -137,8 +139,10 @@ void model_begin_step(Engine& e, int64_t version);
 void model_release_memory(Engine& e);
 void model_resume_memory(Engine& e);
 void model_score(Engine& e, const int32_t* tokens, const int64_t* offs, const int32_t* plen, int n, double* out);
-int64_t model_iter_launches(Model* m);
-void model_iteration(Engine& e, int64_t run_iter, bool timed);         // pages + forward + sampler
+int model_variants(Model* m);              // decode graph variants (plan selections)
+int model_variant_for(Model* m, int rows);  // the variant for a chunk whose live batch is <= rows
+int64_t model_iter_launches(Model* m, int variant);
+void model_iteration(Engine& e, int64_t run_iter, bool timed, int variant);  // pages + forward + sampler
 int64_t model_pages_total(Model* m);
 void model_kernel_cost(Model* m, const std::string& name, double b, double sum_ctx, double* bytes, double* flops);
 

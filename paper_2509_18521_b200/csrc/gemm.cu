@@ -1152,14 +1152,18 @@ void gemm_set_schedule(GemmPlan& p, int force) {
   const auto key = std::make_tuple(p.N, p.K, p.M_cap, p.BN, cs * 4 + (p.pair ? 1 : 0) + (p.nondet ? 2 : 0), force,
                                    p.epi, ncl * 16 + dev);
   std::lock_guard<std::mutex> lock(mu);
+  static std::map<std::tuple<int, int, int, int, int, int, int, int>, std::vector<int>> host_cache;
   auto it = cache.find(key);
   if (it != cache.end()) {
     p.sched = it->second;
+    p.host_tab = host_cache[key];
     return;
   }
   std::vector<int> tab(p.M_cap + 1, 0);
   for (int r = 1; r <= p.M_cap; ++r)
     tab[r] = choose_sched(r, p.N, p.K, p.BN, cs, ncl, force, p.epi, p.pair, nullptr, p.nondet);
+  p.host_tab = tab;
+  host_cache[key] = tab;
   int* d = nullptr;
   AB_CUDA(cudaMalloc(&d, sizeof(int) * tab.size()));
   AB_CUDA(cudaMemcpy(d, tab.data(), sizeof(int) * tab.size(), cudaMemcpyHostToDevice));
@@ -1190,12 +1194,17 @@ std::vector<int> gemm_candidates(const GemmPlan& p, int rows) {
   return out;
 }
 
+int gemm_default_code(const GemmPlan& p, int rows) {
+  return choose_sched(rows, p.N, p.K, p.BN, p.cluster, p.grid / p.cluster, 0, p.epi, p.pair, nullptr, p.nondet);
+}
+
 void gemm_set_table(GemmPlan& p, const std::vector<int>& tab) {
   AB_REQUIRE((int)tab.size() == p.M_cap + 1, AB_ERR_CONFIG, "schedule table size");
   int* d = nullptr;
   AB_CUDA(cudaMalloc(&d, sizeof(int) * tab.size()));
   AB_CUDA(cudaMemcpy(d, tab.data(), sizeof(int) * tab.size(), cudaMemcpyHostToDevice));
   p.sched = d;  // (tables live for the process, like the cached ones)
+  p.host_tab = tab;
   p.idle = std::all_of(tab.begin(), tab.end(), [](int c) { return c == 0; });
 }
 
@@ -1252,6 +1261,7 @@ void gemm_partition(GemmPlan& a, GemmPlan& b) {
     AB_CUDA(cudaMalloc(&d, sizeof(int) * tab.size()));
     AB_CUDA(cudaMemcpy(d, tab.data(), sizeof(int) * tab.size(), cudaMemcpyHostToDevice));
     pt->sched = d;
+    pt->host_tab = tab;
   }
 }
 
@@ -1268,6 +1278,11 @@ void make_tmap_bf16(CUtensorMap* m, const void* ptr, int64_t rows, int64_t cols,
 }
 
 void set_pdl_mask_gemm(int mask) { AB_CUDA(cudaMemcpyToSymbol(c_pdl_mask, &mask, sizeof(int))); }
+
+void gemm_launch_rows(const GemmPlan& p, int rows, cudaStream_t s) {
+  if (!p.host_tab.empty() && (rows < 0 || rows >= (int)p.host_tab.size() || p.host_tab[rows] == 0)) return;
+  gemm_launch(p, s);
+}
 
 void gemm_launch(const GemmPlan& p, cudaStream_t s) {
   if (p.idle) return;

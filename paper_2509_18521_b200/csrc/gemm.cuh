@@ -44,6 +44,7 @@ struct GemmPlan {
   int force = 0;
   const int* sched = nullptr;  // device table: packed schedule per live row count [0, M_cap]
   bool idle = false;           // the table is all zeros: gemm_launch skips the launch
+  std::vector<int> host_tab;   // host copy of the schedule table (row counts known on the host)
   bool early_trigger = false;  // launch_dependents right after setup (successor = a small kernel)
 };
 
@@ -55,6 +56,8 @@ void gemm_plan(GemmPlan& p, const __nv_bfloat16* W, int N, int K, const __nv_bfl
 // launch exits at once.  Both plans are launched every time.
 void gemm_partition(GemmPlan& a, GemmPlan& b);
 void gemm_launch(const GemmPlan& p, cudaStream_t s);
+// Launch only if the plan has work at `rows` (prefill: the row count is known on the host).
+void gemm_launch_rows(const GemmPlan& p, int rows, cudaStream_t s);
 void set_pdl_mask_gemm(int mask);  // early launch_dependents (programmatic dependent launch) per kernel class
 // Autotuning (engine creation): the fixed schedule codes valid for the plan at `rows`; the
 // median device time (us) of `reps` launches of one code at `rows` (L2 flushed before each by
@@ -63,6 +66,8 @@ std::vector<int> gemm_candidates(const GemmPlan& p, int rows);
 double gemm_time_code(const GemmPlan& p, int rows, int code, int reps, void* flush, size_t flush_bytes,
                       cudaStream_t s);
 void gemm_set_table(GemmPlan& p, const std::vector<int>& tab);
+// The cost model's schedule for the plan at `rows` (0: no valid schedule).
+int gemm_default_code(const GemmPlan& p, int rows);
 // Rebuild the plan's schedule table (force: see GemmPlan::force).
 void gemm_set_schedule(GemmPlan& p, int force);
 

@@ -50,6 +50,16 @@ struct Model {
   };
   std::vector<Plans> dec, pf;
   GemmPlan lm_dec, lm_dec2;  // lm_head: CTA pair / 1-SM alternative (autotuned)
+  // Decode plan selection without idle launches.  Every decode projection has two plans whose
+  // cluster shapes differ (a launch attribute), so one captured graph cannot switch between them on
+  // the device.  After autotuning both plans hold FULL schedule tables (valid at every row count)
+  // and each row count has a preferred plan; the distinct preference vectors are the graph
+  // variants (bit j set: projection j = qkv, o, gate-up, down, lm_head runs its second plan).  The
+  // host picks the variant of a chunk of iterations from the chunk's largest possible live batch;
+  // inside the chunk the live batch only shrinks, and the chosen plans are valid at any row count.
+  // Empty: cost-model tables (gemm_autotune = 0), both plans launched with complementary tables.
+  std::vector<int> variant_sel;
+  std::vector<int> variant_of;  // [S + 1]
   // log-prob scoring (model_score): gathered final-norm rows -> lm_head -> log-softmax at the targets
   GemmPlan lm_score;
   bf16* score_a = nullptr;
@@ -110,7 +120,6 @@ int pick_bn(int rows) {
 // fastest (plan, schedule) and the other plan's table entry is 0.  Layers share shapes, so layer 0
 // is tuned and its tables are installed on every layer; results are cached per process.
 static void autotune_decode(Engine& e, Model* M) {
-  static std::map<std::string, std::vector<std::vector<int>>> cache;
   const char* lv = getenv("AB_AUTOTUNE_LOG");
   const bool log = lv != nullptr, log_all = lv && lv[0] == '2';
   cudaStream_t s = e.stream;
@@ -131,13 +140,21 @@ static void autotune_decode(Engine& e, Model* M) {
            std::to_string(p->pair) + "," + std::to_string(p->nondet) + "," + std::to_string(p->grid) + ";";
     return k;
   };
-  auto tune = [&](std::vector<GemmPlan*> g) -> std::vector<std::vector<int>> {
+  // tables: per plan, its best measured schedule at every row count (the cost model's where it has
+  // no valid candidate); choice: per row count, the fastest plan
+  struct Tuned {
+    std::vector<std::vector<int>> tabs;
+    std::vector<int> choice;
+  };
+  static std::map<std::string, Tuned> cache2;
+  auto tune = [&](std::vector<GemmPlan*> g) -> Tuned {
     const std::string key = key_of(g);
-    auto it = cache.find(key);
-    if (it != cache.end()) return it->second;
+    auto it = cache2.find(key);
+    if (it != cache2.end()) return it->second;
     if (!flush) AB_CUDA(cudaMalloc(&flush, flush_bytes));
-    std::vector<std::vector<int>> tabs(g.size(), std::vector<int>(cur_cap + 1, 0));
-    // per ladder row, each plan's best (time, code)
+    Tuned out;
+    out.tabs.assign(g.size(), std::vector<int>(cur_cap + 1, 0));
+    out.choice.assign(cur_cap + 1, 0);
     std::vector<std::vector<std::pair<double, int>>> best(ladder.size(),
                                                           std::vector<std::pair<double, int>>(g.size(), {1e30, 0}));
     for (size_t li = 0; li < ladder.size(); ++li) {
@@ -152,67 +169,96 @@ static void autotune_decode(Engine& e, Model* M) {
           if (us < best[li][i].first) best[li][i] = {us, c};
         }
     }
-    // A plan that is launched costs ~2 us even when its table entry is 0 (the launch, the wait on
-    // its predecessor, the exit): keep both plans only if the second one saves more than that at
-    // some row count; otherwise run every row count on the single best plan.
-    constexpr double kIdleUs = 2.0;
-    std::vector<double> tot(g.size(), 0.0);
-    bool need_both = false;
-    for (size_t li = 0; li < ladder.size(); ++li)
-      for (size_t i = 0; i < g.size(); ++i) tot[i] += best[li][i].first;
-    int single = 0;
-    for (size_t i = 1; i < g.size(); ++i)
-      if (tot[i] < tot[single]) single = (int)i;
-    for (size_t li = 0; li < ladder.size() && g.size() > 1; ++li) {
-      double mn = 1e30;
-      for (size_t i = 0; i < g.size(); ++i) mn = std::min(mn, best[li][i].first);
-      if (best[li][single].first - mn > kIdleUs) need_both = true;
-    }
     int lo = 1;
     for (size_t li = 0; li < ladder.size(); ++li) {
       const int r = ladder[li];
-      int bp = single;
-      if (need_both)
+      int bp = 0;
+      for (size_t i = 1; i < g.size(); ++i)
+        if (best[li][i].first < best[li][bp].first) bp = (int)i;
+      for (int x = lo; x <= r; ++x) {
+        out.choice[x] = bp;
         for (size_t i = 0; i < g.size(); ++i)
-          if (best[li][i].first < best[li][bp].first) bp = (int)i;
-      if (best[li][bp].first < 1e29)
-        for (int x = lo; x <= r; ++x) tabs[bp][x] = best[li][bp].second;
+          out.tabs[i][x] = best[li][i].first < 1e29 ? best[li][i].second : gemm_default_code(*g[i], x);
+      }
       if (log)
-        fprintf(stderr, "[autotune] N=%d K=%d epi=%d rows=%d plan=%d (cluster %d%s) code=0x%x %.1f us (%s)\n", g[0]->N,
-                g[0]->K, g[0]->epi, r, bp, g[bp]->cluster, g[bp]->pair ? " pair" : "", best[li][bp].second,
-                best[li][bp].first, need_both ? "both plans" : "single plan");
+        fprintf(stderr, "[autotune] N=%d K=%d epi=%d rows=%d plan=%d (cluster %d%s) code=0x%x %.1f us (other %.1f us)\n",
+                g[0]->N, g[0]->K, g[0]->epi, r, bp, g[bp]->cluster, g[bp]->pair ? " pair" : "",
+                best[li][bp].second, best[li][bp].first, best[li][1 - bp].first);
       lo = r + 1;
     }
-    cache[key] = tabs;
-    return tabs;
+    out.tabs[0][0] = out.tabs[1][0] = 0;
+    // a plan with no schedule at some row count is never chosen (it could not cover a shrinking batch)
+    for (size_t i = 0; i < g.size(); ++i)
+      for (int x = 1; x <= cur_cap; ++x)
+        if (out.tabs[i][x] == 0) {
+          for (int y = 1; y <= cur_cap; ++y)
+            if (out.choice[y] == (int)i) out.choice[y] = 1 - (int)i;
+          break;
+        }
+    cache2[key] = out;
+    return out;
   };
   const int L = (int)M->dec.size();
-  auto apply = [&](std::vector<Model::Plans>& v, GemmPlan Model::Plans::*a, GemmPlan Model::Plans::*b) {
+  std::vector<std::vector<int>> choices;  // per projection (qkv, o, gate-up, down, lm_head)
+  auto apply = [&](std::vector<Model::Plans>& v, GemmPlan Model::Plans::*a, GemmPlan Model::Plans::*b,
+                   bool decode) {
     std::vector<GemmPlan*> g = {&(v[0].*a), &(v[0].*b)};
-    const auto tabs = tune(g);
-    for (int l = 0; l < L; ++l) {
-      gemm_set_table(v[l].*a, tabs[0]);
-      gemm_set_table(v[l].*b, tabs[1]);
+    Tuned t = tune(g);
+    if (!decode) {  // prefill: the host knows the row count, launch only the chosen plan's entry
+      for (int x = 0; x <= cur_cap; ++x) t.tabs[1 - t.choice[x]][x] = 0;
     }
+    for (int l = 0; l < L; ++l) {
+      gemm_set_table(v[l].*a, t.tabs[0]);
+      gemm_set_table(v[l].*b, t.tabs[1]);
+    }
+    if (decode) choices.push_back(t.choice);
   };
-  apply(M->dec, &Model::Plans::qkv, &Model::Plans::qkv2);
-  apply(M->dec, &Model::Plans::o, &Model::Plans::o2);
-  apply(M->dec, &Model::Plans::down, &Model::Plans::down2);
-  apply(M->dec, &Model::Plans::gu, &Model::Plans::gu2);
+  apply(M->dec, &Model::Plans::qkv, &Model::Plans::qkv2, true);
+  apply(M->dec, &Model::Plans::o, &Model::Plans::o2, true);
+  apply(M->dec, &Model::Plans::gu, &Model::Plans::gu2, true);
+  apply(M->dec, &Model::Plans::down, &Model::Plans::down2, true);
   {
-    const auto tabs = tune({&M->lm_dec, &M->lm_dec2});
-    gemm_set_table(M->lm_dec, tabs[0]);
-    gemm_set_table(M->lm_dec2, tabs[1]);
+    Tuned t = tune({&M->lm_dec, &M->lm_dec2});
+    gemm_set_table(M->lm_dec, t.tabs[0]);
+    gemm_set_table(M->lm_dec2, t.tabs[1]);
+    choices.push_back(t.choice);
   }
+  // graph variants: the distinct per-row-count plan choices
+  M->variant_sel.clear();
+  M->variant_of.assign(S + 1, 0);
+  for (int r = 1; r <= S; ++r) {
+    int sel = 0;
+    for (size_t j = 0; j < choices.size(); ++j) sel |= choices[j][r] << j;
+    int v = -1;
+    for (size_t k = 0; k < M->variant_sel.size(); ++k)
+      if (M->variant_sel[k] == sel) v = (int)k;
+    if (v < 0) {
+      v = (int)M->variant_sel.size();
+      M->variant_sel.push_back(sel);
+    }
+    M->variant_of[r] = v;
+  }
+  M->variant_of[0] = M->variant_of[1];
+  if (log)
+    for (size_t k = 0; k < M->variant_sel.size(); ++k) {
+      int lo = -1, hi = -1;
+      for (int r = 1; r <= S; ++r)
+        if (M->variant_of[r] == (int)k) {
+          if (lo < 0) lo = r;
+          hi = r;
+        }
+      fprintf(stderr, "[autotune] graph variant %zu: plan bits 0x%x (qkv,o,gu,down,lm), rows %d..%d\n", k,
+              M->variant_sel[k], lo, hi);
+    }
   // prefill chunks (up to M_pf rows): 1-SM plans against CTA-pair plans on a coarse ladder
   ladder.clear();
   for (int r = 64; r < M->M_pf; r *= 4) ladder.push_back(r);
   ladder.push_back(M->M_pf);
   cur_cap = M->M_pf;
-  apply(M->pf, &Model::Plans::qkv, &Model::Plans::qkv_p);
-  apply(M->pf, &Model::Plans::o, &Model::Plans::o_p);
-  apply(M->pf, &Model::Plans::gu, &Model::Plans::gu_p);
-  apply(M->pf, &Model::Plans::down, &Model::Plans::down_p);
+  apply(M->pf, &Model::Plans::qkv, &Model::Plans::qkv_p, false);
+  apply(M->pf, &Model::Plans::o, &Model::Plans::o_p, false);
+  apply(M->pf, &Model::Plans::gu, &Model::Plans::gu_p, false);
+  apply(M->pf, &Model::Plans::down, &Model::Plans::down_p, false);
   if (flush) AB_CUDA(cudaFree(flush));
   // the timing runs accumulated into the decode workspaces: the QKV accumulator must start at zero
   AB_CUDA(cudaMemsetAsync(M->qkv32, 0, sizeof(float) * (size_t)S * M->md.qkv_dim, s));
@@ -536,24 +582,24 @@ static void prefill_rows(Engine& e, int R, int nb) {
     const LayerW& w = M->layers[l];
     const Model::Plans& p = M->pf[l];
     launch_rmsnorm(M->x, w.attn_norm, M->xn, m.d, m.eps, nullptr, R, nullptr, s);
-    gemm_launch(p.qkv, s);
-    gemm_launch(p.qkv_p, s);
+    gemm_launch_rows(p.qkv, R, s);
+    gemm_launch_rows(p.qkv_p, R, s);
     launch_rope_kv(m, l, M->qkv, w.q_norm, w.k_norm, M->qrot, nullptr, R, nullptr, s);
     launch_prefill_flash(m, l, M->qrot, M->attn, M->pf_blocks, nb, s);
-    gemm_launch(p.o, s);
-    gemm_launch(p.o_p, s);
+    gemm_launch_rows(p.o, R, s);
+    gemm_launch_rows(p.o_p, R, s);
     launch_rmsnorm(M->x, w.mlp_norm, M->xn, m.d, m.eps, nullptr, R, nullptr, s);
-    gemm_launch(p.gu, s);
-    gemm_launch(p.gu_p, s);
-    gemm_launch(p.down, s);
-    gemm_launch(p.down_p, s);
+    gemm_launch_rows(p.gu, R, s);
+    gemm_launch_rows(p.gu_p, R, s);
+    gemm_launch_rows(p.down, R, s);
+    gemm_launch_rows(p.down_p, R, s);
   }
   AB_CUDA(cudaGetLastError());
   AB_CUDA(cudaStreamSynchronize(s));  // host staging is reused by the next chunk
   int64_t g = 0;
   for (const GemmPlan* pp : {&M->pf[0].qkv, &M->pf[0].qkv_p, &M->pf[0].o, &M->pf[0].o_p, &M->pf[0].gu,
                              &M->pf[0].gu_p, &M->pf[0].down, &M->pf[0].down_p})
-    g += pp->idle ? 0 : 1;
+    g += (pp->idle || (!pp->host_tab.empty() && pp->host_tab[R] == 0)) ? 0 : 1;
   e.launches += 1 + (4 + g) * (int64_t)m.L;
 }
 
@@ -859,17 +905,38 @@ void model_release_group(Engine& e, int group_slot) {
   AB_CUDA(cudaGetLastError());
 }
 
-// kernels one decode iteration launches (plans with an all-zero table are skipped)
-int64_t model_iter_launches(Model* M) {
-  int64_t n = 4 + (M->lm_dec.idle ? 0 : 1) + (M->lm_dec2.idle ? 0 : 1);  // prep, embed, final norm, lm_head, sampler
-  for (const auto& p : M->dec) {
-    n += 4;  // 2 norms, rope / KV write, attention
-    for (const GemmPlan* g : {&p.qkv, &p.qkv2, &p.o, &p.o2, &p.gu, &p.gu2, &p.down, &p.down2}) n += g->idle ? 0 : 1;
+int model_variants(Model* M) { return std::max<int>(1, (int)M->variant_sel.size()); }
+
+int model_variant_for(Model* M, int rows) {
+  if (M->variant_sel.empty()) return 0;
+  return M->variant_of[std::max(0, std::min(rows, M->S))];
+}
+
+// Launch the plan of projection j the variant selects (legacy tables: both, idle ones are skipped).
+static void launch_pair(Model* M, int variant, int j, const GemmPlan& a, const GemmPlan& b, cudaStream_t s) {
+  if (M->variant_sel.empty()) {
+    gemm_launch(a, s);
+    gemm_launch(b, s);
+  } else {
+    gemm_launch(((M->variant_sel[variant] >> j) & 1) ? b : a, s);
   }
+}
+
+static int pair_launches(Model* M, int variant, int j, const GemmPlan& a, const GemmPlan& b) {
+  if (M->variant_sel.empty()) return (a.idle ? 0 : 1) + (b.idle ? 0 : 1);
+  return (((M->variant_sel[variant] >> j) & 1) ? b : a).idle ? 0 : 1;
+}
+
+// kernels one decode iteration of graph variant `variant` launches
+int64_t model_iter_launches(Model* M, int variant) {
+  int64_t n = 4 + pair_launches(M, variant, 4, M->lm_dec, M->lm_dec2);  // prep, embed, final norm, sampler
+  for (const auto& p : M->dec)
+    n += 4 + pair_launches(M, variant, 0, p.qkv, p.qkv2) + pair_launches(M, variant, 1, p.o, p.o2) +
+         pair_launches(M, variant, 2, p.gu, p.gu2) + pair_launches(M, variant, 3, p.down, p.down2);
   return n;
 }
 
-void model_iteration(Engine& e, int64_t run_iter, bool timed) {
+void model_iteration(Engine& e, int64_t run_iter, bool timed, int variant) {
   Model* M = e.model;
   ModelDev& m = M->md;
   cudaStream_t s = e.stream;
@@ -893,8 +960,7 @@ void model_iteration(Engine& e, int64_t run_iter, bool timed) {
     }
     {
       ScopedTimer t(e, timed, "gemm_qkv", run_iter);
-      gemm_launch(p.qkv, s);
-      gemm_launch(p.qkv2, s);
+      launch_pair(M, variant, 0, p.qkv, p.qkv2, s);
     }
     {
       ScopedTimer t(e, timed, "rope_kv", run_iter);
@@ -907,8 +973,7 @@ void model_iteration(Engine& e, int64_t run_iter, bool timed) {
     }
     {
       ScopedTimer t(e, timed, "gemm_o", run_iter);
-      gemm_launch(p.o, s);
-      gemm_launch(p.o2, s);
+      launch_pair(M, variant, 1, p.o, p.o2, s);
     }
     {
       ScopedTimer t(e, timed, "rmsnorm", run_iter);
@@ -916,13 +981,11 @@ void model_iteration(Engine& e, int64_t run_iter, bool timed) {
     }
     {
       ScopedTimer t(e, timed, "gemm_gate_up", run_iter);
-      gemm_launch(p.gu, s);
-      gemm_launch(p.gu2, s);
+      launch_pair(M, variant, 2, p.gu, p.gu2, s);
     }
     {
       ScopedTimer t(e, timed, "gemm_down", run_iter);
-      gemm_launch(p.down, s);
-      gemm_launch(p.down2, s);
+      launch_pair(M, variant, 3, p.down, p.down2, s);
     }
   }
   {
@@ -931,8 +994,7 @@ void model_iteration(Engine& e, int64_t run_iter, bool timed) {
   }
   {
     ScopedTimer t(e, timed, "gemm_lm_head", run_iter);
-    gemm_launch(M->lm_dec, s);
-    gemm_launch(M->lm_dec2, s);
+    launch_pair(M, variant, 4, M->lm_dec, M->lm_dec2, s);
   }
   {
     ScopedTimer t(e, timed, "sampler", run_iter);

