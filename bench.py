@@ -123,23 +123,16 @@ def make_scheduler(pb, w, eng, mode, seed, world=1):
 def learner_glue(pb, w, out, target_token=0, comm=None):
     """Synthetic GRPO glue (simulate.py:47-65): target-token-fraction rewards on the
     delivered token ids, then the K6 advantage kernel over contiguous groups.  Data-parallel:
-    each rank scores the responses it generated and the finished-response results are
-    gathered (NCCL) so every rank sees the whole batch in delivery order."""
+    the finished responses (int32 token ids, fp64 behaviour log-probs, lengths) are gathered
+    over NCCL (`dist.gather_responses`), so the trainer sees the whole batch in delivery order."""
     samples = out.batch_samples()
-    mine = {}
-    for s in samples:
-        # ownership first: a sample generated on another rank is a local mirror whose segments
-        # carry no payload (tokens None), and token_ids() would raise on it
-        if comm is not None and any(seg.tokens is None for seg in s.segments):
-            continue
-        toks = s.token_ids()
-        mine[s.sample_id] = sum(1 for t in toks if t % 4 == target_token) / len(toks) if toks else 0.0
     if comm is not None:
-        merged = {}
-        for part in comm.allgather(mine):
-            merged.update(part)
-        mine = merged
-    rewards = [mine[s.sample_id] for s in samples]
+        from paper_2509_18521_b200.dist import gather_responses
+
+        toks_all = [t for t, _ in gather_responses(comm, samples)]
+    else:
+        toks_all = [s.token_ids() for s in samples]
+    rewards = [sum(1 for t in toks if t % 4 == target_token) / len(toks) if toks else 0.0 for toks in toks_all]
     pb.batch_advantages(rewards, w["g"], w["adv"])
     return float(sum(rewards) / len(rewards)) if rewards else 0.0
 
@@ -339,7 +332,9 @@ def main():
         from paper_2509_18521_b200.dist import DataParallelEngine, GpuLocal, TorchComm
 
         comm = TorchComm(device=f"cuda:{local}")
-        front = DataParallelEngine(GpuLocal(eng), comm, w["slots"])
+        # device lockstep: the per-iteration count exchange runs over NVLink peer memory inside
+        # the captured iteration graph (no host round trip per iteration)
+        front = DataParallelEngine(GpuLocal(eng).attach(comm), comm, w["slots"])
     sched = make_scheduler(pb, w, front, "april", seed, world if dp else 1)
     run_steps(pb, w, sched, eng, 0, args.warmup, timed_e2e=True, comm=comm)
     if dist:
@@ -380,7 +375,7 @@ def main():
         _, eng_s = build_engine(pb, w, local, seed, record=True)
         front_s = eng_s
         if dp:
-            front_s = DataParallelEngine(GpuLocal(eng_s), comm, w["slots"])
+            front_s = DataParallelEngine(GpuLocal(eng_s).attach(comm), comm, w["slots"])
         sch_s = make_scheduler(pb, w, front_s, "baseline", seed, world if dp else 1)
         run_steps(pb, w, sch_s, eng_s, 0, 1, timed_e2e=True, comm=comm)  # warm-up (graphs, autotune cache)
         rs = run_steps(pb, w, sch_s, eng_s, 1, args.sync_steps, timed_e2e=True, comm=comm)
@@ -421,7 +416,8 @@ def main():
                    "prompt_len": w["prompt"], "slots": w["slots"], "temperature": w["temperature"],
                    "gemm": ("fp32-residual split-K partials reduce-added by TMA (split summation order not fixed)"
                             if w.get("nondet_gemm") else "deterministic schedules"),
-                   "parallelism": (f"dp{world} lockstep engines (NCCL per-iteration count allreduce, response gather)"
+                   "parallelism": (f"dp{world} lockstep engines (per-iteration count exchange over NVLink peer memory in the "
+                                    f"iteration graph, NCCL response gather)"
                                    if dp else f"dp{world} replicas"),
                    "l2": "inputs larger than L2 (weights + KV >> 126 MB)"},
         "april": {"tokens_per_s": value, "ms_per_step": ms_step, "steps": len(rec),

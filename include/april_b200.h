@@ -214,6 +214,29 @@ int ab_engine_kernel_stats(ab_engine* e, ab_kernel_stat* out, int cap, int* n);
 int ab_engine_synchronize(ab_engine* e);
 /* data-parallel lockstep: align the device iteration counter with the global index */
 int ab_engine_set_iteration(ab_engine* e, int64_t iteration_index);
+int ab_engine_set_counters(ab_engine* e, int64_t iteration_index, int64_t cumulative_tokens);
+
+/* Data-parallel lockstep on the device (the reference is one engine, and
+ * its trigger loop scheduler.py:272-283 becomes global).  One engine per GPU, one process per GPU.
+ * Each engine exports a small exchange buffer in its own HBM; after every rank attached the world's
+ * buffers, every decode iteration ends with k_dp_exchange: each rank stores its (completed groups,
+ * completed samples, live rows, next live rows, iterations-to-next-finish) into every peer's buffer
+ * over NVLink and sums the world's records, so the APRIL trigger, drain, iteration_index and
+ * cumulative_tokens are global on every rank with no host round trip per iteration.  ab_engine_run
+ * then runs the lockstep loop (events / admissions in the logs are this rank's only).
+ *   export: allocate + zero the buffer; *dev_ptr = its device address, ipc_handle (64 bytes, may be
+ *           NULL) = its cudaIpcMemHandle_t for other processes.
+ *   attach: peers[r] = rank r's buffer (kind 0: same-process device pointer; kind 1: IPC handle);
+ *           every rank must have exported before any rank attaches; timeout_ms bounds each wait. */
+typedef struct ab_dp_peer {
+  uint64_t ptr;
+  int32_t kind; /* 0 = device pointer in this process, 1 = CUDA IPC handle */
+  int32_t reserved;
+  uint8_t ipc[64];
+} ab_dp_peer;
+int ab_engine_dp_export(ab_engine* e, int world, uint64_t* dev_ptr, void* ipc_handle);
+int ab_engine_dp_attach(ab_engine* e, int world, int rank, const ab_dp_peer* peers, int64_t timeout_ms);
+int ab_engine_dp_detach(ab_engine* e);
 
 /* K6: group-normalised advantages over contiguous groups of G rewards.
  * mode 0 = mean baseline, 1 = mean/std (GRPO), 2 = mean/std with a

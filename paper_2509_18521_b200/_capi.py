@@ -82,6 +82,10 @@ class Stats(C.Structure):
                 ("reprefill_tokens", C.c_int64), ("reprefill_seconds", C.c_double)]
 
 
+class DpPeer(C.Structure):
+    _fields_ = [("ptr", C.c_uint64), ("kind", C.c_int32), ("reserved", C.c_int32), ("ipc", C.c_uint8 * 64)]
+
+
 class KernelStat(C.Structure):
     _fields_ = [("name", C.c_char * 32), ("launches", C.c_int64), ("ms", C.c_double), ("bytes", C.c_double),
                 ("flops", C.c_double)]
@@ -120,6 +124,10 @@ _SIGS = {
     "ab_engine_kernel_stats": [P, C.POINTER(KernelStat), C.c_int, C.POINTER(C.c_int)],
     "ab_engine_synchronize": [P],
     "ab_engine_set_iteration": [P, C.c_int64],
+    "ab_engine_set_counters": [P, C.c_int64, C.c_int64],
+    "ab_engine_dp_export": [P, C.c_int, C.POINTER(C.c_uint64), P],
+    "ab_engine_dp_attach": [P, C.c_int, C.c_int, C.POINTER(DpPeer), C.c_int64],
+    "ab_engine_dp_detach": [P],
     "ab_group_advantages": [F64P, C.c_int, C.c_int, C.c_int, C.c_double, F64P, I32P, C.c_int],
     "ab_clipped_ratio_terms": [F64P, F64P, I64P, C.c_int, F64P, C.c_double, C.c_double, C.c_int, F64P, I32P,
                                F64P, C.c_int],

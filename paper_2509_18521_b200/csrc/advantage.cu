@@ -19,6 +19,7 @@
 // clip-higher surrogate (policy.py:153-177: clipped iff A > 0 and r > 1 + eps_high, or
 // A < 0 and r < 1 - eps) and per response sum_t min(r A, clip(r, 1 - eps, 1 + eps_high) A);
 // sequence_level: GSPO's length-normalised ratio exp(mean_t(logp_now - logp_behaviour)).
+#include <mutex>
 #include <vector>
 
 #include "common.cuh"
@@ -102,15 +103,21 @@ __global__ void k_clipped_ratio(const double* __restrict__ now, const double* __
   if (lane == 0) surrogate[k] = acc;
 }
 
-// device scratch reused across calls (grown on demand; one per device) -- no allocation per call
+// Per-device scratch reused across calls (grown on demand, stream-ordered) and a private
+// non-blocking stream: no allocation per call, and no device-wide synchronisation, so a call never
+// waits on an engine's decode loop running on the same device (several engines per process in the
+// data-parallel tests).  The mutex serialises callers that share a device.
 struct Scratch {
+  std::mutex mu;
+  cudaStream_t stream = nullptr;
   void* p = nullptr;
   size_t cap = 0;
   void* get(size_t bytes) {
+    if (!stream) AB_CUDA(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking));
     if (bytes > cap) {
-      if (p) cudaFree(p);
+      if (p) AB_CUDA(cudaFreeAsync(p, stream));
       cap = bytes + (bytes >> 1);
-      AB_CUDA(cudaMalloc(&p, cap));
+      AB_CUDA(cudaMallocAsync(&p, cap, stream));
     }
     return p;
   }
@@ -140,18 +147,20 @@ extern "C" int ab_group_advantages(const double* rewards, int n_groups, int grou
     const bool dev_in = is_device_ptr(rewards), dev_out = is_device_ptr(adv);
     const bool dev_flags = zero_std_flags == nullptr || is_device_ptr(zero_std_flags);
     // host arrays are staged through one reusable device buffer: [rewards | advantages | flags]
-    uint8_t* scratch = nullptr;
-    if (!dev_in || !dev_out || !dev_flags)
-      scratch = (uint8_t*)ab::g_scratch[device].get(2 * n * sizeof(double) + n_groups * sizeof(int32_t));
+    ab::Scratch& sc = ab::g_scratch[device];
+    std::lock_guard<std::mutex> lock(sc.mu);
+    uint8_t* scratch = (uint8_t*)sc.get(2 * n * sizeof(double) + n_groups * sizeof(int32_t));
+    cudaStream_t st = sc.stream;
     const double* dr = dev_in ? rewards : (const double*)scratch;
     double* da = dev_out ? adv : (double*)(scratch + n * sizeof(double));
     int32_t* df = dev_flags ? zero_std_flags : (int32_t*)(scratch + 2 * n * sizeof(double));
-    if (!dev_in) AB_CUDA(cudaMemcpy((void*)dr, rewards, n * sizeof(double), cudaMemcpyHostToDevice));
-    ab::k_group_advantages<<<ab::ceil_div(n_groups, 128), 128>>>(dr, n_groups, group_size, mode, eps, da, df);
+    if (!dev_in) AB_CUDA(cudaMemcpyAsync((void*)dr, rewards, n * sizeof(double), cudaMemcpyHostToDevice, st));
+    ab::k_group_advantages<<<ab::ceil_div(n_groups, 128), 128, 0, st>>>(dr, n_groups, group_size, mode, eps, da, df);
     AB_CUDA(cudaGetLastError());
-    if (!dev_out) AB_CUDA(cudaMemcpy(adv, da, n * sizeof(double), cudaMemcpyDeviceToHost));
-    if (!dev_flags) AB_CUDA(cudaMemcpy(zero_std_flags, df, n_groups * sizeof(int32_t), cudaMemcpyDeviceToHost));
-    AB_CUDA(cudaDeviceSynchronize());
+    if (!dev_out) AB_CUDA(cudaMemcpyAsync(adv, da, n * sizeof(double), cudaMemcpyDeviceToHost, st));
+    if (!dev_flags)
+      AB_CUDA(cudaMemcpyAsync(zero_std_flags, df, n_groups * sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+    AB_CUDA(cudaStreamSynchronize(st));
     return AB_OK;
   } catch (const ab::Error& e) {
     ab::set_last_error(e.what());
@@ -172,7 +181,10 @@ extern "C" int ab_clipped_ratio_terms(const double* logp_now, const double* logp
     const int64_t nr = sequence_level ? n : T;
     // host in / host out through one reusable device buffer
     const size_t bytes = (size_t)(2 * T + n) * 8 + (size_t)(n + 1) * 8 + (size_t)nr * 12 + (size_t)n * 8;
-    uint8_t* p = (uint8_t*)ab::g_scratch[device].get(bytes);
+    ab::Scratch& sc = ab::g_scratch[device];
+    std::lock_guard<std::mutex> lock(sc.mu);
+    uint8_t* p = (uint8_t*)sc.get(bytes);
+    cudaStream_t st = sc.stream;
     double* d_now = (double*)p;
     double* d_beh = d_now + T;
     double* d_adv = d_beh + T;
@@ -181,19 +193,21 @@ extern "C" int ab_clipped_ratio_terms(const double* logp_now, const double* logp
     double* d_sur = d_rat + nr;
     int32_t* d_clip = (int32_t*)(d_sur + n);
     if (T) {
-      AB_CUDA(cudaMemcpy(d_now, logp_now, T * 8, cudaMemcpyHostToDevice));
-      AB_CUDA(cudaMemcpy(d_beh, logp_beh, T * 8, cudaMemcpyHostToDevice));
+      AB_CUDA(cudaMemcpyAsync(d_now, logp_now, T * 8, cudaMemcpyHostToDevice, st));
+      AB_CUDA(cudaMemcpyAsync(d_beh, logp_beh, T * 8, cudaMemcpyHostToDevice, st));
     }
-    AB_CUDA(cudaMemcpy(d_adv, adv, n * 8, cudaMemcpyHostToDevice));
-    AB_CUDA(cudaMemcpy(d_offs, offs, (n + 1) * 8, cudaMemcpyHostToDevice));
-    ab::k_clipped_ratio<<<ab::ceil_div(n, 8), 256>>>(d_now, d_beh, d_offs, n, d_adv, 1.0 - eps_clip,
-                                                     1.0 + eps_clip_high, sequence_level, d_rat, d_clip, d_sur);
+    AB_CUDA(cudaMemcpyAsync(d_adv, adv, n * 8, cudaMemcpyHostToDevice, st));
+    AB_CUDA(cudaMemcpyAsync(d_offs, offs, (n + 1) * 8, cudaMemcpyHostToDevice, st));
+    ab::k_clipped_ratio<<<ab::ceil_div(n, 8), 256, 0, st>>>(d_now, d_beh, d_offs, n, d_adv, 1.0 - eps_clip,
+                                                            1.0 + eps_clip_high, sequence_level, d_rat, d_clip,
+                                                            d_sur);
     AB_CUDA(cudaGetLastError());
     if (nr) {
-      AB_CUDA(cudaMemcpy(ratios, d_rat, nr * 8, cudaMemcpyDeviceToHost));
-      AB_CUDA(cudaMemcpy(clipped, d_clip, nr * 4, cudaMemcpyDeviceToHost));
+      AB_CUDA(cudaMemcpyAsync(ratios, d_rat, nr * 8, cudaMemcpyDeviceToHost, st));
+      AB_CUDA(cudaMemcpyAsync(clipped, d_clip, nr * 4, cudaMemcpyDeviceToHost, st));
     }
-    AB_CUDA(cudaMemcpy(surrogate, d_sur, n * 8, cudaMemcpyDeviceToHost));
+    AB_CUDA(cudaMemcpyAsync(surrogate, d_sur, n * 8, cudaMemcpyDeviceToHost, st));
+    AB_CUDA(cudaStreamSynchronize(st));
     return AB_OK;
   } catch (const ab::Error& e) {
     ab::set_last_error(e.what());

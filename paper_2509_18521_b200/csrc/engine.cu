@@ -16,6 +16,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstddef>
 #include <cstdio>
 #include <cstring>
 #include <mutex>
@@ -51,6 +52,7 @@ __global__ void k_run_begin(EngineDev d, ab_run_args a) {
   c->completed_groups = a.completed_groups;
   c->completed_samples = a.completed_samples;
   c->iters_to_next = 1;
+  c->dp_done = 0;
 }
 
 __device__ __forceinline__ bool trigger_fired(const Ctl* c) {
@@ -68,6 +70,7 @@ __global__ void k_admit(EngineDev d) {
     if (c->use_trigger && trigger_fired(c)) {  // trigger seeded as already fired: no decoding at all
       c->stop = 1;
       c->stop_reason = AB_RUN_TRIGGER;
+      c->dp_done = 1;  // data-parallel: the seeded counters are global, every rank stops here
       s_n = -1;
     } else {
       s_b = c->b;
@@ -106,7 +109,13 @@ __global__ void k_admit(EngineDev d) {
     c->b = b + n;
     c->q_head = s_head + n;
     c->n_admits += n;
-    if (c->error != kErrNone) {
+    if (d.dp_world > 1 && (c->error != kErrNone || c->b == 0)) {
+      // data-parallel: this rank sits the iteration out (stop = 2 skips every kernel up to the
+      // exchange); whether the job is drained or failed is decided globally by k_dp_exchange
+      c->stop = 2;
+      c->dp_groups = c->dp_samples = c->dp_b = c->dp_next = 0;
+      c->dp_hint = 0x7fffffff;
+    } else if (c->error != kErrNone) {
       c->stop = 1;
       c->stop_reason = -2;
     } else if (c->b == 0) {  // engine.py:153-154 / 161-162: nothing to decode
@@ -273,7 +282,22 @@ __global__ void __launch_bounds__(kFinishThreads) k_finish(EngineDev d) {
   if ((threadIdx.x & 31) == 0) atomicMin(&s_min_rem, min_rem);
   __syncthreads();
   for (int i = threadIdx.x; i < tk; i += blockDim.x) d.slot_handle[i] = d.slot_tmp[i];
-  if (threadIdx.x == 0) {
+  if (threadIdx.x == 0 && d.dp_world > 1) {
+    // data-parallel: publish this rank's share; k_dp_exchange advances the global counters and
+    // decides trigger / drain for every rank at once
+    c->b = tk;
+    c->n_events = ev_base + td;
+    if (c->run_iters < d.it_cap) d.it_b[c->run_iters] = b;
+    c->dp_groups = s_new_groups;
+    c->dp_samples = td;
+    c->dp_b = b;
+    c->dp_next = tk + min(d.S - tk, c->q_tail - c->q_head);
+    const bool queue_waiting = (c->q_tail - c->q_head) > 0 && tk < d.S;
+    if (d.stop_mode == AB_STOP_TRACE)
+      c->dp_hint = tk == 0 && !queue_waiting ? 0x7fffffff : (queue_waiting ? 1 : s_min_rem);
+    else
+      c->dp_hint = -1;
+  } else if (threadIdx.x == 0) {
     c->b = tk;
     c->iteration_index = it1;
     c->cumulative_tokens += b;
@@ -300,6 +324,122 @@ __global__ void __launch_bounds__(kFinishThreads) k_finish(EngineDev d) {
       c->stop_reason = AB_RUN_MAX_ITERS;
     }
   }
+}
+
+__device__ __forceinline__ void st_release_sys(int64_t* p, int64_t v) {
+  asm volatile("st.release.sys.global.s64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ int64_t ld_acquire_sys(const int64_t* p) {
+  int64_t v;
+  asm volatile("ld.acquire.sys.global.s64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_relaxed_sys(int64_t* p, int64_t v) {
+  asm volatile("st.relaxed.sys.global.s64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ int64_t ld_relaxed_sys(const int64_t* p) {
+  int64_t v;
+  asm volatile("ld.relaxed.sys.global.s64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+
+constexpr int kDpRec = 8;  // int64 per record: epoch, groups, samples, b, next, hint, error, pad
+
+// Data-parallel lockstep exchange, the last kernel of every iteration when the
+// engine is one of dp_world ranks.  One warp: lane r stores this rank's record into slot
+// [epoch & 1][rank] of rank r's buffer (peer memory over NVLink: payload relaxed, then the epoch
+// with release semantics), then waits for slot [epoch & 1][r] of its own buffer to carry the same
+// epoch (acquire).  The sums are integers, so every rank computes the same global decision:
+// iteration_index / cumulative_tokens / completed counters advance by the global totals, the
+// trigger (scheduler.py:59-64) fires on the global counters, and the job is drained when no rank
+// has a live row.  Two parities: a rank can run at most one exchange ahead of the slowest, so
+// it never overwrites a record that is still being read.  No host round trip per iteration.
+__global__ void k_dp_exchange(EngineDev d) {
+  Ctl* c = d.ctl;
+  if (c->dp_done) return;
+  const int lane = threadIdx.x, W = d.dp_world;
+  const int64_t ep = c->dp_epoch + 1;
+  const int par = (int)(ep & 1);
+  const int64_t err = c->error != kErrNone ? 1 : 0;
+  if (lane < W) {
+    int64_t* dst = d.dp_peers[lane] + ((int64_t)par * W + d.dp_rank) * kDpRec;
+    st_relaxed_sys(dst + 1, c->dp_groups);
+    st_relaxed_sys(dst + 2, c->dp_samples);
+    st_relaxed_sys(dst + 3, c->dp_b);
+    st_relaxed_sys(dst + 4, c->dp_next);
+    st_relaxed_sys(dst + 5, c->dp_hint);
+    st_relaxed_sys(dst + 6, err);
+    st_release_sys(dst, ep);
+  }
+  int64_t g = 0, smp = 0, b = 0, nx = 0, hint = 0x7fffffff, e = 0;
+  int timed_out = 0;
+  if (lane < W) {
+    const int64_t* src = d.dp_local + ((int64_t)par * W + lane) * kDpRec;
+    const uint64_t t0 = globaltimer_ns();
+    while (ld_acquire_sys(src) != ep) {
+      if (globaltimer_ns() - t0 > d.dp_timeout_ns) {
+        timed_out = 1;
+        break;
+      }
+      __nanosleep(32);
+    }
+    if (!timed_out) {
+      g = ld_relaxed_sys(src + 1);
+      smp = ld_relaxed_sys(src + 2);
+      b = ld_relaxed_sys(src + 3);
+      nx = ld_relaxed_sys(src + 4);
+      const int64_t h = ld_relaxed_sys(src + 5);
+      hint = h < 0 ? 0x7fffffff : h;
+      e = ld_relaxed_sys(src + 6);
+    }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    g += __shfl_xor_sync(0xffffffffu, g, o);
+    smp += __shfl_xor_sync(0xffffffffu, smp, o);
+    b += __shfl_xor_sync(0xffffffffu, b, o);
+    nx += __shfl_xor_sync(0xffffffffu, nx, o);
+    e += __shfl_xor_sync(0xffffffffu, e, o);
+    hint = min(hint, __shfl_xor_sync(0xffffffffu, hint, o));
+    timed_out |= __shfl_xor_sync(0xffffffffu, timed_out, o);
+  }
+  if (lane != 0) return;
+  c->dp_epoch = ep;
+  if (timed_out || e) {
+    if (c->error == kErrNone) c->error = timed_out ? kErrDpTimeout : kErrPeer;
+    c->stop = 1;
+    c->stop_reason = -2;
+    c->dp_done = 1;
+    return;
+  }
+  if (b == 0) {  // no rank had a live row: drained (the iteration did not happen)
+    c->stop = 1;
+    c->stop_reason = AB_RUN_DRAINED;
+    c->dp_done = 1;
+    return;
+  }
+  c->iteration_index += 1;
+  c->cumulative_tokens += b;
+  c->completed_groups += g;
+  c->completed_samples += smp;
+  c->run_iters += 1;
+  // trace stop rules: no rank can finish a sample for `hint` iterations (policy rules: unknown)
+  c->iters_to_next = d.stop_mode != AB_STOP_TRACE ? -1 : (int32_t)(hint < 1 ? 1 : (hint > (1 << 14) ? (1 << 14) : hint));
+  c->stop = 0;
+  if (c->use_trigger && smp > 0 && trigger_fired(c)) {
+    c->stop = 1;
+    c->stop_reason = AB_RUN_TRIGGER;
+  } else if (c->stop_on_event && smp > 0) {
+    c->stop = 1;
+    c->stop_reason = AB_RUN_EVENT;
+  } else if (c->max_iters > 0 && c->run_iters >= c->max_iters) {
+    c->stop = 1;
+    c->stop_reason = AB_RUN_MAX_ITERS;
+  } else if (nx == 0) {
+    c->stop = 1;
+    c->stop_reason = AB_RUN_DRAINED;
+  }
+  if (c->stop) c->dp_done = 1;
 }
 
 // Queue submitted descriptors behind the FIFO tail.
@@ -603,6 +743,9 @@ static void destroy(Engine* e) {
   if (e->ctl_host) cudaFreeHost(e->ctl_host);
   if (e->stage_desc_host) cudaFreeHost(e->stage_desc_host);
   if (e->stage_i32_host) cudaFreeHost(e->stage_i32_host);
+  for (void* p : e->dp_ipc_opened) cudaIpcCloseMemHandle(p);
+  if (e->dp_peers_dev) cudaFree(e->dp_peers_dev);
+  if (e->dp_buf) cudaFree(e->dp_buf);
   for (auto ev : e->event_pool) cudaEventDestroy(ev);
   for (auto& p : e->pending) {
     cudaEventDestroy(p.a);
@@ -665,6 +808,11 @@ static void launch_iteration(Engine& e, int64_t run_iter, bool timed = false) {
   {
     ScopedTimer t(e, timed, "finish", run_iter);
     k_finish<<<1, kFinishThreads, 0, e.stream>>>(e.d);
+  }
+  if (e.d.dp_world > 1) {
+    ScopedTimer t(e, timed, "dp_exchange", run_iter);
+    k_dp_exchange<<<1, 32, 0, e.stream>>>(e.d);
+    e.launches += 1;
   }
 }
 
@@ -763,6 +911,10 @@ static void run(Engine& e, const ab_run_args* a, ab_run_result* r, ab_event* ev,
       msg = "sample handle " + std::to_string(c.error_handle) + " has no target length";
     else if (c.error == kErrOutOfKV)
       throw Error(AB_ERR_OUT_OF_KV, "KV page pool exhausted");
+    else if (c.error == kErrPeer)
+      throw Error(AB_ERR_NCCL, "data-parallel: a peer rank's iteration failed");
+    else if (c.error == kErrDpTimeout)
+      throw Error(AB_ERR_NCCL, "data-parallel: a peer rank's exchange record did not arrive in time");
     throw Error(AB_ERR_CONTRACT, msg);
   }
   AB_REQUIRE(c.n_events <= ev_cap || ev == nullptr, AB_ERR_CONTRACT, "event buffer too small");
@@ -843,11 +995,13 @@ static void read_payload(Engine& e, const int32_t* handles, const int32_t* start
   int32_t *dh, *ds, *dt;
   int64_t* doff;
   double* dl;
-  AB_CUDA(cudaMalloc(&dh, sizeof(int32_t) * n));
-  AB_CUDA(cudaMalloc(&ds, sizeof(int32_t) * n));
-  AB_CUDA(cudaMalloc(&doff, sizeof(int64_t) * (n + 1)));
-  AB_CUDA(cudaMalloc(&dt, sizeof(int32_t) * std::max<int64_t>(1, total)));
-  AB_CUDA(cudaMalloc(&dl, sizeof(double) * std::max<int64_t>(1, total)));
+  // stream-ordered scratch: no device-wide synchronisation (other engines of this process may be
+  // decoding on the same device)
+  AB_CUDA(cudaMallocAsync(&dh, sizeof(int32_t) * n, e.stream));
+  AB_CUDA(cudaMallocAsync(&ds, sizeof(int32_t) * n, e.stream));
+  AB_CUDA(cudaMallocAsync(&doff, sizeof(int64_t) * (n + 1), e.stream));
+  AB_CUDA(cudaMallocAsync(&dt, sizeof(int32_t) * std::max<int64_t>(1, total), e.stream));
+  AB_CUDA(cudaMallocAsync(&dl, sizeof(double) * std::max<int64_t>(1, total), e.stream));
   AB_CUDA(cudaMemcpyAsync(dh, handles, sizeof(int32_t) * n, cudaMemcpyHostToDevice, e.stream));
   AB_CUDA(cudaMemcpyAsync(ds, starts, sizeof(int32_t) * n, cudaMemcpyHostToDevice, e.stream));
   AB_CUDA(cudaMemcpyAsync(doff, offs.data(), sizeof(int64_t) * (n + 1), cudaMemcpyHostToDevice, e.stream));
@@ -856,12 +1010,12 @@ static void read_payload(Engine& e, const int32_t* handles, const int32_t* start
     if (tok) AB_CUDA(cudaMemcpyAsync(tok, dt, sizeof(int32_t) * total, cudaMemcpyDeviceToHost, e.stream));
     if (logp) AB_CUDA(cudaMemcpyAsync(logp, dl, sizeof(double) * total, cudaMemcpyDeviceToHost, e.stream));
   }
+  cudaFreeAsync(dh, e.stream);
+  cudaFreeAsync(ds, e.stream);
+  cudaFreeAsync(doff, e.stream);
+  cudaFreeAsync(dt, e.stream);
+  cudaFreeAsync(dl, e.stream);
   AB_CUDA(cudaStreamSynchronize(e.stream));
-  cudaFree(dh);
-  cudaFree(ds);
-  cudaFree(doff);
-  cudaFree(dt);
-  cudaFree(dl);
 }
 
 // Per-sample sum of the recorded behaviour log-probabilities over all generated tokens (one
@@ -890,18 +1044,18 @@ static void seq_logprob(Engine& e, const int32_t* handles, int n, double* sums, 
   for (int i = 0; i < n; ++i) AB_REQUIRE(handles[i] >= 0 && handles[i] < e.d.H, AB_ERR_CONTRACT, "handle out of range");
   int32_t *dh, *dn;
   double* ds;
-  AB_CUDA(cudaMalloc(&dh, sizeof(int32_t) * n));
-  AB_CUDA(cudaMalloc(&dn, sizeof(int32_t) * n));
-  AB_CUDA(cudaMalloc(&ds, sizeof(double) * n));
+  AB_CUDA(cudaMallocAsync(&dh, sizeof(int32_t) * n, e.stream));
+  AB_CUDA(cudaMallocAsync(&dn, sizeof(int32_t) * n, e.stream));
+  AB_CUDA(cudaMallocAsync(&ds, sizeof(double) * n, e.stream));
   AB_CUDA(cudaMemcpyAsync(dh, handles, sizeof(int32_t) * n, cudaMemcpyHostToDevice, e.stream));
   k_seq_logprob<<<ceil_div(n, 8), 256, 0, e.stream>>>(e.d, dh, n, ds, dn);
   AB_CUDA(cudaGetLastError());
   AB_CUDA(cudaMemcpyAsync(sums, ds, sizeof(double) * n, cudaMemcpyDeviceToHost, e.stream));
   AB_CUDA(cudaMemcpyAsync(lens, dn, sizeof(int32_t) * n, cudaMemcpyDeviceToHost, e.stream));
+  cudaFreeAsync(dh, e.stream);
+  cudaFreeAsync(dn, e.stream);
+  cudaFreeAsync(ds, e.stream);
   AB_CUDA(cudaStreamSynchronize(e.stream));
-  cudaFree(dh);
-  cudaFree(dn);
-  cudaFree(ds);
 }
 
 static void set_groups(Engine& e, const int32_t* pairs, int n) {
@@ -920,6 +1074,81 @@ static double read_clock(Engine& e) {
   k_read_clock<<<1, 1, 0, e.stream>>>(e.d);
   sync_ctl(e);
   return (double)(e.ctl_host->clock_ns - e.d.t0_ns) * 1e-9;
+}
+
+static void drop_graphs(Engine& e) {
+  for (auto& x : e.iter_graphs)
+    if (x) cudaGraphExecDestroy(x), x = nullptr;
+  for (auto& x : e.prof_graphs)
+    if (x) cudaGraphExecDestroy(x), x = nullptr;
+}
+
+static void dp_detach(Engine& e) {
+  AB_CUDA(cudaStreamSynchronize(e.stream));
+  for (void* p : e.dp_ipc_opened) cudaIpcCloseMemHandle(p);
+  e.dp_ipc_opened.clear();
+  if (e.dp_peers_dev) cudaFree(e.dp_peers_dev);
+  e.dp_peers_dev = nullptr;
+  e.d.dp_world = 0;
+  e.d.dp_rank = 0;
+  e.d.dp_peers = nullptr;
+  drop_graphs(e);
+}
+
+static void dp_export(Engine& e, int world, uint64_t* dev_ptr, void* ipc) {
+  AB_REQUIRE(world >= 2 && world <= 32, AB_ERR_CONFIG, "data-parallel world size must lie in [2, 32]");
+  if (e.dp_buf) {
+    dp_detach(e);
+    cudaFree(e.dp_buf);
+    e.dp_buf = nullptr;
+  }
+  const size_t bytes = sizeof(int64_t) * 2 * world * kDpRec;
+  AB_CUDA(cudaMalloc(&e.dp_buf, bytes));
+  AB_CUDA(cudaMemset(e.dp_buf, 0, bytes));
+  AB_CUDA(cudaDeviceSynchronize());
+  *dev_ptr = (uint64_t)(uintptr_t)e.dp_buf;
+  if (ipc) {
+    cudaIpcMemHandle_t h;
+    AB_CUDA(cudaIpcGetMemHandle(&h, e.dp_buf));
+    static_assert(sizeof(h) == 64, "CUDA IPC handle is 64 bytes");
+    memcpy(ipc, &h, sizeof(h));
+  }
+}
+
+static void dp_attach(Engine& e, int world, int rank, const ab_dp_peer* peers, int64_t timeout_ms) {
+  AB_REQUIRE(e.dp_buf != nullptr, AB_ERR_CONTRACT, "ab_engine_dp_export must precede ab_engine_dp_attach");
+  AB_REQUIRE(world >= 2 && world <= 32 && rank >= 0 && rank < world, AB_ERR_CONFIG, "bad data-parallel rank");
+  sync_ctl(e);
+  AB_REQUIRE(e.ctl_host->b == 0 && e.ctl_host->q_tail == e.ctl_host->q_head, AB_ERR_CONTRACT,
+             "dp_attach requires an idle engine");
+  std::vector<int64_t*> ptrs(world, nullptr);
+  for (int r = 0; r < world; ++r) {
+    if (r == rank) {
+      ptrs[r] = e.dp_buf;
+    } else if (peers[r].kind == 0) {  // same process (tests: several engines on one device)
+      ptrs[r] = (int64_t*)(uintptr_t)peers[r].ptr;
+    } else {
+      cudaIpcMemHandle_t h;
+      memcpy(&h, peers[r].ipc, sizeof(h));
+      void* p = nullptr;
+      AB_CUDA(cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess));
+      e.dp_ipc_opened.push_back(p);
+      ptrs[r] = (int64_t*)p;
+    }
+    AB_REQUIRE(ptrs[r] != nullptr, AB_ERR_CONTRACT, "null peer exchange buffer");
+  }
+  if (e.dp_peers_dev) cudaFree(e.dp_peers_dev);
+  AB_CUDA(cudaMalloc(&e.dp_peers_dev, sizeof(int64_t*) * world));
+  AB_CUDA(cudaMemcpy(e.dp_peers_dev, ptrs.data(), sizeof(int64_t*) * world, cudaMemcpyHostToDevice));
+  e.d.dp_world = world;
+  e.d.dp_rank = rank;
+  e.d.dp_peers = e.dp_peers_dev;
+  e.d.dp_local = e.dp_buf;
+  e.d.dp_timeout_ns = (uint64_t)(timeout_ms > 0 ? timeout_ms : 60000) * 1000000ull;
+  e.ctl_host->dp_epoch = 0;
+  e.ctl_host->dp_done = 0;
+  AB_CUDA(cudaMemcpy(&e.d.ctl->dp_epoch, &e.ctl_host->dp_epoch, sizeof(int64_t), cudaMemcpyHostToDevice));
+  drop_graphs(e);  // the iteration graphs now end with the exchange
 }
 
 template <typename F>
@@ -1053,10 +1282,31 @@ int ab_engine_resume_memory(ab_engine* e) {
     Engine& g = *e->impl;
     AB_REQUIRE(g.model != nullptr, AB_ERR_CONTRACT, "engine has no transformer model");
     ab::model_resume_memory(g);
-    for (auto& x : g.iter_graphs)
-      if (x) cudaGraphExecDestroy(x), x = nullptr;
-    for (auto& x : g.prof_graphs)
-      if (x) cudaGraphExecDestroy(x), x = nullptr;
+    ab::drop_graphs(g);
+  });
+}
+
+int ab_engine_dp_export(ab_engine* e, int world, uint64_t* dev_ptr, void* ipc_handle) {
+  return ab::guard([&] { ab::dp_export(*e->impl, world, dev_ptr, ipc_handle); });
+}
+
+int ab_engine_dp_attach(ab_engine* e, int world, int rank, const ab_dp_peer* peers, int64_t timeout_ms) {
+  return ab::guard([&] { ab::dp_attach(*e->impl, world, rank, peers, timeout_ms); });
+}
+
+int ab_engine_dp_detach(ab_engine* e) {
+  return ab::guard([&] { ab::dp_detach(*e->impl); });
+}
+
+int ab_engine_set_counters(ab_engine* e, int64_t iteration_index, int64_t cumulative_tokens) {
+  return ab::guard([&] {
+    Engine& g = *e->impl;
+    AB_CUDA(cudaStreamSynchronize(g.stream));
+    int64_t v[2] = {iteration_index, cumulative_tokens};
+    static_assert(offsetof(ab::Ctl, cumulative_tokens) == offsetof(ab::Ctl, iteration_index) + 8, "layout");
+    AB_CUDA(cudaMemcpy(&g.d.ctl->iteration_index, v, sizeof(v), cudaMemcpyHostToDevice));
+    g.ctl_host->iteration_index = iteration_index;
+    g.ctl_host->cumulative_tokens = cumulative_tokens;
   });
 }
 

@@ -31,9 +31,20 @@ struct Ctl {
   int64_t kv_free_top;        // transformer: free-page stack top
   int64_t kv_fail;            // transformer: allocation failures
   uint64_t clock_ns;          // scratch for clock reads
+  // data-parallel lockstep (dp_world > 1): this rank's share of the iteration, published to every
+  // peer by k_dp_exchange, and the exchange epoch (same on every rank: one exchange per global
+  // iteration)
+  int32_t dp_done;            // the global stop of this run is decided: no more exchanges
+  int32_t dp_pad;
+  int64_t dp_epoch;
+  int64_t dp_groups, dp_samples, dp_b, dp_next, dp_hint;
 };
 
-enum : int32_t { kErrNone = 0, kErrVersion = 1, kErrAtStop = 2, kErrNoTarget = 3, kErrOutOfKV = 4 };
+enum : int32_t {
+  kErrNone = 0, kErrVersion = 1, kErrAtStop = 2, kErrNoTarget = 3, kErrOutOfKV = 4,
+  kErrPeer = 5,      // data-parallel: another rank's iteration failed
+  kErrDpTimeout = 6  // data-parallel: a peer's exchange record did not arrive in time
+};
 
 struct Model;  // transformer (model.cu)
 
@@ -66,6 +77,12 @@ struct EngineDev {
   int64_t* it_ctx;     // per run iteration: sum of context lengths
   int it_cap;
   uint64_t t0_ns;
+  // data-parallel lockstep exchange: record slots [2][dp_world][8] int64 in every
+  // rank's device memory; dp_peers[r] = rank r's slots (NVLink P2P / CUDA IPC mapped)
+  int dp_world, dp_rank;
+  int64_t* const* dp_peers;
+  int64_t* dp_local;
+  uint64_t dp_timeout_ns;
 };
 
 struct KernelTimer {
@@ -120,6 +137,11 @@ struct Engine {
   };
   std::vector<PendingTime> pending;
   std::vector<cudaEvent_t> event_pool;
+
+  // data-parallel exchange buffers
+  int64_t* dp_buf = nullptr;            // this rank's record slots (exported to peers)
+  int64_t** dp_peers_dev = nullptr;     // device array of the world's slot pointers
+  std::vector<void*> dp_ipc_opened;     // peer buffers opened through CUDA IPC
 
   cudaEvent_t take_event();
   int timer_index(const char* name);

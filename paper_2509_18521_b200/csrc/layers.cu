@@ -12,6 +12,8 @@
 #include <algorithm>
 #include <cfloat>
 #include <cstdlib>
+#include <map>
+#include <mutex>
 
 #include "model.cuh"
 
@@ -773,26 +775,32 @@ void launch_rope_kv_f32(const ModelDev& m, int layer, float* qkv, const bf16* bi
                rows_dev, rows_cap, stop);
 }
 
-void launch_fork_groups(const EngineDev& e, const ModelDev& m, const ab_sample_desc* descs, int n, cudaStream_t s) {
-  static int32_t* buf = nullptr;
-  static int cap = 0;
-  if (n > cap) {
-    if (buf) cudaFree(buf);
-    cap = n + 1024;
-    AB_CUDA(cudaMalloc(&buf, sizeof(int32_t) * 2 * cap));
+// Fork metadata scratch, one per engine stream (several engines may share a process), grown
+// stream-ordered so a growth never synchronises the device.
+static int32_t* fork_scratch(cudaStream_t s, int n, int* cap_out) {
+  static std::mutex mu;
+  static std::map<cudaStream_t, std::pair<int32_t*, int>> bufs;
+  std::lock_guard<std::mutex> lock(mu);
+  auto& b = bufs[s];
+  if (n > b.second) {
+    if (b.first) AB_CUDA(cudaFreeAsync(b.first, s));
+    b.second = n + 1024;
+    AB_CUDA(cudaMallocAsync(&b.first, sizeof(int32_t) * 2 * b.second, s));
   }
+  *cap_out = b.second;
+  return b.first;
+}
+
+void launch_fork_groups(const EngineDev& e, const ModelDev& m, const ab_sample_desc* descs, int n, cudaStream_t s) {
+  int cap = 0;
+  int32_t* buf = fork_scratch(s, n, &cap);
   k_fork_meta<<<ceil_div(n, 128), 128, 0, s>>>(e, m, descs, n, buf, buf + cap);
   k_fork_copy<<<dim3(n, m.L), 256, 0, s>>>(m, buf, buf + cap);
 }
 
 void launch_resume_fork(const EngineDev& e, const ModelDev& m, const int4* items, int n, cudaStream_t s) {
-  static int32_t* buf = nullptr;
-  static int cap = 0;
-  if (n > cap) {
-    if (buf) cudaFree(buf);
-    cap = n + 1024;
-    AB_CUDA(cudaMalloc(&buf, sizeof(int32_t) * 2 * cap));
-  }
+  int cap = 0;
+  int32_t* buf = fork_scratch(s, n, &cap);
   k_resume_fork<<<ceil_div(n, 128), 128, 0, s>>>(e, m, items, n, buf, buf + cap);
   k_fork_copy<<<dim3(n, m.L), 256, 0, s>>>(m, buf, buf + cap);
 }

@@ -14,16 +14,31 @@ the same global event stream (rank-major within an iteration, slot order
 within a rank) and applies remote outcomes to its mirror of the remote
 samples.
 
-The collective is abstract (`Comm`): `TorchComm` uses torch.distributed
-(NCCL on GPUs, gloo in the CPU tests).  The per-iteration sum is issued by
-the host here; a device-side version (NCCL inside the captured iteration
-graph) is the next step.  Parity: the composed k-engine oracle
-(oracle/sim_ref.py KEngineOracle) — tests/test_dp.py runs world_size 2 over
-gloo and compares canonical step records bit for bit.
+Two lockstep implementations share the placement, mirrors and log merge:
+
+* device lockstep (`GpuLocal` after `Engine.dp_attach`, the GPU path): the
+  per-iteration sum runs on the device.  Every captured decode iteration
+  ends with `k_dp_exchange` (csrc/engine.cu), which stores this rank's
+  counts into every peer's exchange buffer over NVLink (CUDA IPC) and sums
+  the world's records, so each rank's device loop knows the global trigger,
+  drain, iteration_index and cumulative_tokens — one `ab_engine_run` per
+  scheduler call, no host round trip per iteration.
+* host lockstep (`OracleLocal`, the CPU tests): one host allreduce per
+  iteration through `Comm`.
+
+The host collectives are abstract (`Comm`): `TorchComm` uses
+torch.distributed (NCCL on GPUs, gloo in the CPU tests), `ThreadComm` joins
+several engines of one process (one thread each; the one-GPU tests).
+`gather_responses` gathers the finished responses (int32 token ids, fp64
+behaviour log-probs, lengths) to the trainer over the same collectives.
+Parity: the composed k-engine oracle (oracle/sim_ref.py KEngineOracle) —
+tests/test_dp.py (gloo, CPU) and tests/test_dp_gpu.py (device lockstep)
+compare canonical step records bit for bit.
 """
 
 from __future__ import annotations
 
+import threading
 from collections import deque
 
 from .errors import ContractViolation
@@ -64,6 +79,101 @@ class TorchComm(Comm):
         out = [None] * self.world
         self.dist.all_gather_object(out, obj, group=self.group)
         return out
+
+
+class ThreadComm(Comm):
+    """In-process collectives between `world` threads (one engine per thread)."""
+
+    class _Shared:
+        def __init__(self, world, timeout):
+            self.world = world
+            self.barrier = threading.Barrier(world, timeout=timeout)
+            self.slots = [None] * world
+
+    def __init__(self, shared: "ThreadComm._Shared", rank: int):
+        self.shared, self.rank, self.world = shared, rank, shared.world
+
+    @classmethod
+    def group(cls, world, timeout: float = 300.0):
+        sh = cls._Shared(world, timeout)
+        return [cls(sh, r) for r in range(world)]
+
+    def abort(self):
+        """Break the group's barrier (a failing thread releases the others)."""
+        self.shared.barrier.abort()
+
+    def allgather(self, obj):
+        sh = self.shared
+        sh.barrier.wait()
+        sh.slots[self.rank] = obj
+        sh.barrier.wait()
+        out = list(sh.slots)
+        sh.barrier.wait()
+        return out
+
+    def allreduce_sum(self, vals):
+        return [sum(x) for x in zip(*self.allgather(list(vals)))]
+
+
+def gather_responses(comm: Comm, samples):
+    """Finished-response gather to the trainer (once per step).
+
+    `samples` is the delivered batch (same order on every rank).  A rank owns
+    the samples it generated (every segment carries its payload; a remote
+    mirror's segments carry none).  Returns, in delivered order, (token ids,
+    behaviour log-probs) per sample.  Over `TorchComm` the payload moves as
+    three flat tensors per rank (int64 [index, length] pairs, int32 token
+    ids, fp64 log-probs) with torch.distributed all_gather — NCCL over
+    NVLink on GPUs (CUDA tensors), gloo on CPU.
+    """
+    own_idx, own_tok, own_lp = [], [], []
+    for k, s in enumerate(samples):
+        if s.segments and all(seg.tokens is not None for seg in s.segments):
+            own_idx.append(k)
+            own_tok.append(s.token_ids())
+            own_lp.append(s.behavior_logprob_trace())
+    out = [None] * len(samples)
+    if comm.world == 1 or not isinstance(comm, TorchComm):
+        parts = comm.allgather((own_idx, own_tok, own_lp))
+        for idx, tok, lp in parts:
+            for k, t, l in zip(idx, tok, lp):
+                out[k] = (t, l)
+    else:
+        torch, dist = comm.torch, comm.dist
+        dev = comm.device
+        n_own, t_own = len(own_idx), sum(len(t) for t in own_tok)
+        sizes = torch.tensor([n_own, t_own], dtype=torch.int64, device=dev)
+        all_sizes = [torch.zeros_like(sizes) for _ in range(comm.world)]
+        dist.all_gather(all_sizes, sizes, group=comm.group)
+        all_sizes = [tuple(int(x) for x in t.tolist()) for t in all_sizes]
+        max_n = max(1, max(n for n, _ in all_sizes))
+        max_t = max(1, max(t for _, t in all_sizes))
+        meta = torch.zeros(max_n, 2, dtype=torch.int64)
+        tok = torch.zeros(max_t, dtype=torch.int32)
+        lp = torch.zeros(max_t, dtype=torch.float64)
+        o = 0
+        for j, (k, t, l) in enumerate(zip(own_idx, own_tok, own_lp)):
+            meta[j, 0], meta[j, 1] = k, len(t)
+            tok[o:o + len(t)] = torch.tensor(t, dtype=torch.int32)
+            lp[o:o + len(t)] = torch.tensor(l, dtype=torch.float64)
+            o += len(t)
+        pin = str(dev).startswith("cuda")
+        bufs = []
+        for x in (meta, tok, lp):
+            x = x.pin_memory().to(dev, non_blocking=True) if pin else x
+            parts = [torch.empty_like(x) for _ in range(comm.world)]
+            dist.all_gather(parts, x, group=comm.group)
+            bufs.append([p.cpu() for p in parts])
+        for r, (n_r, _) in enumerate(all_sizes):
+            m, tk, l = bufs[0][r], bufs[1][r], bufs[2][r]
+            o = 0
+            for j in range(n_r):
+                k, ln = int(m[j, 0]), int(m[j, 1])
+                out[k] = (tk[o:o + ln].tolist(), l[o:o + ln].tolist())
+                o += ln
+    if any(x is None for x in out):
+        raise ContractViolation("finished-response gather: a delivered sample has no owner")
+    return out
 
 
 class DataParallelEngine:
@@ -162,6 +272,8 @@ class DataParallelEngine:
             self._g_size = g
         if group_done is not None:
             self._g_done = {iid: c for iid, c in group_done.items() if self.place.get(iid) == self.rank}
+        if getattr(self.local, "device_lockstep", False):
+            return self._run_device(stop_on_event, trigger, max_iters)
         G = self._g_size
         adm_log, ev_log = [], []
         live_next = self.comm.allreduce_sum([self.local.next_batch()])[0]
@@ -193,6 +305,17 @@ class DataParallelEngine:
                 break
             if max_iters and its >= max_iters:
                 break
+        return self._merge(adm_log, ev_log)
+
+    def _run_device(self, stop_on_event, trigger, max_iters):
+        """One device call: the lockstep loop with the per-iteration exchange on the GPUs."""
+        adm, evs, it, cum = self.local.run_lockstep(self.iteration_index, self.cumulative_tokens,
+                                                    stop_on_event, trigger, self._g_size, self._g_done,
+                                                    max_iters)
+        adm_log = [(i, s.instance_id, s.sample_index) for s, i in adm]
+        ev_log = [(ev.iteration, ev.sample.instance_id, ev.sample.sample_index, ev.tokens,
+                   _CODE[ev.reason]) for ev in evs]
+        self.iteration_index, self.cumulative_tokens = it, cum
         return self._merge(adm_log, ev_log)
 
     def _merge(self, adm_log, ev_log):
@@ -271,11 +394,41 @@ class OracleLocal:
 
 
 class GpuLocal:
-    """LocalAdapter over this rank's B200 engine: one device iteration per global iteration."""
+    """LocalAdapter over this rank's B200 engine.
+
+    After `attach(comm)` (device lockstep) a scheduler call is one `ab_engine_run`: the decode
+    iterations end with the peer-memory exchange, so the trigger / drain are global on the device.
+    Without it, one device iteration per global iteration with a host allreduce in between.
+    """
 
     def __init__(self, engine):
         self.e = engine
         self._queued_ids = set()
+
+    def attach(self, comm, timeout_ms: int = 60_000):
+        self.e.dp_attach(comm, timeout_ms)
+        return self
+
+    @property
+    def device_lockstep(self):
+        return self.e.dp_world > 1
+
+    def run_lockstep(self, iteration_index, cumulative_tokens, stop_on_event, trigger, g, g_done, max_iters):
+        from . import _capi as capi
+        from .engine import _TRIGGER_MODES
+
+        e = self.e
+        e.set_counters(iteration_index, cumulative_tokens)
+        e._preset_groups(g_done)
+        if trigger is not None:
+            n, g, mode, cg, cs = trigger
+            args = capi.RunArgs(use_trigger=1, trigger_mode=_TRIGGER_MODES[mode], n_target=n, group_size=g,
+                                completed_groups=cg, completed_samples=cs)
+        else:
+            args = capi.RunArgs(group_size=g, stop_on_event=int(stop_on_event), max_iters=int(max_iters))
+        evs = e._run(args, refresh=stop_on_event)
+        adm = list(zip(e.last_admitted, e.last_admit_iterations))
+        return adm, evs, e.last_run.iteration_index, e.last_run.cumulative_tokens
 
     @property
     def idle(self):

@@ -22,6 +22,7 @@ round-trip per token.
 from __future__ import annotations
 
 import ctypes as C
+import os
 from collections import deque
 from dataclasses import dataclass
 
@@ -143,6 +144,8 @@ class Engine:
         self.last_run = None
         self._h2d = self._d2h = 0  # bytes crossing PCIe through this API (bench e2e accounting)
         self.last_admitted: list = []  # admissions of the last device call, in FIFO order
+        self.last_admit_iterations: list = []  # their iteration_index (before the admitting iteration)
+        self.dp_world = 1
         if self._model_kind != capi.MODEL_CONTEXT_FREE:
             self._create()
 
@@ -322,6 +325,40 @@ class Engine:
         capi.call("ab_engine_set_iteration", self._h, int(iteration_index))
         self.iteration_index = int(iteration_index)
 
+    def set_counters(self, iteration_index: int, cumulative_tokens: int) -> None:
+        capi.call("ab_engine_set_counters", self._h, int(iteration_index), int(cumulative_tokens))
+        self.iteration_index, self.cumulative_tokens = int(iteration_index), int(cumulative_tokens)
+
+    def dp_attach(self, comm, timeout_ms: int = 60_000) -> None:
+        """Join the device-side lockstep exchange of `comm.world` engines (one per GPU).
+
+        Every rank exports its exchange buffer; the (pid, device pointer, CUDA IPC handle) triples
+        are all-gathered once; a peer in this process is attached by pointer, a peer in another
+        process through its IPC handle (NVLink P2P on one node).  After this every decode
+        iteration ends with the peer-memory exchange kernel, so `run_until_trigger` /
+        `run_until_drained` / `decode_until_event` decide trigger and drain globally on the device.
+        """
+        if comm.world < 2:
+            return
+        ptr = C.c_uint64()
+        ipc = (C.c_uint8 * 64)()
+        capi.call("ab_engine_dp_export", self._h, comm.world, C.byref(ptr), ipc)
+        mine = (os.getpid(), int(ptr.value), bytes(ipc))
+        peers_info = comm.allgather(mine)
+        peers = (capi.DpPeer * comm.world)()
+        for r, (pid, p, h) in enumerate(peers_info):
+            peers[r].ptr = p
+            peers[r].kind = 0 if pid == os.getpid() else 1
+            C.memmove(peers[r].ipc, h, 64)
+        capi.call("ab_engine_dp_attach", self._h, comm.world, comm.rank, peers, int(timeout_ms))
+        comm.allgather(None)  # every rank attached before any exchange
+        self.dp_world = comm.world
+
+    def dp_detach(self) -> None:
+        if self.dp_world > 1:
+            capi.call("ab_engine_dp_detach", self._h)
+            self.dp_world = 1
+
     def decode_iterations(self, k: int) -> list[Event]:
         """Run up to k decode iterations in one device call (stops early only if drained)."""
         return self._run(capi.RunArgs(max_iters=int(k)))
@@ -368,6 +405,7 @@ class Engine:
         out: list[Event] = []
         finished: list[RolloutSample] = []
         self.last_admitted = []
+        self.last_admit_iterations = []
         with_tokens = self._record
         while i < na or j < ne:
             # admissions of iteration k (logged with index k) precede finishes of iteration k (index k+1)
@@ -380,6 +418,7 @@ class Engine:
                 s.open_segment(self.version, with_tokens=with_tokens)
                 self._active[id(s)] = s
                 self.last_admitted.append(s)
+                self.last_admit_iterations.append(adm[i].iteration)
                 i += 1
             else:
                 e = evs[j]

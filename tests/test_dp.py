@@ -123,3 +123,54 @@ def test_k_engine_oracle_k1_is_the_single_engine():
         out = sch.run_step(k)
         recs.append(canon.step_record(sch, out, eng.event_log))
     assert recs == oracle_replay(canon.CONFIGS["C1"], "april", 6)
+
+
+def _gather_worker(rank, world, port, q):
+    sys.path.insert(0, ROOT)
+    import torch.distributed as dist
+
+    from paper_2509_18521_b200.dist import TorchComm, gather_responses
+    from paper_2509_18521_b200.rollouts import RolloutSample
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        batch = []
+        for k in range(7):  # sample k is owned by rank k % world; the others hold payload-free mirrors
+            s = RolloutSample(k, 0)
+            for v in range(1 + k % 2):
+                seg = s.open_segment(v, with_tokens=(k % world == rank))
+                seg.token_count = 2 + k + v
+                if seg.tokens is not None:
+                    seg.tokens = [100 * k + 10 * v + j for j in range(seg.token_count)]
+                    seg.behavior_logprobs = [-0.5 * j - k for j in range(seg.token_count)]
+            batch.append(s)
+        q.put((rank, gather_responses(TorchComm(), batch)))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_gather_responses_world2_gloo():
+    """Finished-response gather (tokens + log-probs + lengths) over torch.distributed, in delivered order."""
+    import torch.multiprocessing as mp
+
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_gather_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    got = dict(q.get(timeout=300) for _ in range(2))
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    want = []
+    for k in range(7):
+        toks, lps = [], []
+        for v in range(1 + k % 2):
+            n = 2 + k + v
+            toks += [100 * k + 10 * v + j for j in range(n)]
+            lps += [-0.5 * j - k for j in range(n)]
+        want.append((toks, lps))
+    assert got[0] == want and got[1] == want
