@@ -43,10 +43,29 @@ WORKLOADS = {
     # per-GPU slot count of the 8-GPU run); `--workload C3` (not the default line)
     "C3": dict(model="qwen3-4b", n=32, g=8, n_prime=64, slots=64, l_max=16384, mu=7.5, sigma=1.0, rho=0.7,
                prompt=256, temperature=0.8, adv="dapo", page=64, nondet_gemm=True),
+    # BASELINE.json configs[3] per engine: Qwen3-4B shape, GSPO, heavy long tail (L_max 16384),
+    # over-provision sweep N'/N in {1.5, 2, 3} via --over-provision (S = 64 per GPU; the rest queues)
+    "C4": dict(model="qwen3-4b", n=32, g=8, n_prime=64, slots=64, l_max=16384, mu=7.8, sigma=1.2, rho=0.7,
+               prompt=256, temperature=0.8, adv="gspo", page=64, nondet_gemm=True),
+    # BASELINE.json configs[4] per engine of 8: R1-Distill-Qwen-7B shape (untied lm_head, GQA 7:1,
+    # QKV bias), GRPO, 256 prompts x 16 over 8 GPUs = 32 x 16 per engine, N' = 2N; S = 128 rows keeps
+    # the worst-case KV (128 x 16,640 tokens x 57,344 B = 122 GB) resident next to 14.1 GB of weights
+    "C5": dict(model="r1-distill-7b", n=32, g=16, n_prime=64, slots=128, l_max=16384, mu=7.5, sigma=1.0,
+               rho=0.7, prompt=256, temperature=0.8, adv="mean_std_baseline", page=64, nondet_gemm=True),
     # small smoke workload (tiny decoder) for quick checks
     "C1": dict(model="tiny", n=8, g=4, n_prime=16, slots=64, l_max=1024, mu=5.5, sigma=1.0, rho=0.7, prompt=32,
                temperature=0.8, adv="mean_std_baseline", page=16),
 }
+
+
+ADV_NAME = {"mean_std_baseline": "GRPO", "dapo": "DAPO", "gspo": "GSPO", "mean_baseline": "REINFORCE"}
+
+
+def workload(args):
+    w = dict(WORKLOADS[args.workload])
+    if args.over_provision:  # C4 sweep: N' = round(x * N)
+        w["n_prime"] = int(round(args.over_provision * w["n"]))
+    return w
 
 
 def _peaks():
@@ -234,7 +253,7 @@ def reference_arm(args):
     from oracle.cpu_model import CpuDecoder, random_weights
 
     a = _import_reference()
-    w = WORKLOADS[args.workload]
+    w = workload(args)
     spec = pb.PRESETS[w["model"]]
     dec = CpuDecoder(spec, random_weights(spec, 0))
     batch, ctx = 64, 1024
@@ -286,6 +305,8 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--workload", default="C2", choices=sorted(WORKLOADS))
     ap.add_argument("--sync-steps", type=int, default=5)
+    ap.add_argument("--over-provision", type=float, default=None,
+                    help="N'/N (over-sampling groups over rollout groups); the workload's default otherwise")
     ap.add_argument("--no-sync", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--profile-every", type=int, default=8)
@@ -318,7 +339,7 @@ def main():
         dist.init_process_group("nccl", rank=rank, world_size=world)
     import paper_2509_18521_b200 as pb
 
-    w = WORKLOADS[args.workload]
+    w = workload(args)
     dp = (world > 1 and not args.replicas) or args.force_dp
     # data-parallel: one replicated scheduler (same seed everywhere) over lockstep engines;
     # replicas: independent prompt streams per rank
@@ -410,7 +431,7 @@ def main():
         "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "bf16", "data": "synthetic (random-init weights, Philox prompts, replayed "
                                                      "log-normal length trace)",
-        "config": {"workload": f"{args.workload}: {spec.name}-shape GRPO APRIL rollout", "prompts": w["n"],
+        "config": {"workload": f"{args.workload}: {spec.name}-shape {ADV_NAME[w['adv']]} APRIL rollout", "prompts": w["n"],
                    "samples_per_prompt": w["g"], "over_provision_groups": w["n_prime"], "max_len": w["l_max"],
                    "length_dist": f"lognormal({w['mu']}, {w['sigma']}), rho {w['rho']}",
                    "prompt_len": w["prompt"], "slots": w["slots"], "temperature": w["temperature"],
@@ -422,7 +443,9 @@ def main():
                    "l2": "inputs larger than L2 (weights + KV >> 126 MB)"},
         "april": {"tokens_per_s": value, "ms_per_step": ms_step, "steps": len(rec),
                   "iterations_per_step": statistics.mean(r["iters"] for r in rec),
-                  "carried_in_tokens_per_step": statistics.mean(r["carried"] for r in rec)},
+                  "carried_in_tokens_per_step": statistics.mean(r["carried"] for r in rec),
+                  "per_step": [{"step": r["step"], "tokens": r["tokens"], "iterations": r["iters"],
+                                "carried_in": r["carried"], "buffer_after": r["buffer"]} for r in rec]},
         "kv_resume": reprefill,
         "sync": sync,
         "april_over_sync": ((value if dp else value / world) / sync["tokens_per_s"]) if sync else None,

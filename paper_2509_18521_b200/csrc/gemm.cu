@@ -197,8 +197,13 @@ __device__ __forceinline__ float4 ld_dsmem_f4(uint32_t addr) {
 //   splits:   1, or a power of two <= the cluster size CS (cluster split-K: each group of
 //             `splits` consecutive ranks of a cluster reduces one tile, CS/splits tiles per
 //             cluster, one round).
+//   red = 1:  split-K partials reduce-added into the fp32 output by TMA (order not fixed);
+//             sk = 1 (stream-K): no fixed split count -- the grid's CTAs take equal contiguous
+//             ranges of the (tile, k-block pair) sequence, each range one or a few tile
+//             segments, so every SM streams the same bytes whatever the tile count (no partial
+//             last wave: 19,456 gate/up rows are 152 tiles on 148 SMs).
 struct Sched {
-  int swap, pair, red, wn, an, splits, m_tiles, n_tiles, tiles, units, nk, stages, stage_bytes, w_bytes;
+  int swap, pair, red, sk, wn, an, splits, m_tiles, n_tiles, tiles, units, nk, stages, stage_bytes, w_bytes;
 };
 
 __host__ __device__ inline Sched sched_from(int code, int rows, int N, int K) {
@@ -209,6 +214,7 @@ __host__ __device__ inline Sched sched_from(int code, int rows, int N, int K) {
   s.stages = (code >> 10) & 15;
   s.pair = (code >> 14) & 1;
   s.red = (code >> 15) & 1;  // split-K partials reduce-added into the fp32 output by TMA (no cluster)
+  s.sk = (code >> 16) & 1;   // stream-K ranges (with red)
   // pair: one 256 x 256 tile per CTA pair; each CTA stages 128 activation + 128 weight rows
   s.wn = s.pair ? 256 : s.swap ? kBM : t;
   s.an = s.pair ? 256 : s.swap ? t : kBM;
@@ -234,21 +240,23 @@ int choose_sched(int rows, int N, int K, int max_bn, int cs, int ncl, int force,
   const int nk = K / kBK;
   if (est_us) *est_us = 1e30;
   const int grid = cs * ncl;
-  auto pack = [&](int swap, int t, int sp, int pair = 0, int red = 0) {
+  auto pack = [&](int swap, int t, int sp, int pair = 0, int red = 0, int sk = 0) {
     int lg = 0;
     while ((1 << lg) < t) ++lg;
     const int wn = pair ? 128 : swap ? kBM : t, an = pair ? 128 : swap ? t : kBM;
     // stages carry two 64-deep k-blocks (one 3-D TMA box per operand, 8-64 KB per operation)
     const int stages = std::min(kMaxStages, kRingBytes / ((wn * kBK * 2 + an * kBK * 2) * 2));
-    return swap | (lg << 1) | (sp << 5) | (stages << 10) | (pair << 14) | (red << 15);
+    return swap | (lg << 1) | (sp << 5) | (stages << 10) | (pair << 14) | (red << 15) | (sk << 16);
   };
   if (force > 0 && (force & 0x40000000)) {  // a fixed code (tools/gemm_bench.py --sweep)
     if (force & 0x8000) {  // reduce-added split-K (fp32 residual GEMMs, cluster of 1)
       const int code = force & 0x3ff;
-      const int swap = code & 1, t = 1 << ((code >> 1) & 15), sp = (code >> 5) & 31;
-      if (cs != 1 || epi != kEpiAddF32 || sp < 1 || nk < 2 * sp || (!swap && (N % 128 || t < 128))) return 0;
+      const int sk = (force >> 16) & 1;
+      const int swap = code & 1, t = 1 << ((code >> 1) & 15), sp = sk ? 1 : (code >> 5) & 31;
+      if (cs != 1 || epi != kEpiAddF32 || sp < 1 || nk < 2 * sp || nk % 2 || (!swap && (N % 128 || t < 128)))
+        return 0;
       if (swap && (t < 32 || t > 256)) return 0;
-      return pack(swap, t, sp, 0, 1);
+      return pack(swap, t, sp, 0, 1, sk);
     }
     if (force & 0x4000) {  // CTA pair: a cluster of 2, no split
       if (!pair_plan || (epi == kEpiSwiGLU && N % 256) || N % 128 || nk % 2) return 0;
@@ -417,10 +425,18 @@ __global__ void __launch_bounds__(kThreads, 1)
   // work units: split -> one tile per rank group (one round); pair -> tiles strided over the
   // pairs; else tiles strided over the grid
   const int per_cl = split ? cs / sc.splits : pair ? cs / 2 : 1;
-  const int u_first = split ? ((int)blockIdx.x / cs) * per_cl + crank / sc.splits
+  // stream-K: this CTA's range [w0, w1) of the (tile, k-block pair) sequence = tile segments
+  // t_sk0, t_sk0 + 1, ... (units 0 .. n_units-1 of this CTA)
+  const int np_sk = sc.nk >> 1;
+  const int64_t w_all = (int64_t)sc.tiles * np_sk;
+  const int64_t w0 = sc.sk ? w_all * blockIdx.x / gridDim.x : 0, w1 = sc.sk ? w_all * (blockIdx.x + 1) / gridDim.x : 0;
+  const int t_sk0 = sc.sk ? (int)(w0 / np_sk) : 0;
+  const int u_first = sc.sk ? 0
+                      : split ? ((int)blockIdx.x / cs) * per_cl + crank / sc.splits
                       : pair ? (int)blockIdx.x / 2 : (int)blockIdx.x;
-  const int u_step = split ? ((int)gridDim.x / cs) * per_cl : pair ? (int)gridDim.x / 2 : (int)gridDim.x;
-  const int n_units = sc.units;  // tiles, or (tile, split) pairs for reduce-added split-K
+  const int u_step = sc.sk ? 1 : split ? ((int)gridDim.x / cs) * per_cl : pair ? (int)gridDim.x / 2 : (int)gridDim.x;
+  // tiles, (tile, split) pairs for reduce-added split-K, or this CTA's stream-K segments
+  const int n_units = sc.sk ? (w1 > w0 ? (int)((w1 - 1) / np_sk) - t_sk0 + 1 : 0) : sc.units;
   if ((split || pair) ? ((int)blockIdx.x / cs) * per_cl >= sc.tiles : u_first >= n_units)
     return pdl_wait();  // uniform per cluster
 
@@ -457,16 +473,24 @@ __global__ void __launch_bounds__(kThreads, 1)
   // coordinates, so results stay deterministic.
   int rot = 0, npairs = 0;
   auto unit_coords = [&](int u, int& n0, int& m0, int& kb0, int& kb1) {
-    const int z = sc.red ? u % sc.splits : rank;  // K slice
-    if (sc.red) u /= sc.splits;
+    const int np_all = sc.nk >> 1;
+    if (sc.sk) {  // segment u of this CTA's stream-K range: tile t_sk0 + u, pairs [p0, p1)
+      u += t_sk0;
+      const int64_t tb = (int64_t)u * np_all;
+      const int p0 = (int)(max(w0, tb) - tb), p1 = (int)(min(w1, tb + np_all) - tb);
+      kb0 = 2 * p0;
+      kb1 = 2 * p1;
+    } else {
+      const int z = sc.red ? u % sc.splits : rank;  // K slice
+      if (sc.red) u /= sc.splits;
+      // (32-bit arithmetic: 64-bit divisions cost ~1 us on the producer's critical path)
+      kb0 = 2 * ((np_all * z) / sc.splits);  // stages are k-block pairs
+      kb1 = 2 * ((np_all * (z + 1)) / sc.splits);
+    }
     const int nt = u / sc.m_tiles;
     const int mt = u - nt * sc.m_tiles;
     n0 = nt * sc.wn;
     m0 = mt * sc.an;
-    // (32-bit arithmetic: 64-bit divisions cost ~1 us on the producer's critical path)
-    const int np_all = sc.nk >> 1;
-    kb0 = 2 * ((np_all * z) / sc.splits);  // stages are k-block pairs
-    kb1 = 2 * ((np_all * (z + 1)) / sc.splits);
     npairs = (kb1 - kb0) >> 1;
     rot = npairs > 0 ? (mt * npairs) / sc.m_tiles : 0;
   };
@@ -1182,13 +1206,24 @@ std::vector<int> gemm_candidates(const GemmPlan& p, int rows) {
     add(0x40000000 | 0x4000);
     return out;
   }
+  const bool red = p.nondet && p.cluster == 1 && p.epi == kEpiAddF32;
   for (int swap = 1; swap >= 0; --swap)
     for (int lg = swap ? 5 : 7; lg <= 8; ++lg) {
       if (swap && (1 << lg) > std::max(p.BN, 32)) continue;
       for (int sp = 1; sp <= 8; sp <<= 1) {
         add(0x40000000 | swap | (lg << 1) | (sp << 5));
-        if (p.nondet && p.cluster == 1 && p.epi == kEpiAddF32 && sp > 1)
-          add(0x40000000 | 0x8000 | swap | (lg << 1) | (sp << 5));
+        if (red && sp > 1) add(0x40000000 | 0x8000 | swap | (lg << 1) | (sp << 5));
+      }
+      if (red) {
+        add(0x40000000 | 0x10000 | 0x8000 | swap | (lg << 1) | (1 << 5));  // stream-K ranges
+        // reduce-added splits need not be powers of two: the split counts that fill one or two
+        // whole waves of the grid (e.g. 48 QKV tiles x 3 = 144 units on 148 SMs, not 96 or 192)
+        const int wn = swap ? kBM : (1 << lg), an = swap ? (1 << lg) : kBM;
+        const int tiles = ((p.N + wn - 1) / wn) * ((rows + an - 1) / an);
+        for (int waves = 1; waves <= 2; ++waves) {
+          const int sp = tiles > 0 ? (waves * p.grid) / tiles : 0;
+          if (sp >= 2 && sp <= 24 && (sp & (sp - 1))) add(0x40000000 | 0x8000 | swap | (lg << 1) | (sp << 5));
+        }
       }
     }
   return out;

@@ -288,6 +288,40 @@ __global__ void __launch_bounds__(256) k_rmsnorm_v(const float* __restrict__ x, 
   }
 }
 
+// the GEMM's SwiGLU epilogue activation (gemm.cu silu), bit for bit
+__device__ __forceinline__ float swiglu_silu(float x) { return __fdividef(x, 1.f + __expf(-x)); }
+
+// SwiGLU over the gate-up reduce-add workspace: 128-column tile T holds gate features
+// [64T, 64T + 64) in columns [128T, 128T + 64) and the matching up features in the next 64 (the
+// interleaved weight layout).  h = bf16(silu(gate) * up), the same expression as the GEMM's SwiGLU
+// epilogue; the consumed workspace is zeroed for the next reduce-add.
+__global__ void __launch_bounds__(256) k_swiglu_ws(float* __restrict__ ws, bf16* __restrict__ h, int f,
+                                                   const int* __restrict__ sched, const int* rows_dev, int rows_cap,
+                                                   const int* stop) {
+  pdl_wait();
+  if (c_pdl_mask & 4) pdl_launch();
+  if (stopped(stop)) return;
+  const int rows = min(*rows_dev, rows_cap);
+  if (rows <= 0 || sched[rows] == 0) return;  // the workspace plan did not run at this row count
+  const int per_row = f / 4;                   // 4 features per thread
+  const int64_t n = (int64_t)rows * per_row;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const int r = (int)(i / per_row), j = (int)(i - (int64_t)r * per_row) * 4;
+    float* g = ws + (size_t)r * 2 * f + (j >> 6) * 128 + (j & 63);
+    const float4 gv = *reinterpret_cast<const float4*>(g);
+    const float4 uv = *reinterpret_cast<const float4*>(g + 64);
+    const float z[4] = {0.f, 0.f, 0.f, 0.f};
+    *reinterpret_cast<float4*>(g) = *reinterpret_cast<const float4*>(z);
+    *reinterpret_cast<float4*>(g + 64) = *reinterpret_cast<const float4*>(z);
+    const __nv_bfloat162 o01 = __floats2bfloat162_rn(swiglu_silu(gv.x) * uv.x, swiglu_silu(gv.y) * uv.y);
+    const __nv_bfloat162 o23 = __floats2bfloat162_rn(swiglu_silu(gv.z) * uv.z, swiglu_silu(gv.w) * uv.w);
+    uint2 ov;
+    ov.x = *reinterpret_cast<const uint32_t*>(&o01);
+    ov.y = *reinterpret_cast<const uint32_t*>(&o23);
+    *reinterpret_cast<uint2*>(h + (size_t)r * f + j) = ov;
+  }
+}
+
 // ---------------------------------------------------------------------------
 // q/k-norm + RoPE (rotate-half) + KV write into the row's page
 // ---------------------------------------------------------------------------
@@ -731,6 +765,18 @@ void launch_prep_decode(const EngineDev& e, const ModelDev& m, int chunk, cudaSt
 void launch_embed(const ModelDev& m, const bf16* emb, float* x, const int* rows_dev, int rows_cap, const int* stop,
                   cudaStream_t s) {
   k_embed<<<rows_cap, 128, 0, s>>>(m, emb, x, rows_dev, rows_cap, stop);
+}
+
+void launch_swiglu_ws(float* ws, bf16* h, int f, const int* sched, const int* rows_dev, int rows_cap, const int* stop,
+                      cudaStream_t s) {
+  static int grid = 0;
+  if (!grid) {
+    int dev = 0, sms = 0;
+    AB_CUDA(cudaGetDevice(&dev));
+    AB_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    grid = 2 * sms;
+  }
+  launch_pdl(k_swiglu_ws, dim3(grid), dim3(256), 0, s, ws, h, f, sched, rows_dev, rows_cap, stop);
 }
 
 void launch_rmsnorm(const float* x, const bf16* w, bf16* out, int d, float eps, const int* rows_dev, int rows_cap,

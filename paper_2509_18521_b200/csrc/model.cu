@@ -36,6 +36,9 @@ struct Model {
   size_t wbytes = 0;
   int S = 0, M_pf = 0, rows_cap = 0;
   float *x = nullptr, *logits = nullptr, *part_o = nullptr, *part_ml = nullptr;
+  float* gu_ws = nullptr;      // gate-up reduce-add workspace [S, 2f] fp32 (nondeterministic_gemm only)
+  int* samp_cnt = nullptr;     // split sampler: per-row piece arrivals (returned to 0 by the finisher)
+  uint8_t* samp_part = nullptr;  // split sampler: per-piece (max, argmax, sum) partials
   bf16 *xn = nullptr, *qkv = nullptr, *qrot = nullptr, *attn = nullptr, *hbuf = nullptr;
   float* qkv32 = nullptr;
   int max_splits = 1, chunk = 256;
@@ -165,7 +168,7 @@ static void autotune_decode(Engine& e, Model* M) {
             fprintf(stderr, "[autotune]   try N=%d K=%d rows=%d plan=%zu code=0x%x\n", g[i]->N, g[i]->K, r, i, c);
             fflush(stderr);
           }
-          const double us = gemm_time_code(*g[i], r, c, 3, flush, flush_bytes, s);
+          const double us = gemm_time_code(*g[i], r, c, 3, flush, flush_bytes, s) + g[i]->extra_us;
           if (us < best[li][i].first) best[li][i] = {us, c};
         }
     }
@@ -370,6 +373,9 @@ Model* model_create(Engine& e) {
   M->attn = dalloc<bf16>(R * m.qd);
   M->hbuf = dalloc<bf16>(R * m.f);
   M->logits = dalloc<float>((size_t)M->S * m.V);
+  if (ec.nondeterministic_gemm) M->gu_ws = dalloc<float>((size_t)M->S * 2 * m.f);  // kept zeroed between uses
+  M->samp_cnt = dalloc<int>(M->S);
+  M->samp_part = dalloc<uint8_t>(sampler_scratch_bytes(M->S, m.V));
   // smallest KV split of an attention work item (the prep kernel picks the split per iteration);
   // at most 64 splits per row
   M->chunk = std::max(256, (ceil_div(m.max_pos, 64) + 63) / 64 * 64);
@@ -472,7 +478,17 @@ Model* model_create(Engine& e) {
       const bool et = gt ? atoi(gt) != 0 : false;
       d.o.early_trigger = d.o2.early_trigger = d.down.early_trigger = d.down2.early_trigger = et;
     }
-    gemm_plan(d.gu2, w.wgu, 2 * m.f, m.d, M->xn, M->S, m.d, bn_dec, kEpiSwiGLU, M->hbuf, m.f, nullptr, b, stop, 8);
+    if (nd) {
+      // gate-up alternative: raw gate / up accumulators reduce-added into a zeroed fp32 workspace by
+      // stream-K ranges (every SM streams the same weight bytes whatever the tile count), then
+      // k_swiglu_ws forms h = silu(gate) * up and re-zeroes the workspace
+      gemm_plan(d.gu2, w.wgu, 2 * m.f, m.d, M->xn, M->S, m.d, bn_dec, kEpiAddF32, M->gu_ws, 2 * m.f, nullptr, b,
+                stop, 1);
+      d.gu2.nondet = true;
+      d.gu2.extra_us = 3.0;  // the SwiGLU pass (measured ~2-3 us at decode batches)
+    } else {
+      gemm_plan(d.gu2, w.wgu, 2 * m.f, m.d, M->xn, M->S, m.d, bn_dec, kEpiSwiGLU, M->hbuf, m.f, nullptr, b, stop, 8);
+    }
     gemm_set_table(d.gu2, std::vector<int>(M->S + 1, 0));  // idle unless the autotuner picks it
     gemm_plan(p.qkv, w.wqkv, m.qkv_dim, m.d, M->xn, M->M_pf, m.d, 256, kEpiBF16, M->qkv, m.qkv_dim, w.bqkv,
               M->pf_rows, nullptr);
@@ -522,7 +538,7 @@ void model_destroy(Model* M) {
                   M->pf_rows,  M->ga_g,     M->ga_len,    M->ga_last,  m.kv,
                   m.free_pages, m.split_prefix, m.att_counter, m.att_ctl, M->pf_blocks, M->rs_items,
                   M->rs_pieces, M->score_a, M->score_rows, M->score_idx, M->score_tgt, M->score_out,
-                  M->score_items};
+                  M->score_items, M->samp_cnt,  M->samp_part, M->gu_ws};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   if (M->host_stage) cudaFreeHost(M->host_stage);
@@ -927,12 +943,19 @@ static int pair_launches(Model* M, int variant, int j, const GemmPlan& a, const 
   return (((M->variant_sel[variant] >> j) & 1) ? b : a).idle ? 0 : 1;
 }
 
+// the gate-up workspace plan (gu2 with an fp32 output) runs in this variant: its SwiGLU pass follows
+static bool gu_ws_runs(Model* M, int variant, const Model::Plans& p) {
+  if (!M->gu_ws || p.gu2.epi != kEpiAddF32 || p.gu2.idle) return false;
+  return M->variant_sel.empty() || ((M->variant_sel[variant] >> 2) & 1);
+}
+
 // kernels one decode iteration of graph variant `variant` launches
 int64_t model_iter_launches(Model* M, int variant) {
   int64_t n = 4 + pair_launches(M, variant, 4, M->lm_dec, M->lm_dec2);  // prep, embed, final norm, sampler
   for (const auto& p : M->dec)
     n += 4 + pair_launches(M, variant, 0, p.qkv, p.qkv2) + pair_launches(M, variant, 1, p.o, p.o2) +
-         pair_launches(M, variant, 2, p.gu, p.gu2) + pair_launches(M, variant, 3, p.down, p.down2);
+         pair_launches(M, variant, 2, p.gu, p.gu2) + pair_launches(M, variant, 3, p.down, p.down2) +
+         (gu_ws_runs(M, variant, p) ? 1 : 0);
   return n;
 }
 
@@ -983,6 +1006,10 @@ void model_iteration(Engine& e, int64_t run_iter, bool timed, int variant) {
       ScopedTimer t(e, timed, "gemm_gate_up", run_iter);
       launch_pair(M, variant, 2, p.gu, p.gu2, s);
     }
+    if (gu_ws_runs(M, variant, p)) {
+      ScopedTimer t(e, timed, "swiglu", run_iter);
+      launch_swiglu_ws(M->gu_ws, M->hbuf, m.f, p.gu2.sched, b, S, stop, s);
+    }
     {
       ScopedTimer t(e, timed, "gemm_down", run_iter);
       launch_pair(M, variant, 3, p.down, p.down2, s);
@@ -998,7 +1025,7 @@ void model_iteration(Engine& e, int64_t run_iter, bool timed, int variant) {
   }
   {
     ScopedTimer t(e, timed, "sampler", run_iter);
-    launch_sampler(e.d, m, M->logits, M->inv_temp, e.cfg.greedy, e.cfg.top_p, s);
+    launch_sampler(e.d, m, M->logits, M->inv_temp, e.cfg.greedy, e.cfg.top_p, M->samp_cnt, M->samp_part, s);
   }
 }
 
@@ -1026,6 +1053,7 @@ void model_kernel_cost(Model* M, const std::string& name, double b, double sum_c
   } else if (name == "sampler") *bytes = b * V * 4;
   else if (name == "rmsnorm") *bytes = b * d * 6;
   else if (name == "rope_kv") *bytes = b * qkv * 2 + b * (qd + 2 * kvd) * 2;
+  else if (name == "swiglu") *bytes = b * 2 * f * 4 * 2 + b * f * 2;
   else if (name == "embed") *bytes = b * d * 6;
 }
 

@@ -84,8 +84,15 @@ void launch_release_handles(const EngineDev& e, const ModelDev& m, const int32_t
 void launch_group_alloc(const EngineDev& e, const ModelDev& m, const int* groups, const int* lens,
                         const int* last_tok, int n, cudaStream_t s);
 void launch_group_release(const EngineDev& e, const ModelDev& m, int group, cudaStream_t s);
+// h[r][j] = bf16(silu(g) * u) from the gate-up fp32 workspace (interleaved 64-row halves per 128
+// rows), re-zeroing it; a no-op when the plan's schedule entry for the live row count is 0
+void launch_swiglu_ws(float* ws, bf16* h, int f, const int* sched, const int* rows_dev, int rows_cap, const int* stop,
+                      cudaStream_t s);
 // sampler.cu
+// top_p = 1 or greedy: split kernel over fixed logit pieces (cnt [rows] zeroed, part
+// sampler_scratch_bytes); nucleus: one CTA per row
 void launch_sampler(const EngineDev& e, const ModelDev& m, const float* logits, float inv_temp, int greedy,
-                    float top_p, cudaStream_t s);
+                    float top_p, int* cnt, void* part, cudaStream_t s);
+size_t sampler_scratch_bytes(int rows, int V);
 
 }  // namespace ab

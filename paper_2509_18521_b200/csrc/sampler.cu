@@ -1,5 +1,13 @@
 // K1 (transformer path): fused sampler over the lm_head logits.
 //
+// Two kernels share the row rule.  `k_sample_split` (temperature / greedy, top_p = 1, the
+// decode default) splits every row into fixed 1024-logit pieces, one warp per piece, so all
+// SMs stream the logits whatever the live batch: a persistent grid of warps pulls (row, piece)
+// items, each writes its piece's (max, argmax, sum of 2^((z - max) * k2)) and the warp that
+// completes a row's last piece combines the row in fixed piece order and finishes it (draw,
+// owning-piece rescan, growth step).  Piece boundaries do not depend on the batch size, so a
+// row's result does not either.  `k_sample` below (nucleus top_p < 1) keeps one CTA per row:
+//
 // One CTA per live row.  A single pass over the row keeps, per thread and
 // for a fixed contiguous chunk of the vocabulary, an online (max, sum of
 // 2^((z - max) * invT * log2 e)) pair; a block reduction gives the row max
@@ -304,12 +312,295 @@ __global__ void __launch_bounds__(kSampThreads) k_sample_rows(const float* __res
   }
 }
 
+// ---------------------------------------------------------------------------------------------
+// split sampler (top_p = 1)
+
+constexpr int kPiece = 1024;        // logits per piece: one warp, 8 float4 per lane
+constexpr int kSplitWarps = 8;      // warps per CTA
+constexpr int kSplitCtasPerSm = 4;
+
+__device__ __forceinline__ void am_merge(float& m, int& a, float om, int oa) {
+  if (om > m || (om == m && oa < a)) {
+    m = om;
+    a = oa;
+  }
+}
+
+// The growth step of the engine (engine.py:274-289 semantics) for live row i: payload write,
+// gen += 1, stop rules (trace length, or EOS then l_max).
+__device__ __forceinline__ void grow_row(const EngineDev& e, const ModelDev& m, int i, int h, int g, int tok,
+                                        double logp) {
+  if (e.record) {
+    e.h_tokens[(size_t)h * e.L + g] = tok;
+    e.h_logp[(size_t)h * e.L + g] = logp;
+  }
+  const int g1 = g + 1;
+  e.h_gen[h] = g1;
+  m.h_ctx[h] += 1;
+  m.h_last_tok[h] = tok;
+  int reason = -1;
+  if (e.stop_mode == AB_STOP_TRACE) {
+    const int stop_at = e.h_stop[h];
+    if (g1 == stop_at) reason = stop_at >= e.l_max ? AB_REASON_MAX_LENGTH : AB_REASON_TARGET_LENGTH;
+  } else {
+    bool eos = false;
+    for (int k = 0; k < e.n_eos; ++k) eos |= (tok == e.eos[k]);
+    if (eos)
+      reason = AB_REASON_STOP_TOKEN;
+    else if (g1 >= e.l_max)
+      reason = AB_REASON_MAX_LENGTH;
+  }
+  e.slot_token[i] = tok;
+  e.slot_finish[i] = reason + 1;
+}
+
+struct SplitDebug {  // test entry: caller rows / draws / outputs instead of the engine
+  int rows;
+  const double* u;
+  int* tok;
+  double* logp;
+};
+
+// One warp combines row `row` from its P piece partials (fixed piece order: deterministic) and
+// returns the token / logp on every lane.  target = u * S selects the first index whose running
+// mass exceeds it: the owning piece is found from the piece sums, then that piece (1024 logits,
+// L2-resident) is rescanned 128 logits at a time with a warp scan.
+__device__ void split_finish_row(const float* __restrict__ z, int V, int P, const float4* __restrict__ part,
+                                 float k2, float inv_temp, int greedy, double u, int& tok, double& logp) {
+  const int lane = threadIdx.x & 31;
+  const int ppl = (P + 31) / 32;  // pieces per lane (contiguous)
+  const int p0 = min(P, lane * ppl), p1 = min(P, p0 + ppl);
+  float lm = -FLT_MAX;
+  int la = 0x7fffffff;
+  for (int p = p0; p < p1; ++p) {
+    const float4 q = __ldcg(part + p);
+    am_merge(lm, la, q.x, __float_as_int(q.y));
+  }
+  float M = lm;
+  int A = la;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) am_merge(M, A, __shfl_xor_sync(0xffffffffu, M, o), __shfl_xor_sync(0xffffffffu, A, o));
+  double mine = 0.0;
+  for (int p = p0; p < p1; ++p) {
+    const float4 q = __ldcg(part + p);
+    const double sp = __hiloint2double(__float_as_int(q.w), __float_as_int(q.z));
+    if (q.x > -FLT_MAX) mine += sp * (double)exp2f((q.x - M) * k2);
+  }
+  double incl = mine;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const double y = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += y;
+  }
+  const double S = __shfl_sync(0xffffffffu, incl, 31);
+  tok = A;
+  if (!greedy) {
+    const double target = u * S;
+    const double before = incl - mine;
+    const unsigned own = __ballot_sync(0xffffffffu, mine > 0.0 && before <= target && target < incl);
+    int piece = -1;
+    double base = 0.0;
+    if (own) {
+      const int ol = __ffs(own) - 1;
+      if (lane == ol) {
+        double run = before;
+        for (int p = p0; p < p1; ++p) {
+          const float4 q = __ldcg(part + p);
+          const double sp = __hiloint2double(__float_as_int(q.w), __float_as_int(q.z));
+          const double add = q.x > -FLT_MAX ? sp * (double)exp2f((q.x - M) * k2) : 0.0;
+          if (add > 0.0) {  // (rounding: the last massive piece of the lane)
+            piece = p;
+            base = run;
+          }
+          if (add > 0.0 && run + add > target) break;
+          run += add;
+        }
+      }
+      piece = __shfl_sync(0xffffffffu, piece, ol);
+      base = __shfl_sync(0xffffffffu, base, ol);
+    }
+    int found = -1, last = -1;
+    if (piece >= 0) {
+      const int j0 = piece * kPiece, j1 = min(V, j0 + kPiece);
+      for (int t0 = j0; t0 < j1 && found < 0; t0 += 128) {
+        const int j = t0 + 4 * lane;
+        float x[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) x[q] = j + q < j1 ? __ldcg(z + j + q) : -FLT_MAX;
+        double pl[4], ls = 0.0;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          pl[q] = x[q] > -FLT_MAX ? (double)exp2f((x[q] - M) * k2) : 0.0;
+          ls += pl[q];
+        }
+        double li = ls;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const double y = __shfl_up_sync(0xffffffffu, li, o);
+          if (lane >= o) li += y;
+        }
+        const double lb = base + li - ls;
+        const unsigned hit = __ballot_sync(0xffffffffu, ls > 0.0 && base + li > target);
+        const unsigned mass = __ballot_sync(0xffffffffu, ls > 0.0);
+        if (mass) {  // last index with mass so far (fallback when u * S rounds past the piece)
+          const int hl = 31 - __clz(mass);
+          int lq = -1;
+          if (lane == hl)
+            for (int q = 0; q < 4; ++q)
+              if (pl[q] > 0.0) lq = j + q;
+          last = __shfl_sync(0xffffffffu, lq, hl);
+        }
+        if (hit) {
+          const int hl = __ffs(hit) - 1;
+          int fq = -1;
+          if (lane == hl) {
+            double run = lb;
+            for (int q = 0; q < 4; ++q) {
+              run += pl[q];
+              if (pl[q] > 0.0 && run > target) {
+                fq = j + q;
+                break;
+              }
+              if (pl[q] > 0.0) fq = j + q;  // (rounding: last massive index of the lane)
+            }
+          }
+          found = __shfl_sync(0xffffffffu, fq, hl);
+        }
+        base = __shfl_sync(0xffffffffu, base + li, 31);
+      }
+      if (found < 0) found = last;
+    }
+    if (found < 0) {  // u * S rounded past every piece: the last token with mass
+      int t = V - 1;
+      while (t > 0 && z[t] == -FLT_MAX) --t;
+      found = t;
+    }
+    tok = found;
+  }
+  logp = (double)((__ldcg(z + tok) - M) * inv_temp) - log2(S) * kLn2;
+}
+
+__global__ void __launch_bounds__(kSplitWarps * 32, kSplitCtasPerSm)
+    k_sample_split(EngineDev e, ModelDev m, const float* __restrict__ logits, int V, float inv_temp, int greedy,
+                   int* __restrict__ cnt, float4* __restrict__ part, SplitDebug dbg) {
+  pdl_wait();
+  int b;
+  if (dbg.tok) {
+    b = dbg.rows;
+  } else {
+    const Ctl* c = e.ctl;
+    if (c->stop) return;
+    b = c->b;
+  }
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int P = (V + kPiece - 1) / kPiece;
+  const float k2 = inv_temp * kLog2e;
+  const int64_t items = (int64_t)b * P;
+  for (int64_t it = (int64_t)blockIdx.x * kSplitWarps + w; it < items; it += (int64_t)gridDim.x * kSplitWarps) {
+    const int row = (int)(it / P), piece = (int)(it - (int64_t)row * P);
+    const float* z = logits + (size_t)row * V;
+    const int j0 = piece * kPiece, j1 = min(V, j0 + kPiece);
+    float x[32];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      const int j = j0 + 4 * (lane + 32 * k);
+      if (j + 4 <= j1) {
+        const float4 v = __ldg(reinterpret_cast<const float4*>(z + j));
+        x[4 * k] = v.x;
+        x[4 * k + 1] = v.y;
+        x[4 * k + 2] = v.z;
+        x[4 * k + 3] = v.w;
+      } else {
+#pragma unroll
+        for (int q = 0; q < 4; ++q) x[4 * k + q] = j + q < j1 ? z[j + q] : -FLT_MAX;
+      }
+    }
+    float mx = -FLT_MAX;
+    int am = 0x7fffffff;
+#pragma unroll
+    for (int k = 0; k < 8; ++k)
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int j = j0 + 4 * (lane + 32 * k) + q;
+        if (x[4 * k + q] > mx) {  // strictly greater: the lowest index of a lane wins ties
+          mx = x[4 * k + q];
+          am = j;
+        }
+      }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) am_merge(mx, am, __shfl_xor_sync(0xffffffffu, mx, o), __shfl_xor_sync(0xffffffffu, am, o));
+    double sum = 0.0;
+    if (mx > -FLT_MAX) {
+#pragma unroll
+      for (int k = 0; k < 32; ++k)
+        if (x[k] > -FLT_MAX) sum += (double)exp2f((x[k] - mx) * k2);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
+    int done = 0;
+    if (lane == 0) {
+      part[(size_t)row * P + piece] =
+          make_float4(mx, __int_as_float(am), __int_as_float(__double2loint(sum)), __int_as_float(__double2hiint(sum)));
+      __threadfence();
+      done = atomicAdd(&cnt[row], 1) == P - 1;
+    }
+    done = __shfl_sync(0xffffffffu, done, 0);
+    if (!done) continue;
+    // this warp completed the row: combine and finish it
+    __threadfence();
+    if (lane == 0) cnt[row] = 0;
+    double u = 0.0;
+    int h = -1, g = 0;
+    if (dbg.tok) {
+      u = dbg.u[row];
+    } else {
+      h = e.slot_handle[row];
+      g = e.h_gen[h];
+      if (!greedy) {
+        const ulonglong2 key = e.h_key[h];
+        u = philox_uniform(key.x, key.y, (uint64_t)g);
+      }
+    }
+    int tok;
+    double logp;
+    split_finish_row(z, V, P, part + (size_t)row * P, k2, inv_temp, greedy, u, tok, logp);
+    if (lane != 0) continue;
+    if (dbg.tok) {
+      dbg.tok[row] = tok;
+      dbg.logp[row] = logp;
+    } else {
+      grow_row(e, m, row, h, g, tok, logp);
+    }
+  }
+}
+
+int split_grid() {
+  static int grid = 0;
+  if (!grid) {
+    int dev = 0, sms = 0;
+    AB_CUDA(cudaGetDevice(&dev));
+    AB_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    grid = sms * kSplitCtasPerSm;
+  }
+  return grid;
+}
+
 }  // namespace
 
+size_t sampler_scratch_bytes(int rows, int V) { return (size_t)rows * ((V + kPiece - 1) / kPiece) * sizeof(float4); }
+
+bool sampler_uses_split(int greedy, float top_p) { return greedy || top_p >= 1.f; }
+
 void launch_sampler(const EngineDev& e, const ModelDev& m, const float* logits, float inv_temp, int greedy,
-                    float top_p, cudaStream_t s) {
+                    float top_p, int* cnt, void* part, cudaStream_t s) {
   AB_REQUIRE(top_p > 0.f && top_p <= 1.f, AB_ERR_CONFIG, "top_p must lie in (0, 1]");
-  launch_pdl(k_sample, dim3(e.S), dim3(kSampThreads), 0, s, e, m, logits, inv_temp, greedy, top_p);
+  if (sampler_uses_split(greedy, top_p)) {
+    SplitDebug no{0, nullptr, nullptr, nullptr};
+    launch_pdl(k_sample_split, dim3(split_grid()), dim3(kSplitWarps * 32), 0, s, e, m, logits, m.V, inv_temp, greedy,
+               cnt, (float4*)part, no);
+  } else {
+    launch_pdl(k_sample, dim3(e.S), dim3(kSampThreads), 0, s, e, m, logits, inv_temp, greedy, top_p);
+  }
 }
 
 }  // namespace ab
@@ -321,9 +612,28 @@ extern "C" int ab_debug_sample_rows(const float* logits, int rows, int V, float 
   try {
     AB_REQUIRE(top_p > 0.f && top_p <= 1.f, AB_ERR_CONFIG, "top_p must lie in (0, 1]");
     const float inv_temp = temperature > 0.f ? 1.f / temperature : 1.f;
-    ab::k_sample_rows<<<rows, ab::kSampThreads>>>(logits, V, inv_temp, greedy, top_p, u, tok, logp);
-    AB_CUDA(cudaGetLastError());
-    AB_CUDA(cudaDeviceSynchronize());
+    if (rows <= 0) return AB_OK;
+    if (ab::sampler_uses_split(greedy, top_p)) {
+      // the decode path's split kernel (fixed 1024-logit pieces) on caller rows
+      int* cnt = nullptr;
+      void* part = nullptr;
+      AB_CUDA(cudaMalloc(&cnt, sizeof(int) * rows));
+      AB_CUDA(cudaMemset(cnt, 0, sizeof(int) * rows));
+      AB_CUDA(cudaMalloc(&part, ab::sampler_scratch_bytes(rows, V)));
+      ab::SplitDebug dbg{rows, u, tok, logp};
+      ab::EngineDev e{};
+      ab::ModelDev m{};
+      ab::k_sample_split<<<ab::split_grid(), ab::kSplitWarps * 32>>>(e, m, logits, V, inv_temp, greedy, cnt,
+                                                                     (float4*)part, dbg);
+      AB_CUDA(cudaGetLastError());
+      AB_CUDA(cudaDeviceSynchronize());
+      cudaFree(cnt);
+      cudaFree(part);
+    } else {
+      ab::k_sample_rows<<<rows, ab::kSampThreads>>>(logits, V, inv_temp, greedy, top_p, u, tok, logp);
+      AB_CUDA(cudaGetLastError());
+      AB_CUDA(cudaDeviceSynchronize());
+    }
     return AB_OK;
   } catch (const ab::Error& e) {
     ab::set_last_error(e.what());

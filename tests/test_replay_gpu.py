@@ -36,7 +36,9 @@ def test_fused_replay_matches_reference(name, mode):
 
 @pytest.mark.parametrize("name", ["C1", "E_samples", "E_pool"])
 def test_event_path_replay_matches_reference(name):
-    """The reference's own per-event loop (decode_until_event) over the GPU engine."""
+    """The build's Scheduler in per-event mode (`_fused=False`: the reference's loop shape, one
+    decode_until_event per finish, scheduler.py:272-283) over the GPU engine.  The reference's OWN
+    Scheduler driving the GPU engine is tests/test_reference_drives_gpu.py."""
     g = goldens.replay(name, "april")
     recs, _ = product_replay(canon.CONFIGS[name], "april", len(g["records"]), fused=False)
     for mine, ref in zip(recs, g["records"]):

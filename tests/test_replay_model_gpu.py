@@ -95,3 +95,17 @@ def test_model_on_delivered_payload_matches_token_counts():
             multi += len(s.segments) > 1
     assert multi > 0, "no delivered sample spanned a resume"
     sched.engine.close()
+
+
+@pytest.mark.parametrize("name,preset,layers", [("C4_1.5", "qwen3-4b", 1), ("C4_3", "qwen3-4b", 1),
+                                                ("C5", "r1-distill-7b", 1)])
+def test_c4_c5_shape_model_replay_matches_reference_digests(name, preset, layers):
+    """C4 (GSPO-sized heavy tail, L_max 16384, N'/N = 1.5 and 3 at S = 64: the queued surplus returns
+    to the pool) and C5 (256 x 16 samples per step at S = 1024; untied lm_head, GQA 7:1, QKV bias) with
+    the model ON (depth cut so the reference config's KV fits one GPU); trace mode, so the decisions
+    must equal the reference goldens' digests."""
+    dg = goldens.digests()[f"{name}/april"]
+    spec = pb.PRESETS[preset].truncated(layers)
+    recs, sched = product_replay(canon.CONFIGS[name], "april", len(dg), **_model_kw(spec, "reprefill", True))
+    assert [canon.digest(r) for r in recs] == dg
+    sched.engine.close()

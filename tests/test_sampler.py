@@ -50,14 +50,19 @@ def test_oracle_reduces_to_reference_rule_at_t1_p1():
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("V", [1000, 151936])
+@pytest.mark.parametrize("V", [1000, 4097, 151936, 152064])
 @pytest.mark.parametrize("T,top_p,greedy", [(0.8, 1.0, False), (0.8, 0.9, False), (1.0, 0.5, False),
-                                            (0.6, 0.95, False), (0.8, 0.9, True)])
-def test_sampler_kernel_matches_oracle(V, T, top_p, greedy):
+                                            (0.6, 0.95, False), (0.8, 0.9, True), (1.0, 1.0, False),
+                                            (0.8, 1.0, True)])
+@pytest.mark.parametrize("rows", [48, 333])
+def test_sampler_kernel_matches_oracle(V, T, top_p, greedy, rows):
+    """top_p = 1 / greedy run the split kernel (fixed 1024-logit pieces, several per row, rows
+    spread over a persistent grid); nucleus runs the one-CTA-per-row kernel."""
     torch = pytest.importorskip("torch")
     from paper_2509_18521_b200 import _capi
 
-    rows = 48
+    if rows > 48 and top_p < 1.0 and not greedy:
+        pytest.skip("nucleus kernel: one CTA per row, covered at 48 rows")
     g = torch.Generator().manual_seed(V + int(top_p * 100))
     z = (torch.randn(rows, V, generator=g) * 2.5).float()
     u = torch.rand(rows, generator=g, dtype=torch.float64)

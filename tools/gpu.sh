@@ -8,6 +8,7 @@
 #   launches B CTX [preset]  ncu launch list (gpu__time_duration) of decode iterations at (batch, ctx)
 #   ncu_attn B CTX           ncu --set full of the decode attention kernel
 #   sanitize                 compute-sanitizer racecheck + memcheck on the engine / attention tests
+#   forcedp [bench args]     plain vs --force-dp (world-1 lockstep wrapper) decisions, compared
 set -u
 mkdir -p gpurun_out
 export AB_TEST_REPORT_DIR=gpurun_out/test_reports
@@ -37,15 +38,21 @@ case "$MODE" in
     bash tools/gpu_ncu_attn.sh "$@" ;;
   sanitize)
     for tool in racecheck memcheck; do
-      timeout 1800 compute-sanitizer --tool $tool --error-exitcode 9 python -m pytest -q -x -p no:cacheprovider \
+      timeout 900 compute-sanitizer --tool $tool --error-exitcode 9 python -m pytest -q -x -p no:cacheprovider \
         -m gpu tests/test_attention_gpu.py -k "b64 and c3 and page64 or mixed7 and c5" \
         > gpurun_out/sanitize_${tool}_attention.log 2>&1
       echo "rc=$?" >> gpurun_out/sanitize_${tool}_attention.log
-      timeout 1800 compute-sanitizer --tool $tool --error-exitcode 9 python -m pytest -q -x -p no:cacheprovider \
+      timeout 900 compute-sanitizer --tool $tool --error-exitcode 9 python -m pytest -q -x -p no:cacheprovider \
         -m gpu tests/test_engine_gpu.py tests/test_replay_model_gpu.py -k "c1_tiny and april and reprefill or exactly_once or advantages" \
         > gpurun_out/sanitize_${tool}_engine.log 2>&1
       echo "rc=$?" >> gpurun_out/sanitize_${tool}_engine.log
     done
     tail -3 gpurun_out/sanitize_*.log ;;
+  forcedp)
+    # the lockstep DP wrapper at world 1 must make the plain engine's decisions (same iterations and
+    # carried tokens per step): two short bench runs, decisions compared by tools/compare_forcedp.py
+    timeout 1200 python bench.py --steps 3 --warmup 2 --no-sync --no-cpu "$@" > gpurun_out/forcedp_plain.log 2>&1
+    timeout 1200 python bench.py --steps 3 --warmup 2 --no-sync --no-cpu --force-dp "$@" > gpurun_out/forcedp_dp.log 2>&1
+    python tools/compare_forcedp.py gpurun_out/forcedp_plain.log gpurun_out/forcedp_dp.log | tee gpurun_out/forcedp_compare.txt ;;
   *) echo "unknown mode $MODE"; exit 2 ;;
 esac
