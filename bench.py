@@ -120,13 +120,14 @@ class ClockSampler:
                 "reasons": reasons, "samples": len(self.rows)}
 
 
-def build_engine(pb, w, device, seed, record=True, kv_resume="retain"):
+def build_engine(pb, w, device, seed, record=True, kv_resume="retain", kv_pages=0):
     spec = pb.PRESETS[w["model"]]
     eng = pb.LengthDrivenEngine(
         pb.EngineConfig(max_slots=w["slots"], l_max=w["l_max"]), global_seed=seed, model=spec,
         sampling=pb.SamplingConfig(temperature=w["temperature"]), prompt_len=w["prompt"], page_size=w["page"],
         device=device, record_payload=record, max_handles=max(4096, 4 * w["n_prime"] * w["g"]),
-        max_groups=4 * w["n_prime"] + 64, nondeterministic_gemm=w.get("nondet_gemm", False), kv_resume=kv_resume)
+        max_groups=4 * w["n_prime"] + 64, nondeterministic_gemm=w.get("nondet_gemm", False), kv_resume=kv_resume,
+        kv_pages=kv_pages)
     return spec, eng
 
 
@@ -319,6 +320,7 @@ def main():
                     help="paused partials: re-prefill prompt + carried tokens at resume (the cost APRIL pays when "
                          "weights change every step; inside the rollout wall time) or keep their KV resident")
     ap.add_argument("--force-dp", action="store_true", help="run the data-parallel engine even at N = 1 (tests)")
+    ap.add_argument("--kv-pages", type=int, default=0, help="KV pool pages (0: all HBM left after a margin)")
     ap.add_argument("--replicas", action="store_true",
                     help="N > 1: independent engine replicas instead of the lockstep data-parallel engine")
     args = ap.parse_args()
@@ -328,6 +330,11 @@ def main():
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # test hooks: AB_BENCH_DEVICE pins every rank to one GPU and AB_BENCH_BACKEND=gloo runs the host
+    # collectives on the CPU (a world-2 smoke test of the multi-rank path on a one-GPU box; the
+    # per-iteration exchange still runs on the device through CUDA IPC)
+    local = int(os.environ.get("AB_BENCH_DEVICE", local))
+    backend = os.environ.get("AB_BENCH_BACKEND", "nccl")
     dist = None
     if world > 1 or args.force_dp:
         import torch
@@ -336,7 +343,7 @@ def main():
         torch.cuda.set_device(local)
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
         os.environ.setdefault("MASTER_PORT", "29531")
-        dist.init_process_group("nccl", rank=rank, world_size=world)
+        dist.init_process_group(backend, rank=rank, world_size=world)
     import paper_2509_18521_b200 as pb
 
     w = workload(args)
@@ -346,13 +353,13 @@ def main():
     seed = args.seed if dp else args.seed + rank
     hbm_peak, tf_peak, peak_kind = _peaks()
 
-    spec, eng = build_engine(pb, w, local, seed, record=True, kv_resume=args.kv_resume)
+    spec, eng = build_engine(pb, w, local, seed, record=True, kv_resume=args.kv_resume, kv_pages=args.kv_pages)
     comm = None
     front = eng  # what the scheduler drives
     if dp:
         from paper_2509_18521_b200.dist import DataParallelEngine, GpuLocal, TorchComm
 
-        comm = TorchComm(device=f"cuda:{local}")
+        comm = TorchComm(device=f"cuda:{local}" if backend == "nccl" else "cpu")
         # device lockstep: the per-iteration count exchange runs over NVLink peer memory inside
         # the captured iteration graph (no host round trip per iteration)
         front = DataParallelEngine(GpuLocal(eng).attach(comm), comm, w["slots"])
@@ -372,7 +379,7 @@ def main():
         if dist:
             import torch
 
-            tt = torch.tensor([t_dev], device="cuda")
+            tt = torch.tensor([t_dev], device="cuda" if backend == "nccl" else "cpu")
             dist.all_reduce(tt, op=dist.ReduceOp.MAX)
             t_dev = float(tt)
         t_host = time.perf_counter() - t0
@@ -393,7 +400,7 @@ def main():
 
     sync = None
     if not args.no_sync:
-        _, eng_s = build_engine(pb, w, local, seed, record=True)
+        _, eng_s = build_engine(pb, w, local, seed, record=True, kv_pages=args.kv_pages)
         front_s = eng_s
         if dp:
             front_s = DataParallelEngine(GpuLocal(eng_s).attach(comm), comm, w["slots"])
@@ -414,10 +421,12 @@ def main():
     roof = None
     if att and att["ms"] > 0:
         ach = att["bytes"] / (att["ms"] * 1e-3) / 1e9
+        traffic, tpoint = _ncu_traffic(args.workload)
         roof = {"kernel": "paged GQA decode attention (k_decode_attn + combine)", "bound": "hbm",
                 "achieved": ach, "peak": hbm_peak, "unit": "GB/s", "frac": ach / hbm_peak,
-                "peak_kind": peak_kind, "traffic": _ncu_traffic(args.workload), "launches_timed": att["launches"],
-                "avg_launch_us": 1e3 * att["ms"] / att["launches"]}
+                "peak_kind": peak_kind, "traffic": traffic, "traffic_at": tpoint, "launches_timed": att["launches"],
+                "avg_launch_us": 1e3 * att["ms"] / att["launches"],
+                "avg_algorithmic_bytes_per_launch": att["bytes"] / max(att["launches"], 1)}
     kern = {}
     tot_ms = sum(k["ms"] for k in kstats.values()) or 1.0
     for name, k in sorted(kstats.items(), key=lambda kv: -kv[1]["ms"]):
@@ -499,15 +508,20 @@ def write_outputs(pb, w, args, rec_april, rec_sync, world):
 
 
 def _ncu_traffic(workload):
-    """dram read+write bytes per launch of the attention kernel from the committed ncu capture
-    (taken at the C2 decode microbench point; other workloads have no capture -> null)."""
+    """DRAM read+write bytes per launch of the attention kernel from the committed ncu capture
+    (profiles/attention_dram_bytes.json, tools/ncu_attn_point.py) and the operating point it was
+    taken at (the bench's average live batch and context for C2); other workloads -> null."""
     p = os.path.join(ROOT, "profiles", "attention_dram_bytes.json")
     try:
         with open(p) as f:
             d = json.load(f)
-        return d.get("bytes_per_launch") if d.get("workload", "C2") == workload else None
+        if d.get("workload", "C2") != workload:
+            return None, None
+        return d.get("bytes_per_launch"), {"point": d.get("point"),
+                                           "algorithmic_bytes_per_launch": d.get("algorithmic_bytes_per_launch"),
+                                           "source": "profiles/attention_dram_bytes.json"}
     except Exception:
-        return None
+        return None, None
 
 
 if __name__ == "__main__":

@@ -886,9 +886,12 @@ static void run(Engine& e, const ab_run_args* a, ab_run_result* r, ab_event* ev,
       const int bmax = (int)std::min<int64_t>(e.d.S, (int64_t)c0.b + (c0.q_tail - c0.q_head));
       e.variant = model_variant_for(e.model, bmax);
     }
-    for (int i = 0; i < n; ++i) launch_iteration_fast(e, launched + i, i == 0);
-    launched += n;
-    sync_ctl(e);
+    {
+      NvtxRange r("april.chunk");
+      for (int i = 0; i < n; ++i) launch_iteration_fast(e, launched + i, i == 0);
+      launched += n;
+      sync_ctl(e);
+    }
     collect_prof(e);
     const Ctl& c = *e.ctl_host;
     if (c.stop) break;
@@ -1196,10 +1199,12 @@ int ab_engine_destroy(ab_engine* e) {
 }
 
 int ab_engine_begin_step(ab_engine* e, int64_t version, const double* cf_logits) {
+  ab::NvtxRange nvtx("april.begin_step");
   return ab::guard([&] { ab::begin_step(*e->impl, version, cf_logits); });
 }
 
 int ab_engine_submit(ab_engine* e, const ab_sample_desc* descs, int n) {
+  ab::NvtxRange nvtx("april.submit");
   return ab::guard([&] { ab::submit(*e->impl, descs, n); });
 }
 
@@ -1209,10 +1214,12 @@ int ab_engine_set_group_done(ab_engine* e, const int32_t* slot_count_pairs, int 
 
 int ab_engine_run(ab_engine* e, const ab_run_args* args, ab_run_result* res, ab_event* events, int event_cap,
                   ab_admit* admits, int admit_cap) {
+  ab::NvtxRange nvtx("april.run");
   return ab::guard([&] { ab::run(*e->impl, args, res, events, event_cap, admits, admit_cap); });
 }
 
 int ab_engine_abort(ab_engine* e, int32_t* handles, int32_t* gen, int cap, int* n_active, int* n_queued) {
+  ab::NvtxRange nvtx("april.abort");
   return ab::guard([&] { ab::abort_active(*e->impl, handles, gen, cap, n_active, n_queued); });
 }
 
@@ -1222,15 +1229,18 @@ int ab_engine_active(ab_engine* e, int32_t* handles, int32_t* gen, int cap, int*
 
 int ab_engine_read_payload(ab_engine* e, const int32_t* handles, const int32_t* starts, const int32_t* counts, int n,
                            int32_t* tokens, double* logprobs) {
+  ab::NvtxRange nvtx("april.read_payload");
   return ab::guard([&] { ab::read_payload(*e->impl, handles, starts, counts, n, tokens, logprobs); });
 }
 
 int ab_engine_sequence_logprobs(ab_engine* e, const int32_t* handles, int n, double* sums, int32_t* lens) {
+  ab::NvtxRange nvtx("april.sequence_logprobs");
   return ab::guard([&] { ab::seq_logprob(*e->impl, handles, n, sums, lens); });
 }
 
 int ab_engine_score(ab_engine* e, const int32_t* tokens, const int64_t* offs, const int32_t* prompt_lens, int n,
                     double* logprobs) {
+  ab::NvtxRange nvtx("april.score");
   return ab::guard([&] {
     Engine& g = *e->impl;
     AB_REQUIRE(g.model != nullptr, AB_ERR_CONTRACT, "scoring needs the transformer model");
@@ -1253,6 +1263,7 @@ int ab_engine_release(ab_engine* e, const int32_t* handles, int n) {
 }
 
 int ab_engine_open_group(ab_engine* e, int32_t group_slot, const int32_t* prompt, int32_t prompt_len) {
+  ab::NvtxRange nvtx("april.open_group");
   return ab::guard([&] {
     Engine& g = *e->impl;
     AB_REQUIRE(group_slot >= 0 && group_slot < g.d.G_cap, AB_ERR_CONTRACT, "group slot out of range");
@@ -1266,6 +1277,7 @@ int ab_engine_open_group(ab_engine* e, int32_t group_slot, const int32_t* prompt
 // is recomputed by the next submit.  The captured iteration graphs embed the pool address and are
 // re-captured.
 int ab_engine_release_memory(ab_engine* e) {
+  ab::NvtxRange nvtx("april.release_memory");
   return ab::guard([&] {
     Engine& g = *e->impl;
     AB_REQUIRE(g.model != nullptr, AB_ERR_CONTRACT, "engine has no transformer model");
@@ -1278,6 +1290,7 @@ int ab_engine_release_memory(ab_engine* e) {
 }
 
 int ab_engine_resume_memory(ab_engine* e) {
+  ab::NvtxRange nvtx("april.resume_memory");
   return ab::guard([&] {
     Engine& g = *e->impl;
     AB_REQUIRE(g.model != nullptr, AB_ERR_CONTRACT, "engine has no transformer model");
@@ -1291,6 +1304,7 @@ int ab_engine_dp_export(ab_engine* e, int world, uint64_t* dev_ptr, void* ipc_ha
 }
 
 int ab_engine_dp_attach(ab_engine* e, int world, int rank, const ab_dp_peer* peers, int64_t timeout_ms) {
+  ab::NvtxRange nvtx("april.dp_attach");
   return ab::guard([&] { ab::dp_attach(*e->impl, world, rank, peers, timeout_ms); });
 }
 

@@ -7,9 +7,20 @@
 #include <string>
 #include <vector>
 
+#include <nvtx3/nvToolsExt.h>
+
 #include "common.cuh"
 
 namespace ab {
+
+// NVTX range around a C-ABI call / engine phase (nsys / ncu --nvtx timelines; header-only NVTX3,
+// a no-op unless a tool is attached)
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+  NvtxRange(const NvtxRange&) = delete;
+  NvtxRange& operator=(const NvtxRange&) = delete;
+};
 
 // Device control block: one per engine, lives in device memory; copied to a
 // pinned mirror at the host's polling points.

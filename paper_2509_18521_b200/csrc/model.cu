@@ -37,8 +37,8 @@ struct Model {
   int S = 0, M_pf = 0, rows_cap = 0;
   float *x = nullptr, *logits = nullptr, *part_o = nullptr, *part_ml = nullptr;
   float* gu_ws = nullptr;      // gate-up reduce-add workspace [S, 2f] fp32 (nondeterministic_gemm only)
-  int* samp_cnt = nullptr;     // split sampler: per-row piece arrivals (returned to 0 by the finisher)
   uint8_t* samp_part = nullptr;  // split sampler: per-piece (max, argmax, sum) partials
+  bool samp_split = false;       // the sampler runs as two kernels (pieces + finish)
   bf16 *xn = nullptr, *qkv = nullptr, *qrot = nullptr, *attn = nullptr, *hbuf = nullptr;
   float* qkv32 = nullptr;
   int max_splits = 1, chunk = 256;
@@ -374,8 +374,8 @@ Model* model_create(Engine& e) {
   M->hbuf = dalloc<bf16>(R * m.f);
   M->logits = dalloc<float>((size_t)M->S * m.V);
   if (ec.nondeterministic_gemm) M->gu_ws = dalloc<float>((size_t)M->S * 2 * m.f);  // kept zeroed between uses
-  M->samp_cnt = dalloc<int>(M->S);
   M->samp_part = dalloc<uint8_t>(sampler_scratch_bytes(M->S, m.V));
+  M->samp_split = sampler_uses_split(ec.greedy, ec.top_p);
   // smallest KV split of an attention work item (the prep kernel picks the split per iteration);
   // at most 64 splits per row
   M->chunk = std::max(256, (ceil_div(m.max_pos, 64) + 63) / 64 * 64);
@@ -538,7 +538,7 @@ void model_destroy(Model* M) {
                   M->pf_rows,  M->ga_g,     M->ga_len,    M->ga_last,  m.kv,
                   m.free_pages, m.split_prefix, m.att_counter, m.att_ctl, M->pf_blocks, M->rs_items,
                   M->rs_pieces, M->score_a, M->score_rows, M->score_idx, M->score_tgt, M->score_out,
-                  M->score_items, M->samp_cnt,  M->samp_part, M->gu_ws};
+                  M->score_items, M->samp_part, M->gu_ws};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   if (M->host_stage) cudaFreeHost(M->host_stage);
@@ -888,13 +888,17 @@ void model_submit(Engine& e, const ab_sample_desc* descs_dev, int n) {
   const auto t0 = std::chrono::steady_clock::now();
   bool recompute = false;
   for (auto& pg : e.model->pending) recompute |= pg.in_place;
-  flush_prefill(e);
+  {
+    NvtxRange r("april.prompt_prefill");
+    flush_prefill(e);
+  }
   if (recompute) e.reprefill_seconds += std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
   launch_fork_groups(e.d, e.model->md, descs_dev, n, e.stream);
   AB_CUDA(cudaGetLastError());
   check_kv(e);
   if (e.cfg.kv_resume) {
     const auto t1 = std::chrono::steady_clock::now();
+    NvtxRange r("april.reprefill");
     resume_reprefill(e, e.stage_desc_host, n);  // synchronous
     e.reprefill_seconds += std::chrono::duration<double>(std::chrono::steady_clock::now() - t1).count();
   }
@@ -951,7 +955,8 @@ static bool gu_ws_runs(Model* M, int variant, const Model::Plans& p) {
 
 // kernels one decode iteration of graph variant `variant` launches
 int64_t model_iter_launches(Model* M, int variant) {
-  int64_t n = 4 + pair_launches(M, variant, 4, M->lm_dec, M->lm_dec2);  // prep, embed, final norm, sampler
+  // prep, embed, final norm, sampler (+ its finish pass)
+  int64_t n = 4 + (M->samp_split ? 1 : 0) + pair_launches(M, variant, 4, M->lm_dec, M->lm_dec2);
   for (const auto& p : M->dec)
     n += 4 + pair_launches(M, variant, 0, p.qkv, p.qkv2) + pair_launches(M, variant, 1, p.o, p.o2) +
          pair_launches(M, variant, 2, p.gu, p.gu2) + pair_launches(M, variant, 3, p.down, p.down2) +
@@ -1025,7 +1030,7 @@ void model_iteration(Engine& e, int64_t run_iter, bool timed, int variant) {
   }
   {
     ScopedTimer t(e, timed, "sampler", run_iter);
-    launch_sampler(e.d, m, M->logits, M->inv_temp, e.cfg.greedy, e.cfg.top_p, M->samp_cnt, M->samp_part, s);
+    launch_sampler(e.d, m, M->logits, M->inv_temp, e.cfg.greedy, e.cfg.top_p, M->samp_part, s);
   }
 }
 

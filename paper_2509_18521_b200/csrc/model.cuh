@@ -89,10 +89,11 @@ void launch_group_release(const EngineDev& e, const ModelDev& m, int group, cuda
 void launch_swiglu_ws(float* ws, bf16* h, int f, const int* sched, const int* rows_dev, int rows_cap, const int* stop,
                       cudaStream_t s);
 // sampler.cu
-// top_p = 1 or greedy: split kernel over fixed logit pieces (cnt [rows] zeroed, part
-// sampler_scratch_bytes); nucleus: one CTA per row
+// top_p = 1 or greedy: split kernels over fixed logit pieces (part: sampler_scratch_bytes);
+// nucleus: one CTA per row
 void launch_sampler(const EngineDev& e, const ModelDev& m, const float* logits, float inv_temp, int greedy,
-                    float top_p, int* cnt, void* part, cudaStream_t s);
+                    float top_p, void* part, cudaStream_t s);
 size_t sampler_scratch_bytes(int rows, int V);
+bool sampler_uses_split(int greedy, float top_p);  // two kernels (pieces + finish) per iteration
 
 }  // namespace ab

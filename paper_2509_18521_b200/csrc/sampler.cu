@@ -1,12 +1,12 @@
 // K1 (transformer path): fused sampler over the lm_head logits.
 //
-// Two kernels share the row rule.  `k_sample_split` (temperature / greedy, top_p = 1, the
-// decode default) splits every row into fixed 1024-logit pieces, one warp per piece, so all
-// SMs stream the logits whatever the live batch: a persistent grid of warps pulls (row, piece)
-// items, each writes its piece's (max, argmax, sum of 2^((z - max) * k2)) and the warp that
-// completes a row's last piece combines the row in fixed piece order and finishes it (draw,
-// owning-piece rescan, growth step).  Piece boundaries do not depend on the batch size, so a
-// row's result does not either.  `k_sample` below (nucleus top_p < 1) keeps one CTA per row:
+// Two paths share the row rule.  Temperature / greedy (top_p = 1, the decode default) runs two
+// kernels: `k_sample_pieces` splits every row into fixed 1024-logit pieces, one warp per piece, so
+// all SMs stream the logits whatever the live batch (a persistent grid of warps pulls (row, piece)
+// items and writes each piece's (max, argmax, sum of 2^((z - max) * k2))), then `k_sample_finish`
+// (one warp per row) combines the row in fixed piece order and finishes it (draw, owning-piece
+// rescan, growth step).  Piece boundaries do not depend on the batch size, so a row's result does
+// not either.  `k_sample` below (nucleus top_p < 1) keeps one CTA per row:
 //
 // One CTA per live row.  A single pass over the row keeps, per thread and
 // for a fixed contiguous chunk of the vocabulary, an online (max, sum of
@@ -74,9 +74,10 @@ __device__ void sample_row(const float* __restrict__ z, int V, float inv_temp, i
   float mx = -FLT_MAX;
   int am = 0x7fffffff;
   double sum = 0.0;  // sum of 2^((z - mx) * k2)
+  const bool vec_ok = (V & 3) == 0;  // rows 16-byte aligned: float4 loads
   for (int j = b0; j < b1; j += 4) {
     float4 v;
-    if (j + 4 <= b1) {
+    if (vec_ok && j + 4 <= b1) {
       v = *reinterpret_cast<const float4*>(z + j);
     } else {
       v.x = z[j];
@@ -361,30 +362,47 @@ struct SplitDebug {  // test entry: caller rows / draws / outputs instead of the
   double* logp;
 };
 
-// One warp combines row `row` from its P piece partials (fixed piece order: deterministic) and
-// returns the token / logp on every lane.  target = u * S selects the first index whose running
-// mass exceeds it: the owning piece is found from the piece sums, then that piece (1024 logits,
-// L2-resident) is rescanned 128 logits at a time with a warp scan.
+// One warp combines a row from its P piece partials (fixed piece order: deterministic) and returns
+// the token / logp on every lane.  target = u * S selects the first index whose running mass
+// exceeds it: the owning piece is found from the piece sums, then that piece (1024 logits, L2
+// resident) is reloaded in one round (8 float4 per lane, the pass-1 layout: element
+// 128 k + 4 lane + q) and located with per-tile lane sums, tile totals and one warp scan.
+constexpr int kMaxPpl = 8;  // pieces per lane: P <= 256 (V <= 262,144)
+// draw(): the row's uniform (Philox at the current position, or the test's); evaluated after the
+// partial loads are issued so its dependent loads and the Philox rounds overlap them
+template <typename Draw>
 __device__ void split_finish_row(const float* __restrict__ z, int V, int P, const float4* __restrict__ part,
-                                 float k2, float inv_temp, int greedy, double u, int& tok, double& logp) {
+                                 float k2, float inv_temp, int greedy, Draw draw, int& tok, double& logp) {
   const int lane = threadIdx.x & 31;
   const int ppl = (P + 31) / 32;  // pieces per lane (contiguous)
-  const int p0 = min(P, lane * ppl), p1 = min(P, p0 + ppl);
-  float lm = -FLT_MAX;
-  int la = 0x7fffffff;
-  for (int p = p0; p < p1; ++p) {
-    const float4 q = __ldcg(part + p);
-    am_merge(lm, la, q.x, __float_as_int(q.y));
+  const int p0 = lane * ppl;
+  float pm[kMaxPpl];
+  int pa[kMaxPpl];
+  double ps[kMaxPpl];
+#pragma unroll
+  for (int t = 0; t < kMaxPpl; ++t) {
+    pm[t] = -FLT_MAX;
+    pa[t] = 0x7fffffff;
+    ps[t] = 0.0;
+    if (t < ppl && p0 + t < P) {
+      const float4 q = __ldcg(part + p0 + t);
+      pm[t] = q.x;
+      pa[t] = __float_as_int(q.y);
+      ps[t] = __hiloint2double(__float_as_int(q.w), __float_as_int(q.z));
+    }
   }
-  float M = lm;
-  int A = la;
+  const double u = draw();
+  float M = -FLT_MAX;
+  int A = 0x7fffffff;
+#pragma unroll
+  for (int t = 0; t < kMaxPpl; ++t) am_merge(M, A, pm[t], pa[t]);
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) am_merge(M, A, __shfl_xor_sync(0xffffffffu, M, o), __shfl_xor_sync(0xffffffffu, A, o));
   double mine = 0.0;
-  for (int p = p0; p < p1; ++p) {
-    const float4 q = __ldcg(part + p);
-    const double sp = __hiloint2double(__float_as_int(q.w), __float_as_int(q.z));
-    if (q.x > -FLT_MAX) mine += sp * (double)exp2f((q.x - M) * k2);
+#pragma unroll
+  for (int t = 0; t < kMaxPpl; ++t) {
+    ps[t] = pm[t] > -FLT_MAX ? ps[t] * (double)exp2f((pm[t] - M) * k2) : 0.0;  // rescaled to the row max
+    mine += ps[t];
   }
   double incl = mine;
 #pragma unroll
@@ -402,73 +420,94 @@ __device__ void split_finish_row(const float* __restrict__ z, int V, int P, cons
     double base = 0.0;
     if (own) {
       const int ol = __ffs(own) - 1;
-      if (lane == ol) {
-        double run = before;
-        for (int p = p0; p < p1; ++p) {
-          const float4 q = __ldcg(part + p);
-          const double sp = __hiloint2double(__float_as_int(q.w), __float_as_int(q.z));
-          const double add = q.x > -FLT_MAX ? sp * (double)exp2f((q.x - M) * k2) : 0.0;
-          if (add > 0.0) {  // (rounding: the last massive piece of the lane)
-            piece = p;
-            base = run;
-          }
-          if (add > 0.0 && run + add > target) break;
-          run += add;
+      double run = before, pb = 0.0;
+      int pc = -1;
+#pragma unroll
+      for (int t = 0; t < kMaxPpl; ++t) {
+        if (pc >= 0 && run > target) break;  // (found in an earlier piece)
+        if (ps[t] > 0.0) {
+          pc = p0 + t;  // (rounding: the last massive piece of the lane)
+          pb = run;
         }
+        run += ps[t];
       }
-      piece = __shfl_sync(0xffffffffu, piece, ol);
-      base = __shfl_sync(0xffffffffu, base, ol);
+      piece = __shfl_sync(0xffffffffu, pc, ol);
+      base = __shfl_sync(0xffffffffu, pb, ol);
     }
-    int found = -1, last = -1;
+    int found = -1;
     if (piece >= 0) {
       const int j0 = piece * kPiece, j1 = min(V, j0 + kPiece);
-      for (int t0 = j0; t0 < j1 && found < 0; t0 += 128) {
-        const int j = t0 + 4 * lane;
-        float x[4];
+      float x[32];
 #pragma unroll
-        for (int q = 0; q < 4; ++q) x[q] = j + q < j1 ? __ldcg(z + j + q) : -FLT_MAX;
-        double pl[4], ls = 0.0;
+      for (int k = 0; k < 8; ++k)
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
-          pl[q] = x[q] > -FLT_MAX ? (double)exp2f((x[q] - M) * k2) : 0.0;
-          ls += pl[q];
+          const int j = j0 + 4 * (lane + 32 * k) + q;
+          x[4 * k + q] = j < j1 ? __ldcg(z + j) : -FLT_MAX;
         }
-        double li = ls;
+      double ls[8];  // this lane's mass in tile k (elements 128 k + 4 lane + q)
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        ls[k] = 0.0;
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+          if (x[4 * k + q] > -FLT_MAX) ls[k] += (double)exp2f((x[4 * k + q] - M) * k2);
+      }
+      double tt[8];  // tile totals (fixed xor tree)
+#pragma unroll
+      for (int k = 0; k < 8; ++k) tt[k] = ls[k];
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1)
+#pragma unroll
+        for (int k = 0; k < 8; ++k) tt[k] += __shfl_xor_sync(0xffffffffu, tt[k], o);
+      int kt = -1;
+      double tb = base;
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        if (kt < 0 && tt[k] > 0.0) {
+          if (tb + tt[k] > target) kt = k;
+          else tb += tt[k];
+        }
+      }
+      int last = -1;
+      if (kt < 0) {  // u * S rounded past the piece: its last index with mass
+#pragma unroll
+        for (int k = 0; k < 8; ++k)
+#pragma unroll
+          for (int q = 0; q < 4; ++q)
+            if (x[4 * k + q] > -FLT_MAX) last = max(last, j0 + 4 * (lane + 32 * k) + q);
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) last = max(last, __shfl_xor_sync(0xffffffffu, last, o));
+        found = last;
+      } else {
+        double lsk = 0.0;
+#pragma unroll
+        for (int k = 0; k < 8; ++k)
+          if (k == kt) lsk = ls[k];
+        double li = lsk;
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
           const double y = __shfl_up_sync(0xffffffffu, li, o);
           if (lane >= o) li += y;
         }
-        const double lb = base + li - ls;
-        const unsigned hit = __ballot_sync(0xffffffffu, ls > 0.0 && base + li > target);
-        const unsigned mass = __ballot_sync(0xffffffffu, ls > 0.0);
-        if (mass) {  // last index with mass so far (fallback when u * S rounds past the piece)
-          const int hl = 31 - __clz(mass);
-          int lq = -1;
-          if (lane == hl)
-            for (int q = 0; q < 4; ++q)
-              if (pl[q] > 0.0) lq = j + q;
-          last = __shfl_sync(0xffffffffu, lq, hl);
-        }
-        if (hit) {
-          const int hl = __ffs(hit) - 1;
-          int fq = -1;
-          if (lane == hl) {
-            double run = lb;
-            for (int q = 0; q < 4; ++q) {
-              run += pl[q];
-              if (pl[q] > 0.0 && run > target) {
-                fq = j + q;
-                break;
+        const unsigned hit = __ballot_sync(0xffffffffu, lsk > 0.0 && tb + li > target);
+        const int hl = hit ? __ffs(hit) - 1 : 31;
+        int fq = -1;
+        if (lane == hl) {
+          double run = tb + li - lsk;
+#pragma unroll
+          for (int k = 0; k < 8; ++k)
+            if (k == kt)
+#pragma unroll
+              for (int q = 0; q < 4; ++q) {
+                const float xv = x[4 * k + q];
+                if (xv <= -FLT_MAX || fq >= 0 && run > target) continue;
+                run += (double)exp2f((xv - M) * k2);
+                fq = j0 + 4 * (lane + 32 * k) + q;  // the first index whose running mass exceeds target
               }
-              if (pl[q] > 0.0) fq = j + q;  // (rounding: last massive index of the lane)
-            }
-          }
-          found = __shfl_sync(0xffffffffu, fq, hl);
         }
-        base = __shfl_sync(0xffffffffu, base + li, 31);
+        found = __shfl_sync(0xffffffffu, fq, hl);
       }
-      if (found < 0) found = last;
     }
     if (found < 0) {  // u * S rounded past every piece: the last token with mass
       int t = V - 1;
@@ -480,31 +519,35 @@ __device__ void split_finish_row(const float* __restrict__ z, int V, int P, cons
   logp = (double)((__ldcg(z + tok) - M) * inv_temp) - log2(S) * kLn2;
 }
 
+// Pass 1: a persistent grid of warps streams (row, piece) items: per piece its max, lowest argmax
+// and fp64 sum of 2^((z - max) * k2) (8 float4 per lane, one coalesced 4 KB read), written to
+// part[row][piece].  No fences or atomics on the streaming path: pass 2 is the next kernel.
 __global__ void __launch_bounds__(kSplitWarps * 32, kSplitCtasPerSm)
-    k_sample_split(EngineDev e, ModelDev m, const float* __restrict__ logits, int V, float inv_temp, int greedy,
-                   int* __restrict__ cnt, float4* __restrict__ part, SplitDebug dbg) {
+    k_sample_pieces(const Ctl* __restrict__ ctl, int dbg_rows, const float* __restrict__ logits, int V, float inv_temp,
+                    float4* __restrict__ part) {
   pdl_wait();
   int b;
-  if (dbg.tok) {
-    b = dbg.rows;
+  if (ctl) {
+    if (ctl->stop) return;
+    b = ctl->b;
   } else {
-    const Ctl* c = e.ctl;
-    if (c->stop) return;
-    b = c->b;
+    b = dbg_rows;
   }
+  pdl_launch();  // pass 2 launches and waits for this grid
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const int P = (V + kPiece - 1) / kPiece;
   const float k2 = inv_temp * kLog2e;
-  const int64_t items = (int64_t)b * P;
-  for (int64_t it = (int64_t)blockIdx.x * kSplitWarps + w; it < items; it += (int64_t)gridDim.x * kSplitWarps) {
-    const int row = (int)(it / P), piece = (int)(it - (int64_t)row * P);
+  const int items = b * P;
+  const bool vec_ok = (V & 3) == 0;  // rows 16-byte aligned: float4 loads
+  for (int it = (int)blockIdx.x * kSplitWarps + w; it < items; it += (int)gridDim.x * kSplitWarps) {
+    const int row = it / P, piece = it - row * P;
     const float* z = logits + (size_t)row * V;
     const int j0 = piece * kPiece, j1 = min(V, j0 + kPiece);
     float x[32];
 #pragma unroll
     for (int k = 0; k < 8; ++k) {
       const int j = j0 + 4 * (lane + 32 * k);
-      if (j + 4 <= j1) {
+      if (vec_ok && j + 4 <= j1) {
         const float4 v = __ldg(reinterpret_cast<const float4*>(z + j));
         x[4 * k] = v.x;
         x[4 * k + 1] = v.y;
@@ -520,57 +563,66 @@ __global__ void __launch_bounds__(kSplitWarps * 32, kSplitCtasPerSm)
 #pragma unroll
     for (int k = 0; k < 8; ++k)
 #pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        const int j = j0 + 4 * (lane + 32 * k) + q;
+      for (int q = 0; q < 4; ++q)
         if (x[4 * k + q] > mx) {  // strictly greater: the lowest index of a lane wins ties
           mx = x[4 * k + q];
-          am = j;
+          am = j0 + 4 * (lane + 32 * k) + q;
         }
-      }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) am_merge(mx, am, __shfl_xor_sync(0xffffffffu, mx, o), __shfl_xor_sync(0xffffffffu, am, o));
-    double sum = 0.0;
+    // lane sum in fp32 over 32 values (each <= 1), then fp64 across lanes (fixed xor tree)
+    float fs = 0.f;
     if (mx > -FLT_MAX) {
 #pragma unroll
       for (int k = 0; k < 32; ++k)
-        if (x[k] > -FLT_MAX) sum += (double)exp2f((x[k] - mx) * k2);
+        if (x[k] > -FLT_MAX) fs += exp2f((x[k] - mx) * k2);
     }
+    double sum = (double)fs;
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
-    int done = 0;
-    if (lane == 0) {
+    if (lane == 0)
       part[(size_t)row * P + piece] =
           make_float4(mx, __int_as_float(am), __int_as_float(__double2loint(sum)), __int_as_float(__double2hiint(sum)));
-      __threadfence();
-      done = atomicAdd(&cnt[row], 1) == P - 1;
-    }
-    done = __shfl_sync(0xffffffffu, done, 0);
-    if (!done) continue;
-    // this warp completed the row: combine and finish it
-    __threadfence();
-    if (lane == 0) cnt[row] = 0;
-    double u = 0.0;
-    int h = -1, g = 0;
-    if (dbg.tok) {
-      u = dbg.u[row];
-    } else {
-      h = e.slot_handle[row];
-      g = e.h_gen[h];
-      if (!greedy) {
-        const ulonglong2 key = e.h_key[h];
-        u = philox_uniform(key.x, key.y, (uint64_t)g);
-      }
-    }
-    int tok;
-    double logp;
-    split_finish_row(z, V, P, part + (size_t)row * P, k2, inv_temp, greedy, u, tok, logp);
-    if (lane != 0) continue;
-    if (dbg.tok) {
-      dbg.tok[row] = tok;
-      dbg.logp[row] = logp;
-    } else {
-      grow_row(e, m, row, h, g, tok, logp);
-    }
+  }
+}
+
+// Pass 2: one warp per live row combines its piece partials in fixed order, draws, rescans the
+// owning piece and runs the growth step (engine) or writes the test outputs.
+__global__ void __launch_bounds__(256) k_sample_finish(EngineDev e, ModelDev m, const float* __restrict__ logits,
+                                                      int V, float inv_temp, int greedy,
+                                                      const float4* __restrict__ part, SplitDebug dbg) {
+  pdl_wait();
+  int b;
+  if (dbg.tok) {
+    b = dbg.rows;
+  } else {
+    const Ctl* c = e.ctl;
+    if (c->stop) return;
+    b = c->b;
+  }
+  const int lane = threadIdx.x & 31;
+  const int row = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (row >= b) return;
+  const int P = (V + kPiece - 1) / kPiece;
+  const float k2 = inv_temp * kLog2e;
+  int h = -1, g = 0;
+  auto draw = [&]() -> double {
+    if (dbg.tok) return dbg.u[row];
+    h = e.slot_handle[row];
+    g = e.h_gen[h];
+    if (greedy) return 0.0;
+    const ulonglong2 key = e.h_key[h];
+    return philox_uniform(key.x, key.y, (uint64_t)g);
+  };
+  int tok;
+  double logp;
+  split_finish_row(logits + (size_t)row * V, V, P, part + (size_t)row * P, k2, inv_temp, greedy, draw, tok, logp);
+  if (lane != 0) return;
+  if (dbg.tok) {
+    dbg.tok[row] = tok;
+    dbg.logp[row] = logp;
+  } else {
+    grow_row(e, m, row, h, g, tok, logp);
   }
 }
 
@@ -592,12 +644,14 @@ size_t sampler_scratch_bytes(int rows, int V) { return (size_t)rows * ((V + kPie
 bool sampler_uses_split(int greedy, float top_p) { return greedy || top_p >= 1.f; }
 
 void launch_sampler(const EngineDev& e, const ModelDev& m, const float* logits, float inv_temp, int greedy,
-                    float top_p, int* cnt, void* part, cudaStream_t s) {
+                    float top_p, void* part, cudaStream_t s) {
   AB_REQUIRE(top_p > 0.f && top_p <= 1.f, AB_ERR_CONFIG, "top_p must lie in (0, 1]");
   if (sampler_uses_split(greedy, top_p)) {
     SplitDebug no{0, nullptr, nullptr, nullptr};
-    launch_pdl(k_sample_split, dim3(split_grid()), dim3(kSplitWarps * 32), 0, s, e, m, logits, m.V, inv_temp, greedy,
-               cnt, (float4*)part, no);
+    launch_pdl(k_sample_pieces, dim3(split_grid()), dim3(kSplitWarps * 32), 0, s, (const Ctl*)e.ctl, 0, logits, m.V,
+               inv_temp, (float4*)part);
+    launch_pdl(k_sample_finish, dim3(ceil_div(e.S, 8)), dim3(256), 0, s, e, m, logits, m.V, inv_temp, greedy,
+               (const float4*)part, no);
   } else {
     launch_pdl(k_sample, dim3(e.S), dim3(kSampThreads), 0, s, e, m, logits, inv_temp, greedy, top_p);
   }
@@ -615,19 +669,17 @@ extern "C" int ab_debug_sample_rows(const float* logits, int rows, int V, float 
     if (rows <= 0) return AB_OK;
     if (ab::sampler_uses_split(greedy, top_p)) {
       // the decode path's split kernel (fixed 1024-logit pieces) on caller rows
-      int* cnt = nullptr;
       void* part = nullptr;
-      AB_CUDA(cudaMalloc(&cnt, sizeof(int) * rows));
-      AB_CUDA(cudaMemset(cnt, 0, sizeof(int) * rows));
       AB_CUDA(cudaMalloc(&part, ab::sampler_scratch_bytes(rows, V)));
       ab::SplitDebug dbg{rows, u, tok, logp};
       ab::EngineDev e{};
       ab::ModelDev m{};
-      ab::k_sample_split<<<ab::split_grid(), ab::kSplitWarps * 32>>>(e, m, logits, V, inv_temp, greedy, cnt,
-                                                                     (float4*)part, dbg);
+      ab::k_sample_pieces<<<ab::split_grid(), ab::kSplitWarps * 32>>>(nullptr, rows, logits, V, inv_temp,
+                                                                      (float4*)part);
+      ab::k_sample_finish<<<ab::ceil_div(rows, 8), 256>>>(e, m, logits, V, inv_temp, greedy, (const float4*)part,
+                                                           dbg);
       AB_CUDA(cudaGetLastError());
       AB_CUDA(cudaDeviceSynchronize());
-      cudaFree(cnt);
       cudaFree(part);
     } else {
       ab::k_sample_rows<<<rows, ab::kSampThreads>>>(logits, V, inv_temp, greedy, top_p, u, tok, logp);

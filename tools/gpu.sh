@@ -9,6 +9,7 @@
 #   ncu_attn B CTX           ncu --set full of the decode attention kernel
 #   sanitize                 compute-sanitizer racecheck + memcheck on the engine / attention tests
 #   forcedp [bench args]     plain vs --force-dp (world-1 lockstep wrapper) decisions, compared
+#   dp2 [bench args]         bench.py at world 2 on one GPU (gloo host collectives, IPC exchange)
 set -u
 mkdir -p gpurun_out
 export AB_TEST_REPORT_DIR=gpurun_out/test_reports
@@ -54,5 +55,12 @@ case "$MODE" in
     timeout 1200 python bench.py --steps 3 --warmup 2 --no-sync --no-cpu "$@" > gpurun_out/forcedp_plain.log 2>&1
     timeout 1200 python bench.py --steps 3 --warmup 2 --no-sync --no-cpu --force-dp "$@" > gpurun_out/forcedp_dp.log 2>&1
     python tools/compare_forcedp.py gpurun_out/forcedp_plain.log gpurun_out/forcedp_dp.log | tee gpurun_out/forcedp_compare.txt ;;
+  dp2)
+    # the multi-rank bench path at world 2 on ONE GPU: two torchrun ranks pinned to cuda:0, gloo host
+    # collectives, device-side lockstep exchange through CUDA IPC (scaling is not measurable here)
+    AB_BENCH_DEVICE=0 AB_BENCH_BACKEND=gloo timeout 1500 python -m torch.distributed.run --nnodes=1 --nproc-per-node 2 \
+      --master-addr 127.0.0.1 --master-port 29555 bench.py --gpus 2 --no-cpu --kv-pages ${KVP:-30000} "$@" \
+      > gpurun_out/dp2_bench.log 2> gpurun_out/dp2_bench.err
+    echo "dp2 rc=$?" >> gpurun_out/dp2_bench.err; tail -c 2500 gpurun_out/dp2_bench.log ;;
   *) echo "unknown mode $MODE"; exit 2 ;;
 esac

@@ -1,0 +1,7 @@
+# Bench lines for BASELINE.json configs[2..4] on one B200 (per-engine shares of the 8-GPU configs):
+# C3 (DAPO, recycling), the C4 over-provision sweep (GSPO, N'/N = 1.5 / 2 / 3), C5 (R1-Distill-7B shape)
+mkdir -p gpurun_out
+run() { tag=$1; shift; timeout 2400 python bench.py --no-cpu "$@" > gpurun_out/cfg_${tag}.log 2> gpurun_out/cfg_${tag}.err; echo "$tag rc=$?"; }
+run C3 --workload C3 --steps 3 --warmup 3 --sync-steps 2
+for x in 1.5 2 3; do run C4_$x --workload C4 --over-provision $x --steps 3 --warmup 3 --sync-steps 2; done
+run C5 --workload C5 --steps 3 --warmup 3 --sync-steps 2
