@@ -81,6 +81,20 @@ __global__ void k_admit(EngineDev d) {
   __syncthreads();
   const int n = s_n;
   if (n < 0) return;
+  if (d.h_needs_pf) {
+    // KV re-prefill mode: a resumed sample about to be admitted has no KV yet -- stop before
+    // admitting anything (the iteration does not happen); the host rebuilds the next admissions'
+    // KV and resumes the run, so admission order and iteration count are unchanged
+    bool need = false;
+    for (int i = threadIdx.x; i < n; i += blockDim.x) need |= d.h_needs_pf[d.q_buf[(s_head + i) % d.Q]] != 0;
+    if (__syncthreads_or(need)) {
+      if (threadIdx.x == 0) {
+        c->stop = 1;
+        c->stop_reason = kRunNeedPrefill;
+      }
+      return;
+    }
+  }
   const int b = s_b;
   const int64_t it = c->iteration_index;
   const int64_t ver = c->version;
@@ -687,6 +701,7 @@ static Engine* create(const ab_engine_config* cfgp, const ab_model_config* m, in
     d.h_logp = dalloc<double>((size_t)d.H * d.L);
   }
   d.g_done = dalloc<int32_t>(d.G_cap);
+  if (c.model_kind == AB_MODEL_TRANSFORMER && c.kv_resume) d.h_needs_pf = dalloc<int32_t>(d.H);
   d.ev = dalloc<ab_event>(d.H + d.S);
   d.adm = dalloc<ab_admit>(d.H + d.S);
   if (c.model_kind == AB_MODEL_CONTEXT_FREE) {
@@ -737,6 +752,7 @@ static void destroy(Engine* e) {
   void* ptrs[] = {d.ctl,     d.slot_handle, d.slot_tmp, d.slot_finish, d.slot_token, d.q_buf,  d.h_gen,
                   d.h_stop,  d.h_group,     d.h_key,    d.h_version,   d.h_tokens,   d.h_logp, d.g_done,
                   d.ev,      d.adm,         d.cf_logits, d.cf_cdf,     d.cf_logp,    d.it_b,   d.it_ctx,
+                  d.h_needs_pf,
                   e->stage_desc_dev, e->stage_i32_dev};
   for (void* p : ptrs)
     if (p) cudaFree(p);
@@ -894,6 +910,18 @@ static void run(Engine& e, const ab_run_args* a, ab_run_result* r, ab_event* ev,
     }
     collect_prof(e);
     const Ctl& c = *e.ctl_host;
+    if (c.stop && c.stop_reason == kRunNeedPrefill && c.error == kErrNone) {
+      // rebuild the KV of the samples the next admission takes (plus a few beyond it), then go on
+      const int want = std::min(e.d.S - c.b, c.q_tail - c.q_head);
+      model_prefill_deferred(e, std::max(1, want) + 8);
+      e.ctl_host->stop = 0;
+      e.ctl_host->stop_reason = -1;
+      static_assert(offsetof(Ctl, stop_reason) == offsetof(Ctl, stop) + 4, "layout");
+      AB_CUDA(cudaMemcpyAsync(&e.d.ctl->stop, &e.ctl_host->stop, 2 * sizeof(int32_t), cudaMemcpyHostToDevice,
+                              e.stream));
+      chunk = 1;
+      continue;
+    }
     if (c.stop) break;
     if (c.iters_to_next > 0)
       chunk = c.iters_to_next;
@@ -955,6 +983,7 @@ static void abort_active(Engine& e, int32_t* handles, int32_t* gen, int cap, int
   }
   c.b = 0;
   c.q_head = c.q_tail;
+  if (e.model) model_drop_deferred(e);
   AB_CUDA(cudaMemcpy(&e.d.ctl->b, &c.b, sizeof(int32_t), cudaMemcpyHostToDevice));
   AB_CUDA(cudaMemcpy(&e.d.ctl->q_head, &c.q_head, sizeof(int32_t), cudaMemcpyHostToDevice));
   if (e.model && e.cfg.kv_resume && b + q) {
@@ -1254,9 +1283,15 @@ int ab_engine_release(ab_engine* e, const int32_t* handles, int n) {
     Engine& g = *e->impl;
     if (!g.model || n <= 0) return;
     AB_REQUIRE((size_t)n <= g.stage_i32_cap, AB_ERR_CONTRACT, "too many handles");
+    ab::model_forget_deferred(g, handles, n);
     memcpy(g.stage_i32_host, handles, sizeof(int32_t) * n);
     AB_CUDA(cudaMemcpyAsync(g.stage_i32_dev, g.stage_i32_host, sizeof(int32_t) * n, cudaMemcpyHostToDevice,
                             g.stream));
+    if (g.d.h_needs_pf) {  // a released handle is never waiting for a rebuild
+      const int32_t zero = 0;
+      for (int i = 0; i < n; ++i)
+        AB_CUDA(cudaMemcpyAsync(g.d.h_needs_pf + handles[i], &zero, sizeof(int32_t), cudaMemcpyHostToDevice, g.stream));
+    }
     ab::model_release(g, g.stage_i32_dev, n);
     AB_CUDA(cudaStreamSynchronize(g.stream));
   });

@@ -57,6 +57,10 @@ enum : int32_t {
   kErrDpTimeout = 6  // data-parallel: a peer's exchange record did not arrive in time
 };
 
+// internal stop reason: k_admit met a queued sample whose KV must be re-prefilled first (KV
+// re-prefill mode, one engine): the host rebuilds the next admissions' KV and resumes the run
+constexpr int32_t kRunNeedPrefill = 4;
+
 struct Model;  // transformer (model.cu)
 
 // POD view passed by value to kernels.
@@ -79,6 +83,7 @@ struct EngineDev {
   int32_t* h_tokens;  // [H * L]
   double* h_logp;     // [H * L]
   int32_t* g_done;
+  int32_t* h_needs_pf;  // [H] or nullptr: 1 = queued resumed sample whose KV is not rebuilt yet
   ab_event* ev;
   ab_admit* adm;
   double* cf_logits;  // [n_symbols]
@@ -166,6 +171,10 @@ void model_weight_info(Model* m, int idx, std::string* name, int64_t* rows, int6
 void model_open_group(Engine& e, int group_slot, const int32_t* prompt, int prompt_len);
 void model_release_group(Engine& e, int group_slot);
 void model_submit(Engine& e, const ab_sample_desc* descs_dev, int n);  // after per-handle state is set
+// KV re-prefill mode: rebuild the KV of the next `count` deferred resumed samples (FIFO order)
+void model_prefill_deferred(Engine& e, int count);
+void model_drop_deferred(Engine& e);  // abort: queued resumed samples were never rebuilt
+void model_forget_deferred(Engine& e, const int32_t* handles_host, int n);  // released handles
 void model_release(Engine& e, const int32_t* handles_dev, int n);
 void model_evict(Engine& e, const int32_t* handles_host, const int32_t* gen, int n);  // kv_resume: drop private KV
 void model_begin_step(Engine& e, int64_t version);

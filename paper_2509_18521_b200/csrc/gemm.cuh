@@ -46,7 +46,11 @@ struct GemmPlan {
   bool idle = false;           // the table is all zeros: gemm_launch skips the launch
   std::vector<int> host_tab;   // host copy of the schedule table (row counts known on the host)
   bool early_trigger = false;  // launch_dependents right after setup (successor = a small kernel)
-  double extra_us = 0;         // autotuning: cost of a follow-up kernel this plan needs (added to its time)
+  double extra_us = 0;         // autotuning: fixed cost added to this plan's measured time
+  // autotuning: a follow-up kernel this plan needs (timed together with the GEMM), e.g. the SwiGLU
+  // pass of the gate-up workspace plan; follow_arg is its extra operand
+  void (*follow)(const GemmPlan&, cudaStream_t) = nullptr;
+  void* follow_arg = nullptr;
 };
 
 void gemm_plan(GemmPlan& p, const __nv_bfloat16* W, int N, int K, const __nv_bfloat16* A, int M_cap, int64_t lda,

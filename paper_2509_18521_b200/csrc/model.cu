@@ -12,6 +12,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <deque>
 #include <map>
 #include <string>
 #include <vector>
@@ -80,6 +81,9 @@ struct Model {
     bool in_place;  // re-prefill of a resident group's prompt (pages already allocated)
   };
   std::vector<PendingGroup> pending;
+  // KV re-prefill mode, one engine: resumed samples whose KV is rebuilt only when their admission is
+  // next (bounded KV: a long partial-rollout buffer is never rebuilt all at once), FIFO order
+  std::deque<ab_sample_desc> deferred;
   // causal attention blocks of a prefill chunk ({first row, rows, block-table row, first position})
   int4 *pf_blocks = nullptr, *pf_blocks_host = nullptr;
   int pf_blocks_cap = 0;
@@ -116,6 +120,12 @@ int pick_bn(int rows) {
 }
 
 }  // namespace
+
+// the gate-up workspace plan's follow-up pass (timed with it by the autotuner)
+static void follow_swiglu(const GemmPlan& p, cudaStream_t s) {
+  launch_swiglu_ws(reinterpret_cast<float*>(p.out), reinterpret_cast<bf16*>(p.follow_arg), p.N / 2, p.sched,
+                   p.rows_dev, p.M_cap, p.stop_dev, s);
+}
 
 // Decode GEMM autotuning: for every projection, each of its alternative plans (cluster-8 split-K,
 // cluster-1 reduce-add / cluster-2, CTA pair) and every valid fixed schedule is timed on this GPU
@@ -373,7 +383,13 @@ Model* model_create(Engine& e) {
   M->attn = dalloc<bf16>(R * m.qd);
   M->hbuf = dalloc<bf16>(R * m.f);
   M->logits = dalloc<float>((size_t)M->S * m.V);
-  if (ec.nondeterministic_gemm) M->gu_ws = dalloc<float>((size_t)M->S * 2 * m.f);  // kept zeroed between uses
+  // gate-up stream-K workspace plan (experimental, AB_GU_WORKSPACE=1): measured slower than the
+  // cluster-8 SwiGLU plan at decode batches once its SwiGLU pass is included, so off by default
+  {
+    const char* gw = getenv("AB_GU_WORKSPACE");
+    if (ec.nondeterministic_gemm && gw && atoi(gw) != 0)
+      M->gu_ws = dalloc<float>((size_t)M->S * 2 * m.f);  // kept zeroed between uses
+  }
   M->samp_part = dalloc<uint8_t>(sampler_scratch_bytes(M->S, m.V));
   M->samp_split = sampler_uses_split(ec.greedy, ec.top_p);
   // smallest KV split of an attention work item (the prep kernel picks the split per iteration);
@@ -478,14 +494,15 @@ Model* model_create(Engine& e) {
       const bool et = gt ? atoi(gt) != 0 : false;
       d.o.early_trigger = d.o2.early_trigger = d.down.early_trigger = d.down2.early_trigger = et;
     }
-    if (nd) {
+    if (nd && M->gu_ws) {
       // gate-up alternative: raw gate / up accumulators reduce-added into a zeroed fp32 workspace by
       // stream-K ranges (every SM streams the same weight bytes whatever the tile count), then
       // k_swiglu_ws forms h = silu(gate) * up and re-zeroes the workspace
       gemm_plan(d.gu2, w.wgu, 2 * m.f, m.d, M->xn, M->S, m.d, bn_dec, kEpiAddF32, M->gu_ws, 2 * m.f, nullptr, b,
                 stop, 1);
       d.gu2.nondet = true;
-      d.gu2.extra_us = 3.0;  // the SwiGLU pass (measured ~2-3 us at decode batches)
+      d.gu2.follow = follow_swiglu;  // the autotuner times the plan together with its SwiGLU pass
+      d.gu2.follow_arg = M->hbuf;
     } else {
       gemm_plan(d.gu2, w.wgu, 2 * m.f, m.d, M->xn, M->S, m.d, bn_dec, kEpiSwiGLU, M->hbuf, m.f, nullptr, b, stop, 8);
     }
@@ -883,6 +900,21 @@ void model_begin_step(Engine& e, int64_t version) {
   M->last_version = version;
 }
 
+__global__ void k_set_flags(int32_t* flags, const int32_t* idx, int n, int32_t v) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) flags[idx[i]] = v;
+}
+
+// flags[stage_i32_host[0..n)] = v on the device (stage_i32 holds the handles)
+static void set_handle_flags(Engine& e, int n, int32_t v) {
+  if (n <= 0 || !e.d.h_needs_pf) return;
+  AB_CUDA(cudaMemcpyAsync(e.stage_i32_dev, e.stage_i32_host, sizeof(int32_t) * n, cudaMemcpyHostToDevice, e.stream));
+  k_set_flags<<<ceil_div(n, 256), 256, 0, e.stream>>>(e.d.h_needs_pf, e.stage_i32_dev, n, v);
+  AB_CUDA(cudaGetLastError());
+  AB_CUDA(cudaStreamSynchronize(e.stream));  // stage_i32 is reused by the caller
+  e.launches += 1;
+}
+
 void model_submit(Engine& e, const ab_sample_desc* descs_dev, int n) {
   AB_REQUIRE(!e.model->kv_released, AB_ERR_CONTRACT, "KV pool released: call resume_memory first");
   const auto t0 = std::chrono::steady_clock::now();
@@ -897,11 +929,59 @@ void model_submit(Engine& e, const ab_sample_desc* descs_dev, int n) {
   AB_CUDA(cudaGetLastError());
   check_kv(e);
   if (e.cfg.kv_resume) {
-    const auto t1 = std::chrono::steady_clock::now();
-    NvtxRange r("april.reprefill");
-    resume_reprefill(e, e.stage_desc_host, n);  // synchronous
-    e.reprefill_seconds += std::chrono::duration<double>(std::chrono::steady_clock::now() - t1).count();
+    if (e.d.h_needs_pf && e.d.dp_world <= 1) {
+      // defer: flag the resumed samples; k_admit stops the run when one of them is next and
+      // model_prefill_deferred rebuilds the KV of that admission
+      Model* M = e.model;
+      int k = 0;
+      for (int i = 0; i < n; ++i) {
+        const ab_sample_desc& d = e.stage_desc_host[i];
+        if (d.gen_len > 0 && M->evicted[d.handle]) {
+          M->deferred.push_back(d);
+          e.stage_i32_host[k++] = d.handle;
+        }
+      }
+      set_handle_flags(e, k, 1);
+    } else {
+      const auto t1 = std::chrono::steady_clock::now();
+      NvtxRange r("april.reprefill");
+      resume_reprefill(e, e.stage_desc_host, n);  // synchronous
+      e.reprefill_seconds += std::chrono::duration<double>(std::chrono::steady_clock::now() - t1).count();
+    }
   }
+}
+
+void model_prefill_deferred(Engine& e, int count) {
+  Model* M = e.model;
+  const int n = std::min<int>(count, (int)M->deferred.size());
+  if (n <= 0) return;
+  const auto t1 = std::chrono::steady_clock::now();
+  NvtxRange r("april.reprefill");
+  std::vector<ab_sample_desc> descs(M->deferred.begin(), M->deferred.begin() + n);
+  M->deferred.erase(M->deferred.begin(), M->deferred.begin() + n);
+  resume_reprefill(e, descs.data(), n);  // synchronous
+  for (int i = 0; i < n; ++i) e.stage_i32_host[i] = descs[i].handle;
+  set_handle_flags(e, n, 0);
+  e.reprefill_seconds += std::chrono::duration<double>(std::chrono::steady_clock::now() - t1).count();
+}
+
+void model_forget_deferred(Engine& e, const int32_t* handles, int n) {
+  Model* M = e.model;
+  if (M->deferred.empty()) return;
+  for (int i = 0; i < n; ++i)
+    for (auto it = M->deferred.begin(); it != M->deferred.end(); ++it)
+      if (it->handle == handles[i]) {
+        M->deferred.erase(it);
+        break;
+      }
+}
+
+void model_drop_deferred(Engine& e) {
+  Model* M = e.model;
+  int k = 0;
+  for (const auto& d : M->deferred) e.stage_i32_host[k++] = d.handle;
+  M->deferred.clear();
+  set_handle_flags(e, k, 0);
 }
 
 void model_release(Engine& e, const int32_t* handles_dev, int n) {

@@ -149,3 +149,24 @@ def test_tcgen05_gemm_reduce_add_split(shape, code):
     torch.cuda.synchronize()
     ref = base + A.float() @ W.float().t()
     torch.testing.assert_close(out, ref, rtol=2e-3, atol=2e-3 * max(1.0, ref.abs().max().item() * 0.01))
+
+
+@pytest.mark.parametrize("shape", [(19456, 2560, 64), (6144, 2560, 64), (1536, 1536, 384), (2560, 9728, 100),
+                                   (384, 640, 1000)])
+@pytest.mark.parametrize("code", [0x10000 | 1 | (6 << 1) | (1 << 5), 0x10000 | 1 | (7 << 1) | (1 << 5),
+                                  0x10000 | 0 | (7 << 1) | (1 << 5), 1 | (6 << 1) | (3 << 5), 1 | (7 << 1) | (7 << 5)])
+def test_tcgen05_gemm_stream_k_and_odd_splits(shape, code):
+    """Stream-K reduce-add ranges (0x10000: every CTA streams an equal contiguous range of (tile,
+    k-block pair) work, split over tile boundaries) and non-power-of-two reduce-add split counts."""
+    N, K, M = shape
+    if _capi.lib().ab_debug_gemm_sched(N, K, M, 256, 1, 148, 0x40000000 | 0x8000 | code, 2) == 0:
+        pytest.skip("schedule not valid for this shape")
+    g = torch.Generator(device="cuda").manual_seed(N + K + M + code)
+    W = (torch.randn(N, K, device="cuda", generator=g) * 0.05).to(torch.bfloat16)
+    A = torch.randn(M, K, device="cuda", generator=g).to(torch.bfloat16)
+    base = torch.randn(M, N, device="cuda", generator=g)
+    out = base.clone()
+    _capi.call("ab_debug_gemm", _ptr(W), _ptr(A), _ptr(out), None, N, K, M, 0x8000 | code, 2 + 1024 + 128)
+    torch.cuda.synchronize()
+    ref = base + A.float() @ W.float().t()
+    torch.testing.assert_close(out, ref, rtol=2e-3, atol=2e-3 * max(1.0, ref.abs().max().item() * 0.01))
