@@ -20,6 +20,7 @@
 
 #include <algorithm>
 #include <cfloat>
+#include <cstdlib>
 #include <vector>
 
 #include "model.cuh"
@@ -30,6 +31,7 @@ namespace {
 
 constexpr float kLog2e = 1.4426950408889634f;
 __constant__ int c_pdl_mask = 6;  // see gemm.cu
+__constant__ int c_att_prefetch = 0;  // AB_ATT_PREFETCH=1: claim the next work item one item ahead
 constexpr int kTok = 64;        // tokens per tile
 constexpr int kCons = 4;        // consumer warps (16 tokens each)
 constexpr int kThreads = (kCons + 1) * 32;
@@ -167,10 +169,14 @@ __global__ void __launch_bounds__(kThreads, 2)
       const uint32_t qbytes = (uint32_t)(gq * HD * 2);
       const int box_rows = m.P < kTok ? m.P : kTok;
       int g = 0;
+      // work items are pulled dynamically (one cursor per layer, reset by the prep kernel); with
+      // c_att_prefetch the next item's index is claimed while the current one streams (hides the
+      // atomic's round trip at item boundaries, at the price of committing one item ahead)
+      int next = c_att_prefetch ? atomicAdd(&m.att_ctl[1 + layer], 1) : 0;
       for (int k = 0;; ++k) {
-        // work items are pulled dynamically (one cursor per layer, reset by the prep kernel)
-        const int item = atomicAdd(&m.att_ctl[1 + layer], 1);
+        const int item = c_att_prefetch ? next : atomicAdd(&m.att_ctl[1 + layer], 1);
         if (item >= total) break;
+        if (c_att_prefetch) next = atomicAdd(&m.att_ctl[1 + layer], 1);
         const int rs = item / m.hk, kvh = item % m.hk;
         const int packed = m.att_items[rs];
         const int row = packed & 0xffff, sp = packed >> 16;
@@ -438,20 +444,32 @@ void launch_t(const CUtensorMap& map, const EngineDev& e, const ModelDev& m, int
 
 // ---------------------------------------------------------------------------
 // Causal prefill attention (prompt prefill and the re-prefill of resumed
-// partials, §8 f1): flash-attention-2 over the paged pool.  Block = up to 64
+// partials, §8 f1): flash-attention-2 over the paged pool.  Block = up to 128
 // consecutive rows of one sequence (its block-table row and first position
-// come from the host-built block list), one q head per CTA; 4 warps own 16
+// come from the host-built block list), one q head per CTA; 8 warps own 16
 // rows each.  K / V tiles of 64 tokens are gathered page by page with
 // cp.async into the same 128-byte-swizzled layout the decode kernel reads
 // (double-buffered), S = Q K^T and O += P V run as mma.sync m16n8k16 with
 // exp2 online softmax; tokens past a row's position are masked.
 // ---------------------------------------------------------------------------
 
+// Q block of kPfRows rows (8 warps x 16 rows): each K / V tile staged in shared memory serves 128 query
+// rows (the first version used 64-row blocks and 4 warps: half the tile reuse, half the warps)
+constexpr int kPfRows = 128;
+constexpr int kPfThreads = kPfRows / 16 * 32;
+
 template <int HD>
 struct PfCfg {
-  static constexpr int kTile = kTok * HD * 2;        // 64 rows x HD bf16
-  static constexpr int kSmem = 1024 + 5 * kTile;     // Q + 2 stages x (K, V)
+  static constexpr int kTile = kTok * HD * 2;                  // 64 rows x HD bf16
+  static constexpr int kTileQ = kPfRows * HD * 2;              // the Q block
+  static constexpr int kSmem = 1024 + kTileQ + 4 * kTile;      // Q + 2 stages x (K, V)
 };
+
+// tile_off for a tile of R rows (the Q block): 16-byte chunk ch of row r, 128-byte swizzle
+template <int R>
+__device__ __forceinline__ uint32_t tile_off_r(int r, int ch) {
+  return (uint32_t)((ch >> 3) * (R * 128) + r * 128 + (((ch & 7) ^ (r & 7)) << 4));
+}
 
 __device__ __forceinline__ void cp_async16(uint32_t dst, const void* src, bool valid) {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst), "l"(src), "r"(valid ? 16 : 0) : "memory");
@@ -463,7 +481,7 @@ __device__ __forceinline__ void cp_async_wait() {
 }
 
 template <int HD>
-__global__ void __launch_bounds__(128, 2)
+__global__ void __launch_bounds__(kPfThreads, 1)
     k_prefill_flash(ModelDev m, int layer, const bf16* __restrict__ q, bf16* __restrict__ out,
                     const int4* __restrict__ blocks) {
   using Cfg = PfCfg<HD>;
@@ -477,18 +495,18 @@ __global__ void __launch_bounds__(128, 2)
 
   extern __shared__ uint8_t smem_raw[];
   uint8_t* base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  const uint32_t sQ = su32(base), sKV = sQ + Cfg::kTile;
+  const uint32_t sQ = su32(base), sKV = sQ + Cfg::kTileQ;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int gr = lane >> 2, tq = lane & 3;
 
-  for (int i = tid; i < kTok * CH; i += 128) {
+  for (int i = tid; i < kPfRows * CH; i += kPfThreads) {
     const int r = i / CH, ch = i % CH;
     const bool v = r < nrows;
-    cp_async16(sQ + tile_off(r, ch), q + (size_t)(row0 + (v ? r : 0)) * m.qd + head * HD + ch * 8, v);
+    cp_async16(sQ + tile_off_r<kPfRows>(r, ch), q + (size_t)(row0 + (v ? r : 0)) * m.qd + head * HD + ch * 8, v);
   }
   auto load_kv = [&](int kt, int stage) {
     const uint32_t K = sKV + stage * 2 * Cfg::kTile, V = K + Cfg::kTile;
-    for (int i = tid; i < kTok * CH; i += 128) {
+    for (int i = tid; i < kTok * CH; i += kPfThreads) {
       const int r = i / CH, ch = i % CH;
       const int tok = kt * kTok + r;
       const bool v = tok <= last_pos;
@@ -518,7 +536,8 @@ __global__ void __launch_bounds__(128, 2)
     __syncthreads();
     if (kt == 0) {
 #pragma unroll
-      for (int kk = 0; kk < HD / 16; ++kk) ldsm_x4(qa[kk], sQ + tile_off(wq + (lane & 15), kk * 2 + (lane >> 4)), false);
+      for (int kk = 0; kk < HD / 16; ++kk)
+        ldsm_x4(qa[kk], sQ + tile_off_r<kPfRows>(wq + (lane & 15), kk * 2 + (lane >> 4)), false);
     }
     const int tb = kt * kTok;
     if (tb <= warp_last && wq < nrows) {
@@ -617,7 +636,7 @@ void launch_pf(const ModelDev& m, int layer, const bf16* q, bf16* out, const int
     AB_CUDA(cudaFuncSetAttribute(k_prefill_flash<HD>, cudaFuncAttributeMaxDynamicSharedMemorySize, PfCfg<HD>::kSmem));
     init = true;
   }
-  k_prefill_flash<HD><<<dim3(n_blocks, m.hq), 128, PfCfg<HD>::kSmem, s>>>(m, layer, q, out, blocks);
+  k_prefill_flash<HD><<<dim3(n_blocks, m.hq), kPfThreads, PfCfg<HD>::kSmem, s>>>(m, layer, q, out, blocks);
 }
 
 }  // namespace
@@ -631,7 +650,12 @@ void launch_prefill_flash(const ModelDev& m, int layer, const bf16* q, bf16* out
     launch_pf<64>(m, layer, q, out, blocks, n_blocks, s);
 }
 
-void set_pdl_mask_attention(int mask) { AB_CUDA(cudaMemcpyToSymbol(c_pdl_mask, &mask, sizeof(int))); }
+void set_pdl_mask_attention(int mask) {
+  AB_CUDA(cudaMemcpyToSymbol(c_pdl_mask, &mask, sizeof(int)));
+  const char* ap = getenv("AB_ATT_PREFETCH");
+  const int pf = ap ? atoi(ap) : 0;
+  AB_CUDA(cudaMemcpyToSymbol(c_att_prefetch, &pf, sizeof(int)));
+}
 
 void make_kv_tmap(CUtensorMap* map, const ModelDev& m) {
   AB_REQUIRE(m.gq <= kMergeRows, AB_ERR_CONFIG, "decode attention supports GQA groups of at most 8");

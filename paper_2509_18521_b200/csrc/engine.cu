@@ -271,6 +271,19 @@ __global__ void __launch_bounds__(kFinishThreads) k_finish(EngineDev d) {
     if (i >= end) break;
     const int h = d.slot_handle[i];
     if (fin[j]) {
+      if (d.kv_bt) {
+        // free the finished sample's private KV pages now (k_release semantics; the host's later
+        // release of the handle finds nothing left to free)
+        const int have = (d.kv_h_ctx[h] + d.kv_P - 1) / d.kv_P, own0 = d.kv_h_shared[h];
+        const int cnt = have - own0;
+        if (cnt > 0) {
+          const long long base =
+              (long long)atomicAdd(reinterpret_cast<unsigned long long*>(&c->kv_free_top), (unsigned long long)cnt);
+          for (int q = 0; q < cnt; ++q) d.kv_free[base + q] = d.kv_bt[(size_t)h * d.kv_MP + own0 + q];
+        }
+        d.kv_h_ctx[h] = 0;
+        d.kv_h_shared[h] = 0;
+      }
       int complete = 0;
       if (G > 0) {
         const int old = atomicAdd(&d.g_done[d.h_group[h]], 1);
@@ -913,7 +926,8 @@ static void run(Engine& e, const ab_run_args* a, ab_run_result* r, ab_event* ev,
     if (c.stop && c.stop_reason == kRunNeedPrefill && c.error == kErrNone) {
       // rebuild the KV of the samples the next admission takes (plus a few beyond it), then go on
       const int want = std::min(e.d.S - c.b, c.q_tail - c.q_head);
-      model_prefill_deferred(e, std::max(1, want) + 8);
+      AB_REQUIRE(model_prefill_deferred(e, std::max(1, want) + 8) > 0, AB_ERR_CONTRACT,
+                 "a queued sample waits for a KV rebuild that is not pending");
       e.ctl_host->stop = 0;
       e.ctl_host->stop_reason = -1;
       static_assert(offsetof(Ctl, stop_reason) == offsetof(Ctl, stop) + 4, "layout");
@@ -941,7 +955,7 @@ static void run(Engine& e, const ab_run_args* a, ab_run_result* r, ab_event* ev,
     else if (c.error == kErrNoTarget)
       msg = "sample handle " + std::to_string(c.error_handle) + " has no target length";
     else if (c.error == kErrOutOfKV)
-      throw Error(AB_ERR_OUT_OF_KV, "KV page pool exhausted");
+      throw Error(AB_ERR_OUT_OF_KV, "KV page pool exhausted during decode (" + model_kv_report(e) + ")");
     else if (c.error == kErrPeer)
       throw Error(AB_ERR_NCCL, "data-parallel: a peer rank's iteration failed");
     else if (c.error == kErrDpTimeout)

@@ -84,6 +84,13 @@ struct EngineDev {
   double* h_logp;     // [H * L]
   int32_t* g_done;
   int32_t* h_needs_pf;  // [H] or nullptr: 1 = queued resumed sample whose KV is not rebuilt yet
+  // transformer: the KV page state k_finish needs to free a finished sample's private pages at once
+  // (a fused run lasts thousands of iterations; pages must not wait for the host's release)
+  int32_t* kv_bt;       // block tables [rows][kv_MP] (nullptr: no model)
+  int32_t* kv_h_ctx;    // context length per handle
+  int32_t* kv_h_shared; // leading pages shared with the prompt group
+  int32_t* kv_free;     // free-page stack (top in Ctl::kv_free_top)
+  int kv_P, kv_MP;
   ab_event* ev;
   ab_admit* adm;
   double* cf_logits;  // [n_symbols]
@@ -172,7 +179,7 @@ void model_open_group(Engine& e, int group_slot, const int32_t* prompt, int prom
 void model_release_group(Engine& e, int group_slot);
 void model_submit(Engine& e, const ab_sample_desc* descs_dev, int n);  // after per-handle state is set
 // KV re-prefill mode: rebuild the KV of the next `count` deferred resumed samples (FIFO order)
-void model_prefill_deferred(Engine& e, int count);
+int model_prefill_deferred(Engine& e, int count);  // returns how many were rebuilt
 void model_drop_deferred(Engine& e);  // abort: queued resumed samples were never rebuilt
 void model_forget_deferred(Engine& e, const int32_t* handles_host, int n);  // released handles
 void model_release(Engine& e, const int32_t* handles_dev, int n);
@@ -186,6 +193,7 @@ int model_variant_for(Model* m, int rows);  // the variant for a chunk whose liv
 int64_t model_iter_launches(Model* m, int variant);
 void model_iteration(Engine& e, int64_t run_iter, bool timed, int variant);  // pages + forward + sampler
 int64_t model_pages_total(Model* m);
+std::string model_kv_report(Engine& e);  // for out-of-KV errors
 void model_kernel_cost(Model* m, const std::string& name, double b, double sum_ctx, double* bytes, double* flops);
 
 // profiling helper (engine.cu)

@@ -454,6 +454,12 @@ Model* model_create(Engine& e) {
   AB_CUDA(cudaMemcpy(&e.d.ctl->kv_free_top, &np, sizeof(int64_t), cudaMemcpyHostToDevice));
   make_kv_tmap(&M->kvmap, m);
   e.ctl_host->kv_free_top = np;
+  e.d.kv_bt = m.bt;
+  e.d.kv_h_ctx = m.h_ctx;
+  e.d.kv_h_shared = m.h_shared;
+  e.d.kv_free = m.free_pages;
+  e.d.kv_P = m.P;
+  e.d.kv_MP = m.MP;
 
   // ---- GEMM plans ----
   const int* b = &e.d.ctl->b;
@@ -575,6 +581,19 @@ void model_weight_info(Model* M, int idx, std::string* name, int64_t* rows, int6
 
 int64_t model_pages_total(Model* M) { return M->md.NP; }
 
+// pool / batch / resident-state summary for out-of-KV errors
+std::string model_kv_report(Engine& e) {
+  Model* M = e.model;
+  if (!M) return "no model";
+  AB_CUDA(cudaMemcpyAsync(e.ctl_host, e.d.ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, e.stream));
+  AB_CUDA(cudaStreamSynchronize(e.stream));
+  const Ctl& c = *e.ctl_host;
+  return "pages " + std::to_string(M->md.NP) + ", free top " + std::to_string(c.kv_free_top) + ", live rows " +
+         std::to_string(c.b) + ", queued " + std::to_string(c.q_tail - c.q_head) + ", resident prompt groups " +
+         std::to_string(M->prompts.size()) + ", deferred rebuilds " + std::to_string(M->deferred.size()) +
+         ", page " + std::to_string(M->md.P) + " tokens";
+}
+
 void model_open_group(Engine& e, int group_slot, const int32_t* prompt, int prompt_len) {
   Model* M = e.model;
   AB_REQUIRE(prompt != nullptr && prompt_len >= 2, AB_ERR_CONTRACT, "prompt needs >= 2 tokens");
@@ -588,14 +607,17 @@ void model_open_group(Engine& e, int group_slot, const int32_t* prompt, int prom
 static void check_kv(Engine& e) {
   AB_CUDA(cudaMemcpyAsync(&e.ctl_host->error, &e.d.ctl->error, sizeof(int32_t), cudaMemcpyDeviceToHost, e.stream));
   AB_CUDA(cudaStreamSynchronize(e.stream));
-  if (e.ctl_host->error == kErrOutOfKV) throw Error(AB_ERR_OUT_OF_KV, "KV page pool exhausted");
+  if (e.ctl_host->error == kErrOutOfKV)
+    throw Error(AB_ERR_OUT_OF_KV, "KV page pool exhausted (" + model_kv_report(e) + ")");
 }
 
-// Append the causal-attention blocks (<= 64 rows) of one run of rows of a sequence.
+// Append the causal-attention blocks (<= kPfBlockRows rows, attention.cu kPfRows) of one run of rows of a
+// sequence.
+constexpr int kPfBlockRows = 128;
 static int add_blocks(Model* M, int nb, int row0, int n, int btrow, int pos0) {
-  for (int i = 0; i < n; i += 64) {
+  for (int i = 0; i < n; i += kPfBlockRows) {
     AB_REQUIRE(nb < M->pf_blocks_cap, AB_ERR_CONFIG, "prefill block list overflow");
-    M->pf_blocks_host[nb++] = make_int4(row0 + i, std::min(64, n - i), btrow, pos0 + i);
+    M->pf_blocks_host[nb++] = make_int4(row0 + i, std::min(kPfBlockRows, n - i), btrow, pos0 + i);
   }
   return nb;
 }
@@ -951,10 +973,10 @@ void model_submit(Engine& e, const ab_sample_desc* descs_dev, int n) {
   }
 }
 
-void model_prefill_deferred(Engine& e, int count) {
+int model_prefill_deferred(Engine& e, int count) {
   Model* M = e.model;
   const int n = std::min<int>(count, (int)M->deferred.size());
-  if (n <= 0) return;
+  if (n <= 0) return 0;
   const auto t1 = std::chrono::steady_clock::now();
   NvtxRange r("april.reprefill");
   std::vector<ab_sample_desc> descs(M->deferred.begin(), M->deferred.begin() + n);
@@ -963,6 +985,7 @@ void model_prefill_deferred(Engine& e, int count) {
   for (int i = 0; i < n; ++i) e.stage_i32_host[i] = descs[i].handle;
   set_handle_flags(e, n, 0);
   e.reprefill_seconds += std::chrono::duration<double>(std::chrono::steady_clock::now() - t1).count();
+  return n;
 }
 
 void model_forget_deferred(Engine& e, const int32_t* handles, int n) {

@@ -109,3 +109,25 @@ def test_c4_c5_shape_model_replay_matches_reference_digests(name, preset, layers
     recs, sched = product_replay(canon.CONFIGS[name], "april", len(dg), **_model_kw(spec, "reprefill", True))
     assert [canon.digest(r) for r in recs] == dg
     sched.engine.close()
+
+
+@pytest.mark.parametrize("name", ["C4_3", "C3"])
+def test_kv_pages_conserved_across_steps(name):
+    """KV page conservation with the bench's re-prefill mode at S = 64 and a long partial buffer: after
+    each step's abort the pages in use are exactly the resident prompt groups' pages plus one private
+    tail page per held sample that has not generated a token (its fork), nothing else."""
+    spec = pb.PRESETS["qwen3-4b"].truncated(1)
+    cfg = canon.CONFIGS[name]
+    sched = make_scheduler(cfg, "april", **_model_kw(spec, "reprefill", True))
+    eng = sched.engine
+    P, prompt = eng.page_size, eng.prompt_len
+    per_group = (prompt - 1 + P - 1) // P
+    tail = 1 if (prompt - 1) % P else 0
+    for k in range(4):
+        sched.run_step(k)
+        st = eng.stats()
+        used = st.kv_pages_total - st.kv_pages_free
+        held_zero = sum(1 for h, s in eng._by_handle.items() if s.total_tokens == 0)
+        expect = per_group * len(eng._gslot) + tail * held_zero
+        assert used == expect, (k, used, expect, len(eng._gslot), held_zero, len(eng._by_handle))
+    eng.close()

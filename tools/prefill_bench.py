@@ -3,8 +3,9 @@
     python tools/prefill_bench.py --model qwen2.5-1.5b --samples 64 --gen 2000 [--ncu]
 
 Admits `samples` samples (groups of 8, 256-token prompts), decodes `gen` iterations, aborts, bumps the
-version and resubmits: the resubmit re-prefills samples x gen rows (plus the groups' prompts).  Prints
-the re-prefill wall time and rows/s.  --ncu brackets only the resubmit with cudaProfilerStart/Stop.
+version and resubmits: the resubmit plus the admitting iteration re-prefill samples x gen rows (plus the
+groups' prompts).  Prints the re-prefill wall time and rows/s (the timed span includes one decode
+iteration).  --ncu brackets only the resubmit with cudaProfilerStart/Stop.
 """
 import argparse
 import json
@@ -49,6 +50,9 @@ def main():
     for p in paused:
         eng.submit(p)
     eng._flush()
+    # the rebuild happens when the resumed samples are admitted (admission-time re-prefill): one
+    # decode iteration admits them all (S >= samples)
+    eng.decode_iterations(1)
     torch.cuda.synchronize()
     t1 = time.perf_counter()
     if args.ncu:
