@@ -288,7 +288,6 @@ Model* model_create(Engine& e) {
   AB_REQUIRE(c.d_ff % 64 == 0 && c.vocab % 128 == 0, AB_ERR_CONFIG, "d_ff % 64 and vocab % 128 required");
   AB_REQUIRE(ec.page_size >= 16 && ec.page_size % 16 == 0, AB_ERR_CONFIG, "page_size must be a multiple of 16");
   AB_REQUIRE(ec.max_prompt >= 2, AB_ERR_CONFIG, "max_prompt must be >= 2");
-  AB_REQUIRE(ec.top_p >= 1.f, AB_ERR_CONFIG, "top_p < 1 is not supported by this build");
   {
     // which kernels trigger their dependents early (bit 1 GEMM at start, 2 attention, 4 RMSNorm,
     // 8 GEMM after its last MMA)

@@ -340,6 +340,9 @@ class Engine:
         """
         if comm.world < 2:
             return
+        if self._h is None:
+            raise ContractViolation("dp_attach needs the device engine (the context-free model creates it at its "
+                                    "first begin_step)")
         ptr = C.c_uint64()
         ipc = (C.c_uint8 * 64)()
         capi.call("ab_engine_dp_export", self._h, comm.world, C.byref(ptr), ipc)

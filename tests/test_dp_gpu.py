@@ -181,3 +181,69 @@ def test_device_lockstep_across_processes_ipc():
         assert not isinstance(got[r], str), got[r]
         for a, b in zip(got[r], ref):
             assert a == b, canon.first_diff(a, b)
+
+
+def test_device_lockstep_policy_mode_matches_k_engine_oracle():
+    """Policy stop rules (the reference's toy PolicyDrivenEngine on the GPU: Philox draw, softmax,
+    inverse CDF, STOP) under the device lockstep at world 2: no jump hints (the exchange's policy
+    branch), token ids included in the comparison with the composed k-engine oracle."""
+    import numpy as np
+
+    import paper_2509_18521_b200 as pb
+    from oracle import sim_ref
+    from paper_2509_18521_b200.dist import DataParallelEngine, GpuLocal, ThreadComm
+
+    t = canon.TOY
+    z = np.array([0.4, -0.1, 0.2, 0.0, -0.6])
+    steps, world = 10, 2
+    # the composed oracle
+    keng = sim_ref.KEngineOracle(world, t["d0"], t["d1"], t["slots"], t["l_max"], mode="policy", seed=t["seed"])
+    ksch = sim_ref.OracleScheduler(t["n"], t["g"], t["n_prime"], keng, mode="april")
+    ref, ref_tok = [], {}
+    for k in range(steps):
+        keng.event_log = []
+        out = ksch.run_step(k, z)
+        ref.append(canon.step_record(ksch, out, keng.event_log))
+        ref_tok.update({(k, s.sample_id): s.token_ids() for s in out.batch_samples()})
+    # the device lockstep
+    comms = ThreadComm.group(world)
+    ecfg = pb.EngineConfig(max_slots=t["slots"], l_max=t["l_max"])
+    engines = [pb.PolicyDrivenEngine(ecfg, global_seed=t["seed"]) for _ in range(world)]
+    for e in engines:
+        e._create(z.size)  # the context-free engine is otherwise created at its first begin_step
+    out_recs, errors = [None] * world, []
+
+    def work(r):
+        try:
+            front = DataParallelEngine(GpuLocal(engines[r]).attach(comms[r]), comms[r], t["slots"])
+            scfg = pb.SchedulerConfig(rollout_batch_size=t["n"], samples_per_prompt=t["g"],
+                                      over_sampling_batch_size=t["n_prime"], mode="april")
+            sched = pb.Scheduler(scfg, front, pb.InstanceSource(group_size=t["g"]), None)
+            sched.event_sink = []
+            recs, toks = [], {}
+            for k in range(steps):
+                o = sched.run_step(k, pb.PolicyParams(z, k))
+                recs.append(canon.step_record(sched, o, step_events(sched)))
+                # token ids of the delivered samples this rank generated (remote mirrors carry none)
+                toks.update({(k, s.sample_id): s.token_ids() for s in o.batch_samples()
+                             if s.segments and all(seg.tokens is not None for seg in s.segments)})
+            out_recs[r] = (recs, toks)
+        except BaseException as exc:  # noqa: BLE001
+            errors.append(exc)
+            comms[r].abort()
+
+    threads = [threading.Thread(target=work, args=(r,)) for r in range(world)]
+    for th in threads:
+        th.start()
+    for th in threads:
+        th.join(timeout=600)
+    for e in engines:
+        e.close()
+    if errors:
+        raise errors[0]
+    for r in range(world):
+        for a, b in zip(out_recs[r][0], ref):
+            assert a == b, (r, canon.first_diff(a, b))
+    got = {**out_recs[0][1], **out_recs[1][1]}
+    assert set(got) == set(ref_tok)
+    assert all(got[k] == ref_tok[k] for k in ref_tok)

@@ -23,11 +23,11 @@ LOGP_TOL = 0.05     # nats
 
 
 def _engine(spec, prompts, S=8, l_max=64, page=16, greedy=True, temperature=1.0, P=None, nondet=False,
-            kv_resume="retain"):
+            kv_resume="retain", top_p=1.0):
     P = P or max(len(p) for p in prompts.values())
     return pb.LengthDrivenEngine(
         pb.EngineConfig(max_slots=S, l_max=l_max), global_seed=3, model=spec,
-        sampling=pb.SamplingConfig(temperature=temperature, greedy=greedy), prompt_len=P, page_size=page,
+        sampling=pb.SamplingConfig(temperature=temperature, greedy=greedy, top_p=top_p), prompt_len=P, page_size=page,
         kv_pages=1024, max_handles=64, max_groups=16, prompt_source=lambda iid: prompts[iid],
         nondeterministic_gemm=nondet, kv_resume=kv_resume)
 
@@ -125,6 +125,44 @@ def test_resume_across_steps_keeps_kv_and_matches_uninterrupted():
     _drain(eng2)
     assert r.token_ids() == s.token_ids()
     np.testing.assert_allclose(r.behavior_logprob_trace(), s.behavior_logprob_trace(), rtol=0, atol=1e-6)
+
+
+def test_nucleus_sampling_in_the_engine():
+    """top_p < 1 in the engine's decode loop (K1 nucleus kernel, one CTA per row): every token lies in
+    the oracle's nucleus (sampler_ref.nucleus_threshold on the oracle's logits; a token within 1e-3 of
+    the threshold is tolerated) and its behaviour logp is the truncated distribution's."""
+    from oracle import sampler_ref
+
+    spec = pb.PRESETS["tiny"]
+    prompts = _prompts(spec, 1, 16)
+    T, top_p = 0.8, 0.9
+    eng = _engine(spec, prompts, greedy=False, temperature=T, top_p=top_p)
+    eng.begin_step(0)
+    s = RolloutSample(0, 1)
+    s.target_length = 40
+    eng.submit(s)
+    _drain(eng)
+    toks, lps = s.token_ids(), s.behavior_logprob_trace()
+    dec = CpuDecoder(spec, eng.export_weights())
+    cache = dec.new_cache()
+    prompt = [int(t) for t in prompts[0]]
+    dec.forward(prompt[:-1], cache, 0, want_logits=False)
+    tok, pos, outside = prompt[-1], len(prompt) - 1, 0
+    for k, g in enumerate(toks):
+        z = dec.forward([tok], cache, pos).float().numpy()
+        kmin = sampler_ref.nucleus_threshold(z, T, top_p)
+        keys = sampler_ref.logit_keys(z)
+        keep = keys >= np.uint32(kmin)
+        if not keep[g]:
+            zk = z[keep]
+            outside += int(z[g] < zk.min() - 1e-3)
+        p = np.exp2((z - z.max()) * np.float32(1.0 / T) * np.float32(1.4426950408889634)).astype(np.float64)
+        pk = np.where(keep, p, 0.0)
+        ref_lp = float(np.log(p[g] / pk.sum())) if keep[g] else None
+        if ref_lp is not None:
+            assert abs(lps[k] - ref_lp) < LOGP_TOL, (k, lps[k], ref_lp)
+        tok, pos = g, pos + 1
+    assert outside == 0
 
 
 def test_temperature_sampling_follows_philox_inverse_cdf():
