@@ -174,3 +174,58 @@ def test_gather_responses_world2_gloo():
             lps += [-0.5 * j - k for j in range(n)]
         want.append((toks, lps))
     assert got[0] == want and got[1] == want
+
+
+@pytest.mark.parametrize("name,world", [("C1", 3), ("E_pool", 2)])
+def test_dp_threads_match_k_engine_oracle(name, world):
+    """The same host lockstep with in-process collectives (ThreadComm, one thread per rank): every
+    rank's replicated scheduler produces the composed k-engine oracle's records."""
+    import threading
+
+    import canon
+    import paper_2509_18521_b200 as pb
+    from oracle import sim_ref
+    from paper_2509_18521_b200.dist import DataParallelEngine, OracleLocal, ThreadComm
+
+    cfg = canon.CONFIGS[name]
+    steps = 6
+    comms = ThreadComm.group(world, timeout=120)
+    out, errors = [None] * world, []
+
+    def work(r):
+        try:
+            local = OracleLocal(sim_ref.OracleEngine(0.05, 0.002, cfg["slots"], cfg["l_max"]))
+            eng = DataParallelEngine(local, comms[r], cfg["slots"])
+            d = cfg["dist"]
+            dist_obj = pb.LengthDistribution.lognormal(d[1], d[2], cfg["l_max"])
+            scfg = pb.SchedulerConfig(rollout_batch_size=cfg["n"], samples_per_prompt=cfg["g"],
+                                      over_sampling_batch_size=cfg["n_prime"], mode="april")
+            sched = pb.Scheduler(scfg, eng, pb.InstanceSource(group_size=cfg["g"]),
+                                 pb.LengthSampler(dist_obj, cfg["rho"], cfg["seed"]))
+            sched.event_sink = []
+            recs = []
+            for k in range(steps):
+                o = sched.run_step(k)
+                evs = [[x["iteration_index"], *map(int, x["sample_id"].split(":")), x["tokens"], x["reason"]]
+                       for x in sched.event_sink if x["reason"] != "aborted"]
+                sched.event_sink.clear()
+                recs.append(canon.step_record(sched, o, evs))
+            out[r] = recs
+        except BaseException as exc:  # noqa: BLE001
+            errors.append(exc)
+            comms[r].abort()
+
+    ts = [threading.Thread(target=work, args=(r,)) for r in range(world)]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join(timeout=300)
+    if errors:
+        raise errors[0]
+    ceng, csch = sim_ref.make_k_oracle(dict(cfg, mode="april"), world)
+    for k in range(steps):
+        ceng.event_log = []
+        o = csch.run_step(k)
+        ref = canon.step_record(csch, o, ceng.event_log)
+        for r in range(world):
+            assert out[r][k] == ref, (r, k, canon.first_diff(out[r][k], ref))
