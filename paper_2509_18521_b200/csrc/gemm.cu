@@ -431,7 +431,12 @@ __global__ void __launch_bounds__(kThreads, 1)
   // t_sk0, t_sk0 + 1, ... (units 0 .. n_units-1 of this CTA)
   const int np_sk = sc.nk >> 1;
   const int64_t w_all = (int64_t)sc.tiles * np_sk;
-  const int64_t w0 = sc.sk ? w_all * blockIdx.x / gridDim.x : 0, w1 = sc.sk ? w_all * (blockIdx.x + 1) / gridDim.x : 0;
+  // (32-bit divisions where the products fit: a 64-bit division is hundreds of instructions)
+  const bool sk32 = w_all * (int64_t)(gridDim.x + 1) < ((int64_t)1 << 31);
+  auto sk_bound = [&](uint32_t c) -> int64_t {
+    return sk32 ? (int64_t)(((uint32_t)w_all * c) / gridDim.x) : w_all * c / gridDim.x;
+  };
+  const int64_t w0 = sc.sk ? sk_bound(blockIdx.x) : 0, w1 = sc.sk ? sk_bound(blockIdx.x + 1) : 0;
   const int t_sk0 = sc.sk ? (int)(w0 / np_sk) : 0;
   const int u_first = sc.sk ? 0
                       : split ? ((int)blockIdx.x / cs) * per_cl + crank / sc.splits
@@ -893,26 +898,47 @@ __global__ void __launch_bounds__(kThreads, 1)
         // ---------------- swap-AB: lane = weight row, columns = activation rows ----------------
         const int n = n0 + lrow;
         if constexpr (EPI == kEpiSwiGLU) {
-          // lanes 0-63: gate rows, lanes 64-127: up rows of the same 64 features
-          const int j = (n0 >> 1) + (lrow & 63);
+          // lanes 0-63: gate rows, lanes 64-127: up rows of the same 64 features.  Both halves go
+          // through shared memory ([32 columns][128 lanes] fp32) so all four epilogue warps form
+          // h = silu(gate) * up (16 values each; with the gate lanes alone doing 32 each the loop
+          // was latency-bound at ~1 us per chunk), staged as bf16 [32 rows][64 features] and
+          // written as 16-byte vectors along each output row (the per-element 2-byte stores of
+          // the transposed tile were slower still).
+          float* ex = xchg;
+          __nv_bfloat16* stg = reinterpret_cast<__nv_bfloat16*>(xchg + 32 * 128);
+          const int f = te & 63, hc = (te >> 6) * 16;  // this thread's feature and column half
           for (int c0 = c_first; c0 < ncols; c0 += c_step) {
             float v[32];
             fetch(c0, v);
-            if (lrow >= 64) {
+            if (c0 == 0 && threadIdx.x == 128) trace_mark(trace, 14);
 #pragma unroll
-              for (int c = 0; c < 32; ++c) xchg[c * 64 + (lrow - 64)] = v[c];
+            for (int c = 0; c < 32; ++c) ex[c * 128 + lrow] = v[c];
+            asm volatile("bar.sync 1, 128;" ::: "memory");
+            {
+              float g[16], u[16];
+#pragma unroll
+              for (int i = 0; i < 16; ++i) {
+                g[i] = ex[(hc + i) * 128 + f];
+                u[i] = ex[(hc + i) * 128 + 64 + f];
+              }
+#pragma unroll
+              for (int i = 0; i < 16; ++i) stg[(hc + i) * 64 + f] = __float2bfloat16(silu(g[i]) * u[i]);
             }
             asm volatile("bar.sync 1, 128;" ::: "memory");
-            if (lrow < 64) {
-              __nv_bfloat16* o = reinterpret_cast<__nv_bfloat16*>(out);
+            {
+              __nv_bfloat16* o = reinterpret_cast<__nv_bfloat16*>(out) + (n0 >> 1);
 #pragma unroll
-              for (int c = 0; c < 32; ++c) {
+              for (int k = 0; k < 2; ++k) {
+                const int i = te + 128 * k, c = i >> 3, q = i & 7;
                 const int m = m0 + c0 + c;
-                if (m < rows) o[(int64_t)m * ldo + j] = __float2bfloat16(silu(v[c]) * xchg[c * 64 + lrow]);
+                if (m < rows)
+                  *reinterpret_cast<uint4*>(o + (int64_t)m * ldo + q * 8) =
+                      *reinterpret_cast<const uint4*>(stg + c * 64 + q * 8);
               }
             }
             asm volatile("bar.sync 1, 128;" ::: "memory");
           }
+          if (threadIdx.x == 128) trace_mark(trace, 15);
         } else {
           float bv = 0.f;
           if (EPI == kEpiBF16 && bias != nullptr) bv = __bfloat162float(bias[n]);
@@ -986,6 +1012,18 @@ __global__ void __launch_bounds__(kThreads, 1)
 }
 
 int g_trace_on = 0;
+
+// L2 flush for timing: READ a buffer larger than L2 (a memset would leave ~126 MB of dirty lines
+// whose write-back then competes with the timed kernel's reads -- the decode GEMMs never run after
+// such a burst of writes).  The sink store is never taken.
+__global__ void __launch_bounds__(512) k_l2_flush_read(const uint4* __restrict__ p, size_t n, int* sink) {
+  uint32_t acc = 0;
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) {
+    const uint4 v = __ldcg(p + i);
+    acc ^= v.x ^ v.y ^ v.z ^ v.w;
+  }
+  if (acc == 0x9E3779B9u && sink) *sink = (int)acc;
+}
 
 __global__ void k_trace_mark(int slot) {
   unsigned long long t;
@@ -1125,6 +1163,11 @@ void launch_t(const GemmPlan& p, cudaStream_t s) {
 }
 
 }  // namespace
+
+void l2_flush(void* buf, size_t bytes, cudaStream_t s) {
+  k_l2_flush_read<<<4 * 148, 512, 0, s>>>(reinterpret_cast<const uint4*>(buf), bytes / 16, nullptr);
+  AB_CUDA(cudaGetLastError());
+}
 
 void gemm_plan(GemmPlan& p, const __nv_bfloat16* W, int N, int K, const __nv_bfloat16* A, int M_cap, int64_t lda,
                int BN, int epi, void* out, int64_t ldo, const __nv_bfloat16* bias, const int* rows_dev,
@@ -1270,7 +1313,7 @@ double gemm_time_code(const GemmPlan& p, int rows, int code, int reps, void* flu
   std::vector<cudaEvent_t> ev(2 * reps);
   for (auto& x : ev) AB_CUDA(cudaEventCreate(&x));
   for (int r = 0; r < reps; ++r) {
-    if (flush) AB_CUDA(cudaMemsetAsync(flush, r & 0xff, flush_bytes, s));
+    if (flush) l2_flush(flush, flush_bytes, s);
     AB_CUDA(cudaEventRecord(ev[2 * r], s));
     gemm_launch(t, s);
     if (t.follow) t.follow(t, s);
@@ -1354,7 +1397,11 @@ extern "C" int ab_debug_gemm_time(const void* W, const void* A, void* out, const
     const bool nondet = (epi & 1024) != 0;
     const int force = (epi & 128) ? (0x40000000 | BN) : (epi & 32) ? 0 : (epi & 64) ? -BN : BN;
     epi &= 15;
-    if (!flush) AB_CUDA(cudaMalloc(&flush, size_t(256) << 20));
+    if (!flush) {
+      AB_CUDA(cudaMalloc(&flush, size_t(256) << 20));
+      AB_CUDA(cudaMemset(flush, 0, size_t(256) << 20));
+      ab::l2_flush(flush, size_t(256) << 20, 0);  // (write the memset's dirty lines back once)
+    }
     ab::GemmPlan p;
     ab::gemm_plan(p, (const __nv_bfloat16*)W, N, K, (const __nv_bfloat16*)A, M, K, (force > 0 && (force & 0x40000000)) ? 256 : BN, epi, out,
                   epi == ab::kEpiSwiGLU ? N / 2 : N, (const __nv_bfloat16*)bias, nullptr, nullptr, max_splits,
@@ -1367,7 +1414,7 @@ extern "C" int ab_debug_gemm_time(const void* W, const void* A, void* out, const
     AB_CUDA(cudaEventCreate(&a));
     AB_CUDA(cudaEventCreate(&b));
     for (int r = 0; r < reps; ++r) {
-      AB_CUDA(cudaMemsetAsync(flush, r & 0xff, size_t(256) << 20, 0));
+      ab::l2_flush(flush, size_t(256) << 20, 0);
       AB_CUDA(cudaEventRecord(a, 0));
       ab::gemm_launch(p, 0);
       AB_CUDA(cudaEventRecord(b, 0));

@@ -73,6 +73,8 @@ double gemm_time_code(const GemmPlan& p, int rows, int code, int reps, void* flu
 void gemm_set_table(GemmPlan& p, const std::vector<int>& tab);
 // The cost model's schedule for the plan at `rows` (0: no valid schedule).
 int gemm_default_code(const GemmPlan& p, int rows);
+// Evict L2 for timing by reading `bytes` (> L2) of `buf` (reads leave no dirty lines behind).
+void l2_flush(void* buf, size_t bytes, cudaStream_t s);
 // Rebuild the plan's schedule table (force: see GemmPlan::force).
 void gemm_set_schedule(GemmPlan& p, int force);
 

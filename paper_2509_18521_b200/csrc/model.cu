@@ -164,7 +164,11 @@ static void autotune_decode(Engine& e, Model* M) {
     const std::string key = key_of(g);
     auto it = cache2.find(key);
     if (it != cache2.end()) return it->second;
-    if (!flush) AB_CUDA(cudaMalloc(&flush, flush_bytes));
+    if (!flush) {
+      AB_CUDA(cudaMalloc(&flush, flush_bytes));
+      AB_CUDA(cudaMemsetAsync(flush, 0, flush_bytes, s));
+      l2_flush(flush, flush_bytes, s);  // (the memset's dirty lines are written back before any timing)
+    }
     Tuned out;
     out.tabs.assign(g.size(), std::vector<int>(cur_cap + 1, 0));
     out.choice.assign(cur_cap + 1, 0);

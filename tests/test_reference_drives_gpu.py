@@ -128,3 +128,36 @@ def test_convergence_parity_with_gpu_engine():
     apr = sum(finals["april"]) / 3
     assert base > 3 * uniform and apr > 3 * uniform, finals
     assert abs(apr - base) / base <= 0.05, finals
+
+
+_LENGTH_FIELDS = tuple(f for f in _ENGINE_FIELDS if f != "mean_reward")
+
+
+def test_build_simulation_runs_reference_config_on_gpu():
+    """`pb.build_simulation` (the drop-in for simulate.py:105-121) takes the reference's own
+    RunConfig: its default length-driven run (N 32, G 8, N' 64, lognormal tail) replayed on the GPU
+    engine gives the reference run's step reports (every field the engine determines), and the
+    toy-policy run with the reference trainer's update rule trains the same policy bit for bit."""
+    cfg = a.default_config().with_overrides(**{"run.steps": 6, "run.write_manifest": True})
+    mine, ref = pb.build_simulation(cfg), a.build_simulation(cfg)
+    for k in range(cfg.run.steps):
+        d1, d2 = mine.run_step().to_json_dict(), ref.run_step().to_json_dict()
+        for f in _LENGTH_FIELDS:
+            assert d1[f] == d2[f], (k, f, d1[f], d2[f])
+    assert len(mine.manifest) == len(ref.manifest)
+    assert [tuple(r.values()) for r in mine.manifest] == [
+        (r.step, r.instance_id, r.sample_index, r.start_version, r.complete_version, r.tokens) for r in ref.manifest]
+    assert mine.summary().buffer_high_water == ref.summary().buffer_high_water
+    mine.close()
+
+    cfg = a.toy_policy_config().with_overrides(**{"run.steps": 25, "run.seed": 3})
+    with pytest.raises(pb.ConfigError):
+        pb.build_simulation(cfg)  # a policy-driven run needs the trainer's update rule
+    mine = pb.run_simulation(cfg, policy_update=a.reinforce_update)
+    ref = a.run_simulation(cfg)
+    for r1, r2 in zip(mine.reports, ref.reports):
+        d1, d2 = r1.to_json_dict(), r2.to_json_dict()
+        for f in _ENGINE_FIELDS:
+            assert d1[f] == d2[f], (r1.step, f, d1[f], d2[f])
+    assert list(mine.policy.logits) == list(ref.policy.logits)
+    mine.close()

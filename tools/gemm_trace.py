@@ -34,9 +34,9 @@ ends = max(r[7] for r in t if r[7])
 print(f"marker kernel before: {(mk[0] - t0) / 1e3:.2f} us, last CTA exit {(ends - t0) / 1e3:.2f} us, "
       f"marker after: {(mk[1] - t0) / 1e3:.2f} us (includes a host sync)")
 names = ["entry", "setup", "tma0", "full0", "mma_end", "acc0", "epi_end", "exit", "part_wr", "prod0", "policy",
-         "acquired", "fetched", "slot0"]
+         "acquired", "fetched", "slot0", "epi_f0", "epi_lp"]
 print(f"{'cta':>4} " + " ".join(f"{n:>8}" for n in names) + "   (us after the first CTA entry)")
 for i, r in enumerate(t):
     if not r[0]:
         continue
-    print(f"{i:4d} " + " ".join(f"{(x - t0) / 1e3:8.2f}" if x else f"{'-':>8}" for x in r[:14]))
+    print(f"{i:4d} " + " ".join(f"{(x - t0) / 1e3:8.2f}" if x else f"{'-':>8}" for x in r[:16]))
