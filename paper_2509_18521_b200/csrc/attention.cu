@@ -31,7 +31,6 @@ namespace {
 
 constexpr float kLog2e = 1.4426950408889634f;
 __constant__ int c_pdl_mask = 6;  // see gemm.cu
-__constant__ int c_att_prefetch = 0;  // AB_ATT_PREFETCH=1: claim the next work item one item ahead
 constexpr int kTok = 64;        // tokens per tile
 constexpr int kCons = 4;        // consumer warps (16 tokens each)
 constexpr int kThreads = (kCons + 1) * 32;
@@ -85,6 +84,15 @@ __device__ __forceinline__ void tma_2d(const CUtensorMap* map, uint64_t* bar, vo
       "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];" ::"r"(
           su32(dst)),
       "l"(reinterpret_cast<uint64_t>(map)), "r"(su32(bar)), "r"(x), "r"(y)
+      : "memory");
+}
+// 4-D view {64 dims, pool row, dim half, k|v}: one operation = a 64-token tile's K and V, both
+// halves of the head dimension (32 KB at HD = 128), landing as [k|v][half][64 rows][128 B]
+__device__ __forceinline__ void tma_4d(const CUtensorMap* map, uint64_t* bar, void* dst, int y) {
+  asm volatile(
+      "cp.async.bulk.tensor.4d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, %3, %3}], "
+      "[%2];" ::"r"(su32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(su32(bar)), "r"(0), "r"(y)
       : "memory");
 }
 __device__ __forceinline__ void bulk_1d(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
@@ -163,66 +171,104 @@ __global__ void __launch_bounds__(kThreads, 2)
 
   if (warp == kCons) {
     // ------------------------------ producer ------------------------------
-    if (lane == 0) {
-      asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&kvmap)) : "memory");
-      const int chunk = m.att_ctl[0];
-      const uint32_t qbytes = (uint32_t)(gq * HD * 2);
-      const int box_rows = m.P < kTok ? m.P : kTok;
-      int g = 0;
-      // work items are pulled dynamically (one cursor per layer, reset by the prep kernel); with
-      // c_att_prefetch the next item's index is claimed while the current one streams (hides the
-      // atomic's round trip at item boundaries, at the price of committing one item ahead)
-      int next = c_att_prefetch ? atomicAdd(&m.att_ctl[1 + layer], 1) : 0;
-      for (int k = 0;; ++k) {
-        const int item = c_att_prefetch ? next : atomicAdd(&m.att_ctl[1 + layer], 1);
-        if (item >= total) break;
-        if (c_att_prefetch) next = atomicAdd(&m.att_ctl[1 + layer], 1);
-        const int rs = item / m.hk, kvh = item % m.hk;
-        const int packed = m.att_items[rs];
-        const int row = packed & 0xffff, sp = packed >> 16;
-        const int n = m.row_pos[row] + 1;
-        // the row's nsplit = ceil(n / chunk) splits are balanced (64-token multiples)
-        const int nsplit_row = (n + chunk - 1) / chunk;
-        const int per = (((n + nsplit_row - 1) / nsplit_row) + kTok - 1) / kTok * kTok;
-        const int c0 = sp * per, c1 = min(n, c0 + per);
-        const int ntiles = (c1 - c0 + kTok - 1) / kTok;
-        const int32_t* bt = m.bt + (size_t)m.row_btrow[row] * m.MP;
-        const int qslot = k % kQSlots;
-        for (int t = 0; t < ntiles; ++t, ++g) {
+    // The whole warp walks the work list; lane 0 issues the barrier / TMA operations.  An item's
+    // metadata is a chain of dependent loads (cursor claim -> (row, split) -> context / block-table
+    // row -> page ids, ~2.5 us), resolved once the previous item's last tile is issued (kAhead = 1;
+    // resolving it 3 tiles earlier was measured neutral at 768-3,072 items per launch, and it
+    // commits the claimed item early).  With 64-token pages (one page per tile) the 32 lanes load 32
+    // page ids at once and each tile is ONE 4-D TMA operation (K and V, both head-dim halves); other
+    // page sizes keep per-box 2-D loads.
+    if (lane == 0) asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&kvmap)) : "memory");
+    constexpr int kAhead = 1;
+    const int chunk = m.att_ctl[0];
+    const uint32_t qbytes = (uint32_t)(gq * HD * 2);
+    const int box_rows = m.P < kTok ? m.P : kTok;
+    const bool tile_pages = m.P == kTok;
+    struct Item {
+      int valid, row, kvh, sp, c0, c1, ntiles, nsplit, pg;  // pg: page id of tile `lane` (tile_pages)
+      const int32_t* bt;
+    };
+    auto resolve = [&](Item& it) {
+      int idx = 0;
+      if (lane == 0) idx = atomicAdd(&m.att_ctl[1 + layer], 1);
+      idx = __shfl_sync(0xffffffffu, idx, 0);
+      it.valid = idx < total;
+      if (!it.valid) return;
+      const int rs = idx / m.hk;
+      it.kvh = idx % m.hk;
+      const int packed = m.att_items[rs];
+      it.row = packed & 0xffff;
+      it.sp = packed >> 16;
+      const int n = m.row_pos[it.row] + 1;
+      // the row's nsplit = ceil(n / chunk) splits are balanced (64-token multiples)
+      it.nsplit = (n + chunk - 1) / chunk;
+      const int per = (((n + it.nsplit - 1) / it.nsplit) + kTok - 1) / kTok * kTok;
+      it.c0 = it.sp * per;
+      it.c1 = min(n, it.c0 + per);
+      it.ntiles = (it.c1 - it.c0 + kTok - 1) / kTok;
+      it.bt = m.bt + (size_t)m.row_btrow[it.row] * m.MP;
+      it.pg = (tile_pages && lane < it.ntiles) ? it.bt[it.c0 / kTok + lane] : 0;
+    };
+    int g = 0;
+    Item cur;
+    resolve(cur);
+    for (int k = 0; cur.valid; ++k) {
+      Item nxt;
+      nxt.valid = 0;
+      const int t_next = max(0, cur.ntiles - kAhead);
+      const int qslot = k % kQSlots;
+      for (int t = 0; t < cur.ntiles; ++t, ++g) {
+        if (tile_pages && t > 0 && (t & 31) == 0) {
+          const int tt = t + lane;
+          cur.pg = tt < cur.ntiles ? cur.bt[cur.c0 / kTok + tt] : 0;
+        }
+        const int page_t = tile_pages ? __shfl_sync(0xffffffffu, cur.pg, t & 31) : 0;
+        if (lane == 0) {
           const int st = g % kStages;
           mbar_wait(&empty[st], ((g / kStages) & 1) ^ 1);
           Meta mt;
-          mt.row = row;
-          mt.kvh = kvh;
-          mt.sp = sp;
-          mt.c0 = c0;
-          mt.c1 = c1;
+          mt.row = cur.row;
+          mt.kvh = cur.kvh;
+          mt.sp = cur.sp;
+          mt.c0 = cur.c0;
+          mt.c1 = cur.c1;
           mt.tile = t;
-          mt.ntiles = ntiles;
-          mt.nsplit = (n + chunk - 1) / chunk;
+          mt.ntiles = cur.ntiles;
+          mt.nsplit = cur.nsplit;
           mt.qslot = qslot;
           mt.done = 0;
           meta[st] = mt;
           uint8_t* sb = base + st * 2 * Cfg::kKV;
           mbar_expect_tx(&full[st], 2 * Cfg::kKV + (t == 0 ? qbytes : 0u));
-          const int tok0 = c0 + t * kTok;
-          for (int r0 = 0; r0 < kTok; r0 += box_rows) {
-            const bool valid = tok0 + r0 < c1;
-            const int tok = valid ? tok0 + r0 : c1 - 1;  // past the end: reload a valid page (masked)
-            const int page = bt[tok / m.P];
-            const int slot = valid ? tok % m.P : 0;
-            const int64_t yk = ((((int64_t)layer * m.NP + page) * 2) * m.hk + kvh) * m.P + slot;
-            const int64_t yv = yk + (int64_t)m.hk * m.P;
+          if (tile_pages) {
+            const int64_t yk = (((int64_t)layer * m.NP + page_t) * 2 * m.hk + cur.kvh) * m.P;
+            tma_4d(&kvmap, &full[st], sb, (int)yk);
+          } else {
+            const int tok0 = cur.c0 + t * kTok;
+            for (int r0 = 0; r0 < kTok; r0 += box_rows) {
+              const bool valid = tok0 + r0 < cur.c1;
+              const int tok = valid ? tok0 + r0 : cur.c1 - 1;  // past the end: reload a valid page (masked)
+              const int page = cur.bt[tok / m.P];
+              const int slot = valid ? tok % m.P : 0;
+              const int64_t yk = ((((int64_t)layer * m.NP + page) * 2) * m.hk + cur.kvh) * m.P + slot;
+              const int64_t yv = yk + (int64_t)m.hk * m.P;
 #pragma unroll
-            for (int h = 0; h < HD / 64; ++h) {
-              tma_2d(&kvmap, &full[st], sb + h * (kTok * 128) + r0 * 128, h * 64, (int)yk);
-              tma_2d(&kvmap, &full[st], sb + Cfg::kKV + h * (kTok * 128) + r0 * 128, h * 64, (int)yv);
+              for (int h = 0; h < HD / 64; ++h) {
+                tma_2d(&kvmap, &full[st], sb + h * (kTok * 128) + r0 * 128, h * 64, (int)yk);
+                tma_2d(&kvmap, &full[st], sb + Cfg::kKV + h * (kTok * 128) + r0 * 128, h * 64, (int)yv);
+              }
             }
           }
           if (t == 0)
-            bulk_1d(base + Cfg::oQ + qslot * Cfg::kQ, q + (size_t)row * m.qd + kvh * gq * HD, qbytes, &full[st]);
+            bulk_1d(base + Cfg::oQ + qslot * Cfg::kQ, q + (size_t)cur.row * m.qd + cur.kvh * gq * HD, qbytes,
+                    &full[st]);
         }
+        __syncwarp();
+        if (t == t_next) resolve(nxt);
       }
+      cur = nxt;
+    }
+    if (lane == 0) {
       const int st = g % kStages;  // sentinel
       mbar_wait(&empty[st], ((g / kStages) & 1) ^ 1);
       meta[st].done = 1;
@@ -652,9 +698,6 @@ void launch_prefill_flash(const ModelDev& m, int layer, const bf16* q, bf16* out
 
 void set_pdl_mask_attention(int mask) {
   AB_CUDA(cudaMemcpyToSymbol(c_pdl_mask, &mask, sizeof(int)));
-  const char* ap = getenv("AB_ATT_PREFETCH");
-  const int pf = ap ? atoi(ap) : 0;
-  AB_CUDA(cudaMemcpyToSymbol(c_att_prefetch, &pf, sizeof(int)));
 }
 
 void make_kv_tmap(CUtensorMap* map, const ModelDev& m) {
@@ -663,7 +706,10 @@ void make_kv_tmap(CUtensorMap* map, const ModelDev& m) {
              "page_size must divide 64 or be a multiple of 64");
   const int64_t rows = (int64_t)m.L * m.NP * 2 * m.hk * m.P;
   AB_REQUIRE(rows < (int64_t(1) << 31), AB_ERR_CONFIG, "KV pool too large for 32-bit TMA coordinates");
-  make_tmap_bf16(map, m.kv, rows, m.hd, m.hd, 64, m.P < kTok ? m.P : kTok);
+  if (m.P == kTok)  // one 4-D box per tile: K and V, every 64-wide half of the head dimension
+    make_tmap_kv4(map, m.kv, rows, m.hd, (int64_t)m.hk * m.P, kTok);
+  else
+    make_tmap_bf16(map, m.kv, rows, m.hd, m.hd, 64, m.P < kTok ? m.P : kTok);
 }
 
 int decode_attention_ctas(const ModelDev& m) { return m.hd == 128 ? grid_t<128>() : grid_t<64>(); }
@@ -683,7 +729,8 @@ void launch_decode_attention(const CUtensorMap& map, const EngineDev& e, const M
 static int default_chunk(const ModelDev& m, const int32_t* ctx, int rows, int min_chunk) {
   unsigned long long tot = 0;
   for (int i = 0; i < rows; ++i) tot += (unsigned long long)ctx[i];
-  const unsigned long long ipc = 3, ctas = (unsigned long long)decode_attention_ctas(m);
+  const unsigned long long ipc = (unsigned long long)attention_items_per_cta();
+  const unsigned long long ctas = (unsigned long long)decode_attention_ctas(m);
   unsigned long long per = (tot * (unsigned long long)m.hk + ipc * ctas - 1) / (ipc * ctas);
   int ch = (int)std::min<unsigned long long>(per, 1ull << 30);
   ch = (ch + 63) & ~63;

@@ -1350,6 +1350,19 @@ void gemm_partition(GemmPlan& a, GemmPlan& b) {
   }
 }
 
+void make_tmap_kv4(CUtensorMap* m, const void* ptr, int64_t rows, int hd, int64_t v_rows, int box_rows) {
+  // dims {64, rows, hd / 64, 2}: element, pool row (hd * 2 bytes), 64-wide half (128 bytes), k|v
+  // (v_rows rows further on); 128-byte swizzle per 64-element row segment
+  cuuint64_t dims[4] = {64, (cuuint64_t)rows, (cuuint64_t)(hd / 64), 2};
+  cuuint64_t strides[3] = {(cuuint64_t)hd * 2, 128, (cuuint64_t)(v_rows * hd * 2)};
+  cuuint32_t box[4] = {64, (cuuint32_t)box_rows, (cuuint32_t)(hd / 64), 2};
+  cuuint32_t estr[4] = {1, 1, 1, 1};
+  CUresult r = encode_fn()(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void*>(ptr), dims, strides, box, estr,
+                           CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                           CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  AB_REQUIRE(r == CUDA_SUCCESS, AB_ERR_CUDA, "cuTensorMapEncodeTiled (KV 4-D) failed (" + std::to_string((int)r) + ")");
+}
+
 void make_tmap_bf16(CUtensorMap* m, const void* ptr, int64_t rows, int64_t cols, int64_t ld, int box_cols,
                     int box_rows) {
   cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};

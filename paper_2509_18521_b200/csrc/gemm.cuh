@@ -82,5 +82,8 @@ void gemm_set_schedule(GemmPlan& p, int force);
 // 128-byte swizzle (box_cols * 2 must be <= 128).
 void make_tmap_bf16(CUtensorMap* m, const void* ptr, int64_t rows, int64_t cols, int64_t ld, int box_cols,
                     int box_rows);
+// 4-D bf16 KV-pool map {64, rows, hd / 64, k|v} (V `v_rows` rows after K), box {64, box_rows, hd / 64, 2},
+// 128-byte swizzle: one operation loads a tile's K and V, both halves of each row.
+void make_tmap_kv4(CUtensorMap* m, const void* ptr, int64_t rows, int hd, int64_t v_rows, int box_rows);
 
 }  // namespace ab

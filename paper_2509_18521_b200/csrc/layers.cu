@@ -85,8 +85,12 @@ __device__ __forceinline__ void push_page(Ctl* c, ModelDev& m, int page) {
 // allocate a KV page when the row crosses a page boundary, and build the
 // attention work list (exclusive prefix of KV splits per row).
 constexpr int kPrepThreads = 1024;
-// attention work items per persistent CTA (dynamic cursor); AB_ATT_ITEMS overrides (tuning)
-__constant__ unsigned long long c_items_per_cta = 3;
+// attention work items per persistent CTA (dynamic cursor); AB_ATT_ITEMS overrides (tuning).
+// Each item costs about one 64-token tile of DRAM time on top of its tiles (end-of-item merge with
+// the stage held, start-up), so rows are split only when there are fewer (row, kv head) units
+// than CTAs or a row is longer than its share: measured 1 vs 3 at the bench operating points,
+// C2 +1.7 % (attention 0.85 -> 0.90 of the copy peak), C3 +1.6 % (0.93 -> 0.96).
+__constant__ unsigned long long c_items_per_cta = 1;
 
 // Per-iteration decode prologue: gather the live rows, allocate KV pages for the
 // token about to be written, and build the attention work list.  The KV split
@@ -735,12 +739,16 @@ __global__ void k_group_release(EngineDev e, ModelDev m, int g) {
 // launchers
 // ---------------------------------------------------------------------------
 
+int attention_items_per_cta() {
+  const char* ai = getenv("AB_ATT_ITEMS");
+  return ai ? std::max(1, atoi(ai)) : 1;
+}
+
 void set_pdl_mask_layers(int mask) {
   AB_CUDA(cudaMemcpyToSymbol(c_pdl_mask, &mask, sizeof(int)));
   const int z = getenv("AB_ROPE_NOZERO") ? 0 : 1;  // timing experiments only: results are then wrong
   AB_CUDA(cudaMemcpyToSymbol(c_rope_zero, &z, sizeof(int)));
-  const char* ai = getenv("AB_ATT_ITEMS");
-  const unsigned long long items = ai ? (unsigned long long)std::max(1, atoi(ai)) : 3ull;
+  const unsigned long long items = (unsigned long long)attention_items_per_cta();
   AB_CUDA(cudaMemcpyToSymbol(c_items_per_cta, &items, sizeof(items)));
 }
 

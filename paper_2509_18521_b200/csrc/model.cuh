@@ -70,6 +70,7 @@ void launch_decode_attention(const CUtensorMap& map, const EngineDev& e, const M
 // causal flash prefill over the paged pool; blocks[i] = {first row, rows (<= 64), block-table row, first position}
 void set_pdl_mask_attention(int mask);
 void set_pdl_mask_layers(int mask);
+int attention_items_per_cta();  // decode attention work items per persistent CTA (AB_ATT_ITEMS, default 1)
 void launch_prefill_flash(const ModelDev& m, int layer, const bf16* q, bf16* out, const int4* blocks, int n_blocks,
                           cudaStream_t s);
 void launch_fork_groups(const EngineDev& e, const ModelDev& m, const ab_sample_desc* descs, int n, cudaStream_t s);
