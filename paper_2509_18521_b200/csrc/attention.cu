@@ -4,15 +4,17 @@
 // writes the (row, split) list each iteration; a persistent grid (2 CTAs per
 // SM) walks it.  Warp 4 is the producer: running up to kStages tiles ahead on
 // empty/full mbarriers, it issues per 64-token tile cp.async.bulk.tensor
-// loads of the kv head's K and V rows straight out of the paged pool (2-D
-// tensor map over kv[layer][page][k|v][head][slot][dim], 128-byte swizzle),
+// loads of the kv head's K and V rows straight out of the paged pool (one 4-D
+// box per tile with 64-token pages, else 2-D boxes; tensor map over
+// kv[layer][page][k|v][head][slot][dim], 128-byte swizzle),
 // plus on an item's first tile a 1-D bulk copy of the GQA group's q rows, and
 // hands the item's metadata to the consumers through shared memory (all
 // global-memory latency of the work list lives in the producer).  Warps 0-3
 // consume: each owns 16 tokens of a tile, S = Q K^T and O += P V as mma.sync
 // m16n8k16 bf16 tiles with the q heads as the 16-row M side
 // (flash-attention-2 register layout, exp2 online softmax).  At an item's
-// end the 4 warps merge in a fixed order; rows with one split write the
+// end the stage goes back to the producer and the 4 warps merge pairwise in
+// a fixed order through a small buffer; rows with one split write the
 // output directly, multi-split rows are merged in split order by the last
 // CTA to finish (arrival counter, self-resetting): deterministic end to end.
 #include <cuda.h>
@@ -49,9 +51,12 @@ struct AttCfg {
   static constexpr int kQ = kMergeRows * HD * 2;
   static constexpr int oQ = kStages * 2 * kKV;
   static constexpr int oZero = oQ + kQSlots * kQ;
-  static constexpr int oML = oZero + HD * 2;                       // [kCons][kMergeRows] (m, l)
-  static constexpr int oMLs = oML + kCons * kMergeRows * 8;        // [kMergeRows][kMaxSplits] split (m, l)
-  static constexpr int oMeta = oMLs + kMergeRows * kMaxSplits * 8;
+  // end-of-item merge buffer: [2][kMergeRows][HD] fp32 + [2][kMergeRows] (m, l); the split combine's
+  // [kMergeRows][kMaxSplits] (m, l) aliases it (used only after the merge)
+  static constexpr int kMB = 2 * kMergeRows * HD * 4 + 2 * kMergeRows * 8;
+  static constexpr int oMB = oZero + HD * 2;
+  static constexpr int oMLs = oMB;
+  static constexpr int oMeta = oMB + (kMB > kMergeRows * kMaxSplits * 8 ? kMB : kMergeRows * kMaxSplits * 8);
   static constexpr int oBar = oMeta + kStages * (int)sizeof(Meta);
   static constexpr int kSmem = 1024 + oBar + 2 * kStages * 8;
   // the 4 consumer warps' unscaled outputs are merged in the K half of the item's last stage
@@ -149,7 +154,6 @@ __global__ void __launch_bounds__(kThreads, 2)
 
   extern __shared__ uint8_t smem_raw[];
   uint8_t* base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  float2* sML = reinterpret_cast<float2*>(base + Cfg::oML);    // [kCons][kMergeRows]
   float2* sMLs = reinterpret_cast<float2*>(base + Cfg::oMLs);  // [kMergeRows][kMaxSplits]
   Meta* meta = reinterpret_cast<Meta*>(base + Cfg::oMeta);
   uint64_t* full = reinterpret_cast<uint64_t*>(base + Cfg::oBar);
@@ -360,62 +364,75 @@ __global__ void __launch_bounds__(kThreads, 2)
       mma16816(o[2 * nt2 + 1], pa, bb[2], bb[3]);
     }
     __syncwarp();
-    if (mt.tile != mt.ntiles - 1) {
-      if (lane == 0) mbar_arrive(&empty[st]);  // this warp is done with the stage
-      continue;
-    }
+    if (lane == 0) mbar_arrive(&empty[st]);  // this warp is done with the stage (the last one too)
+    if (mt.tile != mt.ntiles - 1) continue;
 
-    // ---- item complete: the item's last stage stays claimed; its K half holds the
-    // 4 warps' unscaled outputs, merged in one pass (fixed warp order: deterministic) ----
+    // ---- item complete: merge the 4 warps' unscaled outputs pairwise in fixed order (1 -> 0,
+    // 3 -> 2, then 2 -> 0: deterministic) through a small dedicated buffer, so the item's last
+    // stage has already gone back to the producer.  (Merging inside the held stage kept the ring at
+    // two tiles in flight during every merge: ~1.2 us of CTA DRAM time per item, measured by
+    // skipping the merge; a separate merge warp holding the stage longer was slower still.) ----
 #pragma unroll
     for (int r = 0; r < 2; ++r) {
       lrow[r] += __shfl_xor_sync(0xffffffffu, lrow[r], 1);
       lrow[r] += __shfl_xor_sync(0xffffffffu, lrow[r], 2);
     }
-    float* sO = reinterpret_cast<float*>(base + st * 2 * Cfg::kKV);  // [kCons][kMergeRows][HD]
-    cons_sync();  // every warp is done reading this stage's K / V
-    if (gr < gq) {
-      float* dst = sO + (warp * kMergeRows + gr) * HD;
+    float* bO = reinterpret_cast<float*>(base + Cfg::oMB);                        // [2][kMergeRows][HD]
+    float2* bML = reinterpret_cast<float2*>(base + Cfg::oMB + 2 * kMergeRows * HD * 4);  // [2][kMergeRows]
+    auto put = [&](int slot) {
+      if (gr < gq) {
+        float* dst = bO + (slot * kMergeRows + gr) * HD;
 #pragma unroll
-      for (int nt = 0; nt < HD / 8; ++nt)
-        *reinterpret_cast<float2*>(dst + nt * 8 + tq * 2) = make_float2(o[nt][0], o[nt][1]);
-      if (tq == 0) sML[warp * kMergeRows + gr] = make_float2(mrow[0], lrow[0]);
-    }
+        for (int nt = 0; nt < HD / 8; ++nt)
+          *reinterpret_cast<float2*>(dst + nt * 8 + tq * 2) = make_float2(o[nt][0], o[nt][1]);
+        if (tq == 0) bML[slot * kMergeRows + gr] = make_float2(mrow[0], lrow[0]);
+      }
+    };
+    auto take = [&](int slot) {
+      if (gr < gq) {
+        const float2 ml = bML[slot * kMergeRows + gr];
+        const float M = fmaxf(mrow[0], ml.x);
+        const float a = mrow[0] == -FLT_MAX ? 0.f : exp2f(mrow[0] - M);
+        const float bw = ml.x == -FLT_MAX ? 0.f : exp2f(ml.x - M);
+        const float* src = bO + (slot * kMergeRows + gr) * HD;
+#pragma unroll
+        for (int nt = 0; nt < HD / 8; ++nt) {
+          const float2 v = *reinterpret_cast<const float2*>(src + nt * 8 + tq * 2);
+          o[nt][0] = o[nt][0] * a + v.x * bw;
+          o[nt][1] = o[nt][1] * a + v.y * bw;
+        }
+        mrow[0] = M;
+        lrow[0] = lrow[0] * a + ml.y * bw;
+      }
+    };
+    cons_sync();  // the previous item's readers of the buffer are done
+    if (warp & 1) put(warp >> 1);
+    cons_sync();
+    if (!(warp & 1)) take(warp >> 1);
+    cons_sync();
+    if (warp == 2) put(0);
     cons_sync();
     const int i = mt.row, kvh = mt.kvh, sp = mt.sp, nsplit = mt.nsplit;
-    for (int idx = tid; idx < gq * (HD / 4); idx += kCons * 32) {
-      const int row = idx / (HD / 4), d4 = idx % (HD / 4);
-      float M = -FLT_MAX;
+    if (warp == 0) {
+      take(0);
+      if (gr < gq) {  // warp 0 holds the item's output rows
+        const int head = kvh * gq + gr;
+        if (nsplit == 1) {
+          const float inv = 1.f / lrow[0];
+          __nv_bfloat16* dst = out + (size_t)i * m.qd + head * HD + tq * 2;
 #pragma unroll
-      for (int w = 0; w < kCons; ++w) M = fmaxf(M, sML[w * kMergeRows + row].x);
-      float L = 0.f;
-      float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+          for (int nt = 0; nt < HD / 8; ++nt)
+            *reinterpret_cast<uint32_t*>(dst + nt * 8) = pack_bf16(o[nt][0] * inv, o[nt][1] * inv);
+        } else {
+          const size_t pb = ((size_t)i * m.hq + head) * max_splits + sp;
 #pragma unroll
-      for (int w = 0; w < kCons; ++w) {
-        const float2 ml = sML[w * kMergeRows + row];
-        const float wgt = ml.x == -FLT_MAX ? 0.f : exp2f(ml.x - M);
-        L += ml.y * wgt;
-        const float4 v = *reinterpret_cast<const float4*>(sO + (w * kMergeRows + row) * HD + d4 * 4);
-        acc.x += v.x * wgt;
-        acc.y += v.y * wgt;
-        acc.z += v.z * wgt;
-        acc.w += v.w * wgt;
+          for (int nt = 0; nt < HD / 8; ++nt)
+            *reinterpret_cast<float2*>(part_o + pb * HD + nt * 8 + tq * 2) = make_float2(o[nt][0], o[nt][1]);
+          if (tq == 0) *reinterpret_cast<float2*>(part_ml + pb * 2) = make_float2(mrow[0], lrow[0]);
+        }
       }
-      const int head = kvh * gq + row;
-      if (nsplit == 1) {
-        const float inv = 1.f / L;
-        uint2 w2;
-        w2.x = pack_bf16(acc.x * inv, acc.y * inv);
-        w2.y = pack_bf16(acc.z * inv, acc.w * inv);
-        *reinterpret_cast<uint2*>(out + (size_t)i * m.qd + head * HD + d4 * 4) = w2;
-      } else {
-        const size_t pb = ((size_t)i * m.hq + head) * max_splits + sp;
-        *reinterpret_cast<float4*>(part_o + pb * HD + d4 * 4) = acc;
-        if (d4 == 0) *reinterpret_cast<float2*>(part_ml + pb * 2) = make_float2(M, L);
-      }
+      __syncwarp();
     }
-    cons_sync();  // merge reads of the stage are done: hand it back to the producer
-    if (lane == 0) mbar_arrive(&empty[st]);
     if (nsplit > 1) {
       // split combine by the last CTA to finish a split of this (row, kv head): split order, deterministic
       if (tid == 0) {
@@ -428,7 +445,7 @@ __global__ void __launch_bounds__(kThreads, 2)
         }
         s_last = last;
       }
-      cons_sync();
+      cons_sync();  // (also: warp 0 is done with the merge buffer, which sMLs aliases)
       if (s_last) {
         for (int idx = tid; idx < gq * nsplit; idx += kCons * 32) {
           const int row = idx / nsplit, s2 = idx % nsplit;
