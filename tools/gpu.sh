@@ -48,7 +48,7 @@ case "$MODE" in
         > gpurun_out/sanitize_${tool}_engine.log 2>&1
       echo "rc=$?" >> gpurun_out/sanitize_${tool}_engine.log
     done
-    tail -3 gpurun_out/sanitize_*.log ;;
+    tail -n 3 gpurun_out/sanitize_*.log ;;
   forcedp)
     # the lockstep DP wrapper at world 1 must make the plain engine's decisions (same iterations and
     # carried tokens per step): two short bench runs, decisions compared by tools/compare_forcedp.py
