@@ -8,6 +8,7 @@
 #   launches B CTX [preset]  ncu launch list (gpu__time_duration) of decode iterations at (batch, ctx)
 #   ncu_attn B CTX           ncu --set full of the decode attention kernel
 #   sanitize                 compute-sanitizer racecheck + memcheck on the engine / attention tests
+#                            (closed on the GPU pool since round 2 session 3)
 #   forcedp [bench args]     plain vs --force-dp (world-1 lockstep wrapper) decisions, compared
 #   dp2 [bench args]         bench.py at world 2 on one GPU (gloo host collectives, IPC exchange)
 set -u
