@@ -59,8 +59,8 @@ struct AttCfg {
   static constexpr int oMeta = oMB + (kMB > kMergeRows * kMaxSplits * 8 ? kMB : kMergeRows * kMaxSplits * 8);
   static constexpr int oBar = oMeta + kStages * (int)sizeof(Meta);
   static constexpr int kSmem = 1024 + oBar + 2 * kStages * 8;
-  // the 4 consumer warps' unscaled outputs are merged in the K half of the item's last stage
-  static_assert(kCons * kMergeRows * HD * 4 <= kKV, "merge buffer must fit in a K tile");
+  // two CTAs per SM: 228 KB of shared memory, 1 KB reserved per CTA
+  static_assert(2 * (kSmem + 1024) <= 228 * 1024, "decode attention must fit two CTAs per SM");
 };
 
 __device__ __forceinline__ uint32_t su32(const void* p) { return static_cast<uint32_t>(__cvta_generic_to_shared(p)); }
